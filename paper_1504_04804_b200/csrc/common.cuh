@@ -1,0 +1,177 @@
+// common.cuh — CUDA plumbing shared by every translation unit of the engine:
+// error handling (status codes of include/mgraph_b200.h), launch accounting,
+// warp-aggregated queue appends and the policy-aware device buffer that
+// re-states the reference's CapVector/MemoryBudget (frontier.hpp:63-187).
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <atomic>
+#include <cstdint>
+#include <string>
+#include <vector>
+
+#include "host_graph.hpp"
+#include "mgraph_b200.h"
+
+namespace mgb {
+
+constexpr uint32_t kInfLabel = 0xFFFFFFFFu;
+constexpr uint64_t kInfDist = 0xFFFFFFFFFFFFFFFFull;
+constexpr int kMaxWorkers = 64;
+constexpr int kMaxAssoc = 2;  // vertex / value associates per record (reference allows 8)
+constexpr int kNumSMs = 148;
+
+extern std::atomic<uint64_t> g_launches;
+
+#define MGB_CUDA(call)                                                                    \
+  do {                                                                                    \
+    cudaError_t _e = (call);                                                              \
+    if (_e != cudaSuccess)                                                                \
+      throw ::mgb::Error(MG_ECUDA, std::string(#call) + ": " + cudaGetErrorString(_e));   \
+  } while (0)
+
+// every kernel launch goes through here so gpu_launches is an exact count
+#define MGB_LAUNCH(kernel, grid, block, smem, stream, ...)                               \
+  do {                                                                                    \
+    kernel<<<(grid), (block), (smem), (stream)>>>(__VA_ARGS__);                           \
+    ::mgb::g_launches.fetch_add(1, std::memory_order_relaxed);                            \
+    MGB_CUDA(cudaGetLastError());                                                         \
+  } while (0)
+
+inline unsigned grid_for(uint64_t items, unsigned per_block, unsigned cap = kNumSMs * 8) {
+  uint64_t g = (items + per_block - 1) / per_block;
+  if (g < 1) g = 1;
+  if (g > cap) g = cap;
+  return static_cast<unsigned>(g);
+}
+
+// ---------------------------------------------------------------------------
+// device helpers
+
+__device__ __forceinline__ unsigned lane_id() { return threadIdx.x & 31u; }
+
+// Warp-aggregated append: every active lane with `pred` gets a slot in the
+// queue; one atomicAdd per warp.  Returns the slot or 0xFFFFFFFF.
+__device__ __forceinline__ uint32_t warp_append(uint32_t* counter, bool pred) {
+  unsigned active = __activemask();
+  unsigned mask = __ballot_sync(active, pred);
+  if (!pred) return 0xFFFFFFFFu;
+  unsigned leader = __ffs(mask) - 1;
+  uint32_t base = 0;
+  if (lane_id() == leader) base = atomicAdd(counter, (uint32_t)__popc(mask));
+  base = __shfl_sync(mask, base, leader);
+  return base + __popc(mask & ((1u << lane_id()) - 1u));
+}
+
+__device__ __forceinline__ void warp_add_u64(unsigned long long* counter, uint64_t v) {
+  unsigned active = __activemask();
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(active, v, o);
+  // lanes outside `active` contributed nothing; the lowest active lane adds
+  if (lane_id() == (unsigned)(__ffs(active) - 1)) atomicAdd(counter, (unsigned long long)v);
+}
+
+// ---------------------------------------------------------------------------
+// policy-aware device buffer (CapVector + BufferStats + MemoryBudget)
+
+struct BufferStats {  // frontier.hpp:71-81
+  uint64_t realloc_count = 0, peak_items = 0, peak_bytes = 0;
+  void merge(const BufferStats& o) {
+    realloc_count += o.realloc_count;
+    peak_items = peak_items > o.peak_items ? peak_items : o.peak_items;
+    peak_bytes = peak_bytes > o.peak_bytes ? peak_bytes : o.peak_bytes;
+  }
+};
+
+struct MemoryBudget {  // frontier.hpp:86-104
+  uint64_t allocated = 0, peak = 0, hard_cap = 0;
+  void charge(uint64_t add, uint64_t release) {
+    allocated = allocated + add - release;
+    if (allocated > peak) peak = allocated;
+    if (hard_cap && allocated > hard_cap)
+      throw Error(MG_ECAPACITY, "worker memory cap exceeded: need " + std::to_string(allocated) +
+                                    " bytes, cap " + std::to_string(hard_cap) +
+                                    " (graph does not fit under this budget)");
+  }
+};
+
+// Device array with exact ("just-enough") growth: capacity extends to exactly
+// the requested size, never speculatively; prealloc() is the policy's up-front
+// sizing and is not counted as a reallocation (frontier.hpp:109-187).
+template <class T>
+struct DevBuf {
+  T* ptr = nullptr;
+  uint64_t cap = 0;
+  BufferStats* stats = nullptr;
+  MemoryBudget* budget = nullptr;
+
+  void attach(BufferStats* s, MemoryBudget* b) {
+    stats = s;
+    budget = b;
+  }
+  void release() {
+    if (ptr) cudaFree(ptr);
+    if (budget && cap) budget->allocated -= cap * sizeof(T);
+    ptr = nullptr;
+    cap = 0;
+  }
+  // grow to exactly `items`; contents up to `keep` items are preserved
+  void grow(uint64_t items, bool counted, uint64_t keep, cudaStream_t s) {
+    if (budget) budget->charge(items * sizeof(T), cap * sizeof(T));
+    T* np = nullptr;
+    MGB_CUDA(cudaMalloc(&np, items * sizeof(T) + 16));
+    if (ptr) {
+      if (keep) MGB_CUDA(cudaMemcpyAsync(np, ptr, keep * sizeof(T), cudaMemcpyDeviceToDevice, s));
+      MGB_CUDA(cudaStreamSynchronize(s));
+      cudaFree(ptr);
+    }
+    ptr = np;
+    cap = items;
+    if (stats) {
+      if (counted) ++stats->realloc_count;
+      if (cap > stats->peak_items) stats->peak_items = cap;
+      if (cap * sizeof(T) > stats->peak_bytes) stats->peak_bytes = cap * sizeof(T);
+    }
+  }
+  void prealloc(uint64_t items, cudaStream_t s) {
+    if (items > cap) grow(items, false, 0, s);
+  }
+  void ensure(uint64_t items, cudaStream_t s, uint64_t keep = 0) {
+    if (items > cap) grow(items, true, keep, s);
+  }
+};
+
+// plain owned device array (graph data, per-run state): no policy accounting
+template <class T>
+struct DevArray {
+  T* ptr = nullptr;
+  uint64_t n = 0;
+  void alloc(uint64_t count) {
+    free_();
+    n = count;
+    if (count) MGB_CUDA(cudaMalloc(&ptr, count * sizeof(T) + 16));
+  }
+  void free_() {
+    if (ptr) cudaFree(ptr);
+    ptr = nullptr;
+    n = 0;
+  }
+  void upload(const T* h, uint64_t count, cudaStream_t s) {
+    alloc(count);
+    if (count) MGB_CUDA(cudaMemcpyAsync(ptr, h, count * sizeof(T), cudaMemcpyHostToDevice, s));
+  }
+};
+
+struct DeviceGuard {
+  int prev = 0;
+  explicit DeviceGuard(int dev) {
+    cudaGetDevice(&prev);
+    if (dev != prev) cudaSetDevice(dev);
+  }
+  ~DeviceGuard() { cudaSetDevice(prev); }
+};
+
+void set_error(const std::string& msg);
+
+}  // namespace mgb

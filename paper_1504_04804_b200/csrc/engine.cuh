@@ -1,0 +1,530 @@
+// engine.cuh — the BSP superstep engine on B200 (reference run_primitive,
+// engine.hpp:712-981) as a host C++ enactor driving sm_100a kernels.
+//
+// Per superstep, for every worker (partition) p:
+//   body        primitive kernels (advance/filter/compute) -> output        (E:874-875)
+//   split+pack  one kernel: owner(v)==p -> next_input, else the record (id +
+//               gathered associates) is stored straight into the destination
+//               worker's inbox slot [parity][p] — a peer-HBM store over NVLink
+//               when the destination is another GPU                        (E:877-915)
+//   publish     per-destination record counts written into the peer's slot
+//               counters; an event orders them before the peer's merge      (E:361-391)
+//   merge       combine() every received record, enqueue once via the merge
+//               stamp                                                        (E:823-852)
+//   report      one D2H of the worker counters; the host reduces the
+//               WorkerReports into a GlobalView and applies the stop rule   (E:784-820)
+// Only the final report needs a host round trip: pack->merge ordering across
+// workers uses CUDA events (cudaStreamWaitEvent), not a host barrier.
+#pragma once
+
+#include <chrono>
+#include <cstring>
+#include <functional>
+#include <optional>
+
+#include "operators.cuh"
+
+namespace mgb {
+
+struct WorkerReport {  // engine.hpp:216-223
+  uint64_t out_frontier = 0, next_frontier = 0, edges_delta = 0, combine_delta = 0;
+  double f[4] = {0, 0, 0, 0};
+  uint64_t u[4] = {0, 0, 0, 0};
+};
+
+struct GlobalView {  // engine.hpp:225-253
+  uint32_t iteration = 0, num_workers = 1;
+  std::vector<WorkerReport> reports;
+  uint64_t total_out = 0, total_next = 0, inflight_records = 0;
+  double sum_f(int k) const {
+    double s = 0;
+    for (auto& r : reports) s += r.f[k];
+    return s;
+  }
+  double max_f(int k) const {
+    double s = 0;
+    for (auto& r : reports) s = s > r.f[k] ? s : r.f[k];
+    return s;
+  }
+  uint64_t max_u(int k) const {
+    uint64_t s = 0;
+    for (auto& r : reports) s = s > r.u[k] ? s : r.u[k];
+    return s;
+  }
+  bool all_u_equal(int k, uint64_t v) const {
+    for (auto& r : reports)
+      if (r.u[k] != v) return false;
+    return true;
+  }
+};
+
+// ---------------------------------------------------------------------------
+// split + pack: route every output vertex (engine.hpp:880-909) and store the
+// remote records directly into the destination inbox slot
+
+template <class F>
+__global__ void __launch_bounds__(256)
+    split_pack_kernel(F f, OwnerView ow, GraphView g, const uint32_t* __restrict__ out,
+                      Counters* ctr, uint32_t* __restrict__ next, const SlotView* __restrict__ table,
+                      uint32_t n, int broadcast, unsigned long long drop_mask, int nva, int nvv) {
+  const uint32_t cnt = ctr->out_cnt;
+  unsigned long long my_deg = 0;
+  for (uint32_t base = blockIdx.x * blockDim.x; base < cnt; base += gridDim.x * blockDim.x) {
+    uint32_t i = base + threadIdx.x;
+    bool local = false;
+    uint32_t v = 0, q = ow.p;
+    if (i < cnt) {
+      v = out[i];
+      q = broadcast ? ow.p : ow.owner_of_local(v);
+      local = (q == ow.p);
+    }
+    uint32_t slot = warp_append(&ctr->next_cnt, local);
+    if (local) {
+      next[slot] = v;
+      my_deg += g.off[v + 1] - g.off[v];
+    }
+    if (i >= cnt) continue;
+    if (broadcast) {
+      uint32_t va[kMaxAssoc];
+      double vv[kMaxAssoc];
+      f.gather(v, va, vv);
+      for (uint32_t d = 0; d < n; ++d) {
+        if (d == ow.p || ((drop_mask >> d) & 1ull)) continue;
+        uint32_t pos = atomicAdd(&ctr->send_cnt[d], 1u);
+        const SlotView& s = table[d];
+        if (pos >= s.cap) {
+          atomicExch(&ctr->overflow, 1u);
+          continue;
+        }
+        s.ids[pos] = v;
+        for (int a = 0; a < nva; ++a) s.va[a][pos] = va[a];
+        for (int a = 0; a < nvv; ++a) s.vv[a][pos] = vv[a];
+      }
+    } else if (!local && f.send_filter(q, v)) {
+      uint32_t va[kMaxAssoc];
+      double vv[kMaxAssoc];
+      f.gather(v, va, vv);
+      if ((drop_mask >> q) & 1ull) continue;
+      uint32_t pos = atomicAdd(&ctr->send_cnt[q], 1u);
+      const SlotView& s = table[q];
+      if (pos >= s.cap) {
+        atomicExch(&ctr->overflow, 1u);
+        continue;
+      }
+      s.ids[pos] = f.peer_id(v, q, i);
+      for (int a = 0; a < nva; ++a) s.va[a][pos] = va[a];
+      for (int a = 0; a < nvv; ++a) s.vv[a][pos] = vv[a];
+    }
+  }
+  warp_add_u64(&ctr->next_deg, my_deg);
+}
+
+// publish per-destination counts into the peers' slot counters; the system
+// fence makes the record stores visible before the count (P2P over NVLink)
+static __global__ void publish_kernel(const Counters* ctr, uint32_t* const* cnt_ptr, uint32_t n,
+                               uint32_t p) {
+  uint32_t d = threadIdx.x;
+  __threadfence_system();
+  if (d < n && d != p) *cnt_ptr[d] = ctr->send_cnt[d] < 0xFFFFFFFFu ? ctr->send_cnt[d] : 0u;
+}
+
+// merge (engine.hpp:823-852): combine every received record; an accepted
+// vertex is enqueued once per superstep through the merge stamp
+template <class F>
+__global__ void __launch_bounds__(256)
+    merge_kernel(F f, const SlotView* __restrict__ slots, const uint32_t* __restrict__ inbox_cnt,
+                 uint32_t p, uint32_t stamp, uint32_t iteration, uint32_t* merge_stamp,
+                 uint32_t* __restrict__ next, Counters* ctr, GraphView g, int nva, int nvv,
+                 int enqueue) {
+  const uint32_t src = blockIdx.y;
+  if (src == p) return;
+  const uint32_t cnt = inbox_cnt[src];
+  const SlotView s = slots[src];
+  if (threadIdx.x == 0 && blockIdx.x == 0) ctr->recv_cnt[src] = cnt;
+  unsigned long long my_deg = 0, my_comb = 0;
+  for (uint32_t base = blockIdx.x * blockDim.x; base < cnt; base += gridDim.x * blockDim.x) {
+    uint32_t i = base + threadIdx.x;
+    bool push = false;
+    uint32_t v = 0;
+    if (i < cnt) {
+      v = s.ids[i];
+      uint32_t va[kMaxAssoc];
+      double vv[kMaxAssoc];
+      for (int a = 0; a < nva; ++a) va[a] = s.va[a][i];
+      for (int a = 0; a < nvv; ++a) vv[a] = s.vv[a][i];
+      ++my_comb;
+      bool accepted = f.combine(v, va, vv, iteration);
+      if (accepted && enqueue) push = atomicExch(&merge_stamp[v], stamp) != stamp;
+    }
+    uint32_t slot = warp_append(&ctr->next_cnt, push);
+    if (push) {
+      next[slot] = v;
+      my_deg += g.off[v + 1] - g.off[v];
+    }
+  }
+  warp_add_u64(&ctr->next_deg, my_deg);
+  warp_add_u64(&ctr->combine, my_comb);
+}
+
+// degree sum of a frontier (init: the advance bound of superstep 0)
+static __global__ void degsum_kernel(GraphView g, const uint32_t* __restrict__ in, uint32_t n,
+                              unsigned long long* out) {
+  unsigned long long d = 0;
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    uint32_t v = in[i];
+    d += g.off[v + 1] - g.off[v];
+  }
+  warp_add_u64(out, d);
+}
+
+// ---------------------------------------------------------------------------
+// per-(run, worker) context: the WorkerHandle of the reference (engine.hpp:478-582)
+
+struct RunState;
+
+struct Ctx {
+  Plan* P = nullptr;
+  Worker* w = nullptr;
+  RunState* run = nullptr;
+  uint64_t iter = 0;
+  const GlobalView* prev = nullptr;
+  bool fused = false;
+  uint32_t in_count = 0;    // input frontier length (host-known)
+  uint64_t in_degsum = 0;   // sum of its out-degrees (host-known)
+  WorkerReport report;      // host-side f/u fields set by hooks
+
+  uint32_t worker() const { return w->p; }
+  uint32_t num_workers() const { return P->n; }
+  cudaStream_t stream() const { return w->stream; }
+  OwnerView owner_view() const {
+    return {w->owner.ptr, w->l2g.ptr, w->p, w->nlocal, P->dup};
+  }
+  GraphView graph() const { return w->graph(); }
+  Counters* ctr() const { return w->ctr.ptr; }
+
+  // seed the initial frontier (valid inside init only), E:511-514
+  void push_initial(const std::vector<uint32_t>& vs);
+
+  void ensure_output(uint64_t items) { w->output.ensure(items, w->stream); }
+
+  // advance over the input frontier (E:516-520)
+  template <class F>
+  void run_advance(const F& f, uint32_t* dst, uint32_t* dst_cnt) {
+    if (in_count == 0) return;
+    GraphView g = graph();
+    unsigned grid = grid_for(in_count, kAdvBlock, kNumSMs * 16);
+    MGB_LAUNCH((advance_chunk_kernel<F, false>), grid, kAdvBlock, 0, w->stream, f, g,
+               w->input.ptr, in_count, dst, dst_cnt, w->big.ptr, &ctr()->big_cnt, &ctr()->edges);
+    launch_big<F, false>(f, dst, dst_cnt);
+  }
+
+  template <class F, bool kFused>
+  void launch_big(const F& f, uint32_t* dst, uint32_t* dst_cnt) {
+    if (in_degsum <= kBigDegree) return;  // no vertex can exceed the threshold
+    GraphView g = graph();
+    MGB_LAUNCH(big_prefix_kernel, 1, 1024, 0, w->stream, g, w->input.ptr, w->big.ptr,
+               &ctr()->big_cnt, w->big_prefix.ptr);
+    unsigned grid = grid_for(in_degsum, kAdvBlock, kNumSMs * 8);
+    MGB_LAUNCH((advance_big_kernel<F, kFused>), grid, kAdvBlock, 0, w->stream, f, g,
+               w->input.ptr, w->big.ptr, &ctr()->big_cnt, w->big_prefix.ptr, dst, dst_cnt);
+  }
+
+  // fused or two-stage traversal per the active policy (E:528-541); the
+  // result lands in w->output with its length in ctr()->out_cnt
+  template <class F>
+  void pipeline(const F& f, uint64_t dedup_bound) {
+    if (fused) {
+      uint64_t b = in_degsum < dedup_bound ? in_degsum : dedup_bound;
+      ensure_output(b);
+      if (in_count == 0) return;
+      GraphView g = graph();
+      unsigned grid = grid_for(in_count, kAdvBlock, kNumSMs * 16);
+      MGB_LAUNCH((advance_chunk_kernel<F, true>), grid, kAdvBlock, 0, w->stream, f, g,
+                 w->input.ptr, in_count, w->output.ptr, &ctr()->out_cnt, w->big.ptr,
+                 &ctr()->big_cnt, &ctr()->edges);
+      launch_big<F, true>(f, w->output.ptr, &ctr()->out_cnt);
+    } else {
+      w->advance_out.ensure(in_degsum, w->stream);
+      run_advance(f, w->advance_out.ptr, &ctr()->adv_cnt);
+      // filter_output_bound(advance_out.size(), |V_i|) (frontier.hpp:204-208): the
+      // unfused path reads the advance length back to size the filter exactly
+      uint32_t adv = 0;
+      MGB_CUDA(cudaMemcpyAsync(&adv, &ctr()->adv_cnt, 4, cudaMemcpyDeviceToHost, w->stream));
+      MGB_CUDA(cudaStreamSynchronize(w->stream));
+      ensure_output(adv < dedup_bound ? adv : dedup_bound);
+      if (adv == 0) return;
+      MGB_LAUNCH(filter_kernel<F>, grid_for(adv, 256, kNumSMs * 8), 256, 0, w->stream, f,
+                 w->advance_out.ptr, &ctr()->adv_cnt, w->output.ptr, &ctr()->out_cnt);
+    }
+  }
+};
+
+struct RunState {
+  int comm = MG_COMM_SELECTIVE;
+  std::vector<GlobalView> views;
+  std::vector<uint32_t> in_count, next_count;
+  std::vector<uint64_t> in_deg, next_deg;
+  std::vector<cudaEvent_t> packed;  // per worker, recorded after publish
+};
+
+inline void Ctx::push_initial(const std::vector<uint32_t>& vs) {
+  uint32_t& nc = run->next_count[w->p];
+  w->next_input.ensure(nc + vs.size(), w->stream, nc);
+  if (!vs.empty())
+    MGB_CUDA(cudaMemcpyAsync(w->next_input.ptr + nc, vs.data(), vs.size() * 4,
+                             cudaMemcpyHostToDevice, w->stream));
+  MGB_CUDA(cudaStreamSynchronize(w->stream));  // vs is a host temporary
+  nc += static_cast<uint32_t>(vs.size());
+}
+
+// allocate / grow the receiver inbox arena of worker w for slot capacities caps[src]
+void ensure_inboxes(Plan& P, Worker& w, int nva, int nvv, const std::vector<uint64_t>& caps);
+// refresh every local worker's send tables (after any arena changed)
+void build_send_tables(Plan& P);
+void prepare_worker(Plan& P, Worker& w, const mg_config& cfg);
+void collect_buffer_stats(Plan& P);
+
+// ---------------------------------------------------------------------------
+// the enactor
+
+template <class Prim>
+void run_primitive(Plan& P, Prim& prim, const mg_config& cfg) {
+  const uint32_t n = P.n;
+  if (prim.dup_required >= 0 && P.dup != prim.dup_required)
+    throw Error(MG_EINVAL, std::string(prim.name) + ": requires --dup " +
+                               (prim.dup_required == MG_DUP_ALL ? "all" : "onehop"));
+  for (int r = 0; r < MG_NUM_ROLES; ++r)
+    if (cfg.factors[r] < 0.0)
+      throw Error(MG_EINVAL, std::string("sizing factor for ") +
+                                 (r == 0 ? "advance_output" : r == 1 ? "filter_output" :
+                                  r == 2 ? "input_frontier" : r == 3 ? "outbox" : "inbox") +
+                                 " must not be negative");
+  int comm = prim.communication;
+  if (cfg.comm_override >= 0 && cfg.comm_override != prim.communication) {
+    if (!prim.allow_comm_override)
+      throw Error(MG_EINVAL, std::string(prim.name) + ": communication mode is fixed to " +
+                                 (prim.communication == MG_COMM_SELECTIVE ? "selective"
+                                                                          : "broadcast"));
+    comm = cfg.comm_override;
+  }
+  const bool fused = cfg.fused == MG_FUSED_ON || (cfg.fused == MG_FUSED_AUTO &&
+                                                  cfg.policy == MG_POLICY_FUSED);
+  RunState rs;
+  rs.comm = comm;
+  rs.in_count.assign(n, 0);
+  rs.next_count.assign(n, 0);
+  rs.in_deg.assign(n, 0);
+  rs.next_deg.assign(n, 0);
+  rs.packed.assign(n, nullptr);
+
+  std::vector<Ctx> ctx(n);
+  for (uint32_t p : P.local_workers) {
+    Worker& w = *P.workers[p];
+    DeviceGuard dg(w.dev);
+    prepare_worker(P, w, cfg);
+    std::vector<uint64_t> caps(n, 0);
+    for (uint32_t s = 0; s < n; ++s)
+      if (s != p) caps[s] = prim.inbox_bound(P, s, p, comm);
+    ensure_inboxes(P, w, prim.nva, prim.nvv, caps);
+    MGB_CUDA(cudaEventCreateWithFlags(&rs.packed[p], cudaEventDisableTiming));
+    ctx[p].P = &P;
+    ctx[p].w = &w;
+    ctx[p].run = &rs;
+    ctx[p].fused = fused;
+  }
+  build_send_tables(P);
+  P.h_matrix.assign(n, std::vector<uint64_t>(n, 0));
+  P.h_per_iter.clear();
+  P.out_per_iter.clear();
+  P.edges_per_iter.clear();
+  P.combine_per_iter.clear();
+  uint64_t launches0 = g_launches.load();
+  uint64_t total_edges = 0, total_combine = 0, wire = 0, xbytes = 0;
+  const uint32_t inflation = cfg.h_inflation ? cfg.h_inflation : 1;
+  int stop_reason = MG_STOP_FRONTIERS_EMPTY;
+
+  auto t0 = std::chrono::steady_clock::now();
+  for (uint32_t p : P.local_workers) {
+    Worker& w = *P.workers[p];
+    DeviceGuard dg(w.dev);
+    MGB_CUDA(cudaEventRecord(w.ev_start, w.stream));
+    MGB_CUDA(cudaMemsetAsync(w.ctr.ptr, 0, sizeof(Counters), w.stream));
+    MGB_CUDA(cudaMemsetAsync(w.merge_stamp.ptr, 0, sizeof(uint32_t) * w.nv, w.stream));
+    prim.init(ctx[p]);
+    // advance bound of superstep 0
+    if (rs.next_count[p])
+      MGB_LAUNCH(degsum_kernel, grid_for(rs.next_count[p], 256, 1024), 256, 0, w.stream,
+                 w.graph(), w.next_input.ptr, rs.next_count[p], &w.ctr.ptr->next_deg);
+    MGB_CUDA(cudaMemcpyAsync(w.host_ctr, w.ctr.ptr, sizeof(Counters), cudaMemcpyDeviceToHost,
+                             w.stream));
+  }
+  for (uint32_t p : P.local_workers) {
+    MGB_CUDA(cudaStreamSynchronize(P.workers[p]->stream));
+    rs.next_deg[p] = P.workers[p]->host_ctr->next_deg;
+  }
+
+  for (uint64_t iter = 0;; ++iter) {
+    const GlobalView* prev = rs.views.empty() ? nullptr : &rs.views.back();
+    const uint32_t parity = iter & 1u;
+    std::vector<int> step_comm(n, comm);
+    // body + split/pack + publish
+    for (uint32_t p : P.local_workers) {
+      Worker& w = *P.workers[p];
+      Ctx& c = ctx[p];
+      DeviceGuard dg(w.dev);
+      std::swap(w.input, w.next_input);
+      c.in_count = rs.in_count[p] = rs.next_count[p];
+      c.in_degsum = rs.in_deg[p] = rs.next_deg[p];
+      rs.next_count[p] = 0;
+      c.iter = iter;
+      c.prev = prev;
+      c.report = WorkerReport{};
+      MGB_CUDA(cudaMemsetAsync(w.ctr.ptr, 0, sizeof(Counters), w.stream));
+      prim.body(c);
+      step_comm[p] = prim.comm_selector(c, comm);
+      // next_input holds the local part plus everything merged this superstep
+      uint64_t incoming = 0;
+      for (uint32_t s = 0; s < n; ++s) incoming += (s == p) ? 0 : w.slot_cap[s];
+      w.next_input.ensure(w.output.cap + incoming, w.stream);
+      unsigned long long drop = 0;
+      if (cfg.drop_enabled && cfg.drop_src == p && cfg.drop_iteration == iter &&
+          cfg.drop_dst < 64)
+        drop = 1ull << cfg.drop_dst;
+      if (n > 1) MGB_CUDA(cudaEventRecord(w.ev_x0, w.stream));
+      auto dev = prim.dev(c);
+      MGB_LAUNCH(split_pack_kernel<decltype(dev)>, grid_for(w.output.cap, 256, kNumSMs * 8),
+                 256, 0, w.stream, dev, c.owner_view(), w.graph(), w.output.ptr, w.ctr.ptr,
+                 w.next_input.ptr, w.send_table.ptr + parity * n, n,
+                 step_comm[p] == MG_COMM_BROADCAST ? 1 : 0, drop, prim.nva, prim.nvv);
+      if (n > 1) {
+        MGB_LAUNCH(publish_kernel, 1, 64, 0, w.stream, w.ctr.ptr, w.send_cnt_ptr.ptr + parity * n,
+                   n, p);
+        MGB_CUDA(cudaEventRecord(w.ev_x1, w.stream));
+      }
+      MGB_CUDA(cudaEventRecord(rs.packed[p], w.stream));
+    }
+    // merge (after every peer's pack: event dependencies, no host barrier)
+    for (uint32_t p : P.local_workers) {
+      Worker& w = *P.workers[p];
+      Ctx& c = ctx[p];
+      DeviceGuard dg(w.dev);
+      if (n > 1) {
+        for (uint32_t s : P.local_workers)
+          if (s != p) MGB_CUDA(cudaStreamWaitEvent(w.stream, rs.packed[s], 0));
+        auto dev = prim.dev(c);
+        uint64_t maxcap = 0;
+        for (uint32_t s = 0; s < n; ++s)
+          if (s != p && w.slot_cap[s] > maxcap) maxcap = w.slot_cap[s];
+        dim3 grid(grid_for(maxcap, 256, kNumSMs * 2), n);
+        MGB_LAUNCH(merge_kernel<decltype(dev)>, grid, 256, 0, w.stream, dev, w.slots[parity],
+                   w.inbox_cnt.ptr + parity * kMaxWorkers, p, (uint32_t)(iter + 1),
+                   (uint32_t)iter, w.merge_stamp.ptr, w.next_input.ptr, w.ctr.ptr, w.graph(),
+                   prim.nva, prim.nvv, 1);
+      }
+      prim.after_merge(c);
+      MGB_CUDA(cudaMemcpyAsync(w.host_ctr, w.ctr.ptr, sizeof(Counters), cudaMemcpyDeviceToHost,
+                               w.stream));
+    }
+    // barrier + completion (E:940, E:784-820)
+    GlobalView view;
+    view.iteration = static_cast<uint32_t>(iter);
+    view.num_workers = n;
+    view.reports.resize(n);
+    std::vector<uint64_t> h_src(n, 0);
+    uint64_t it_edges = 0, it_comb = 0;
+    for (uint32_t p : P.local_workers) {
+      Worker& w = *P.workers[p];
+      MGB_CUDA(cudaStreamSynchronize(w.stream));
+      const Counters& hc = *w.host_ctr;
+      if (hc.overflow) throw Error(MG_EWORKER, "inbox overflow on worker " + std::to_string(p));
+      WorkerReport r = ctx[p].report;
+      r.out_frontier = hc.out_cnt;
+      r.next_frontier = hc.next_cnt;
+      r.edges_delta = hc.edges;
+      r.combine_delta = hc.combine;
+      for (int k = 0; k < 4; ++k) {
+        if (r.f[k] == 0.0) r.f[k] = hc.f[k];
+        if (r.u[k] == 0) r.u[k] = hc.u[k];
+      }
+      view.reports[p] = r;
+      rs.next_count[p] = hc.next_cnt;
+      rs.next_deg[p] = hc.next_deg;
+      if (n > 1) {
+        for (uint32_t q = 0; q < n; ++q) {
+          if (q == p) continue;
+          uint64_t len = hc.send_cnt[q];
+          P.h_matrix[p][q] += len;
+          h_src[p] += len;
+          wire += len * inflation;
+          xbytes += len * (4ull + 4ull * prim.nva + 8ull * prim.nvv);
+        }
+        float xms = 0;
+        cudaEventElapsedTime(&xms, w.ev_x0, w.ev_x1);
+        P.last.exchange_ms += xms;
+      }
+      it_edges += hc.edges;
+      it_comb += hc.combine;
+    }
+    for (auto& r : view.reports) {
+      view.total_out += r.out_frontier;
+      view.total_next += r.next_frontier;
+    }
+    view.inflight_records = 0;  // every delivered slot was merged this superstep
+    P.out_per_iter.push_back(view.total_out);
+    P.h_per_iter.push_back(h_src);
+    P.edges_per_iter.push_back(it_edges);
+    P.combine_per_iter.push_back(it_comb);
+    total_edges += it_edges;
+    total_combine += it_comb;
+    bool stop = false;
+    if (iter + 1 >= cfg.max_supersteps) {
+      stop = true;
+      stop_reason = MG_STOP_MAX_SUPERSTEPS;
+    } else {
+      bool conv = prim.has_stop_condition ? prim.stop_condition(view)
+                                          : (view.total_next == 0 && view.inflight_records == 0);
+      if (conv) {
+        stop = true;
+        stop_reason = prim.has_stop_condition ? MG_STOP_CONDITION : MG_STOP_FRONTIERS_EMPTY;
+      }
+    }
+    rs.views.push_back(std::move(view));
+    if (stop) break;
+  }
+  for (uint32_t p : P.local_workers) {
+    Worker& w = *P.workers[p];
+    DeviceGuard dg(w.dev);
+    prim.finalize(ctx[p], rs.views.back());
+    MGB_CUDA(cudaEventRecord(w.ev_end, w.stream));
+  }
+  double dev_ms = 0;
+  for (uint32_t p : P.local_workers) {
+    Worker& w = *P.workers[p];
+    MGB_CUDA(cudaEventSynchronize(w.ev_end));
+    float ms = 0;
+    cudaEventElapsedTime(&ms, w.ev_start, w.ev_end);
+    if (ms > dev_ms) dev_ms = ms;
+    cudaEventDestroy(rs.packed[p]);
+  }
+  auto t1 = std::chrono::steady_clock::now();
+  mg_stats& st = P.last;
+  st.n = n;
+  st.stop_reason = stop_reason;
+  st.communication = comm;
+  st.policy = cfg.policy;
+  st.supersteps = rs.views.size();
+  st.edges_examined = total_edges;
+  st.combine_ops = total_combine;
+  uint64_t h = 0;
+  for (auto& row : P.h_matrix)
+    for (auto v : row) h += v;
+  st.h_total = h;
+  st.wire_records = wire;
+  st.wall_ms = std::chrono::duration<double, std::milli>(t1 - t0).count();
+  st.device_ms = dev_ms;
+  st.gpu_launches = g_launches.load() - launches0;
+  st.exchange_bytes = xbytes;
+  collect_buffer_stats(P);
+}
+
+}  // namespace mgb

@@ -1,0 +1,159 @@
+// plan.cuh — the device-resident partition plan and per-worker runtime state.
+//
+// One Worker per partition (reference WorkerHandle, engine.hpp:478-582), each
+// bound to a CUDA device.  Under Duplicate-All (partition.cpp:157-173) every
+// worker holds a |V|-row sub-CSR in which only its hosted rows are non-empty,
+// so local ID == global ID and ownership is a u8 lookup.  Inboxes (the
+// reference ExchangeFabric slots, engine.hpp:320-445) live in the RECEIVING
+// worker's HBM; senders' pack kernels store records into them directly — over
+// NVLink when the workers sit on different GPUs.
+#pragma once
+
+#include <memory>
+#include <vector>
+
+#include "common.cuh"
+
+namespace mgb {
+
+// POD view of one partition's sub-CSR handed to kernels
+struct GraphView {
+  uint32_t nv;
+  uint64_t ne;
+  const uint32_t* __restrict__ off;
+  const uint32_t* __restrict__ col;
+  const uint32_t* __restrict__ w;  // nullptr if unweighted
+};
+
+// ownership view: hosts(v) / owner(v) / to_global(v) for the local ID space
+struct OwnerView {
+  const uint8_t* __restrict__ owner;  // Duplicate-All: owner[global]
+  const uint32_t* __restrict__ l2g;   // OneHop: local -> global (nullptr under All)
+  uint32_t p;
+  uint32_t nlocal;  // OneHop: hosted vertices are local IDs [0, nlocal)
+  int dup;
+  __device__ __forceinline__ bool hosts(uint32_t v) const {
+    return dup == MG_DUP_ALL ? owner[v] == p : v < nlocal;
+  }
+  __device__ __forceinline__ uint32_t to_global(uint32_t v) const {
+    return dup == MG_DUP_ALL ? v : l2g[v];
+  }
+  __device__ __forceinline__ uint32_t owner_of_local(uint32_t v) const {
+    return owner[to_global(v)];
+  }
+};
+
+// One inbox slot (dst, src, parity): SoA record arrays in the receiver's HBM
+struct SlotView {
+  uint32_t* ids;
+  uint32_t* va[kMaxAssoc];
+  double* vv[kMaxAssoc];
+  uint64_t cap;
+};
+
+// per-worker device counters, copied to pinned host memory once per superstep
+struct Counters {
+  uint32_t out_cnt;       // body output length (reference WorkerReport.out_frontier)
+  uint32_t next_cnt;      // next-input length after split + merge
+  uint32_t adv_cnt;       // unfused advance output length
+  uint32_t big_cnt;       // advance: vertices deferred to the big-vertex pass
+  uint32_t overflow;      // an inbox / buffer bound was violated
+  uint32_t misc;
+  unsigned long long edges;      // W delta (edges examined)
+  unsigned long long combine;    // C delta
+  unsigned long long next_deg;   // sum of out-degrees of next_input (advance bound)
+  double f[4];                   // primitive-defined scalars (WorkerReport.f)
+  unsigned long long u[4];       // primitive-defined scalars (WorkerReport.u)
+  uint32_t send_cnt[kMaxWorkers];  // records packed for each destination
+  uint32_t recv_cnt[kMaxWorkers];  // records received from each source (merge)
+};
+
+struct Worker {
+  uint32_t p = 0;
+  int dev = 0;
+  cudaStream_t stream = nullptr;
+  cudaEvent_t ev_start = nullptr, ev_end = nullptr, ev_x0 = nullptr, ev_x1 = nullptr;
+
+  // sub-graph
+  uint32_t nv = 0;
+  uint64_t ne = 0;
+  uint32_t nlocal = 0;
+  DevArray<uint32_t> off, col, w;
+  DevArray<uint32_t> hosted;  // hosted local IDs (reference hosted_local(), engine.hpp:756-763)
+  DevArray<uint8_t> owner;    // global owner map (u8; n <= 255)
+  DevArray<uint32_t> l2g;     // OneHop only
+  DevArray<uint32_t> border;  // static remote sub-frontier (PR): local IDs, grouped by peer
+  std::vector<uint64_t> border_len;  // per peer
+  std::vector<uint64_t> border_off;  // per peer start in `border`
+
+  // policy-managed frontier buffers (roles of frontier.hpp:33-35)
+  MemoryBudget budget;
+  BufferStats stats[MG_NUM_ROLES];
+  DevBuf<uint32_t> input, next_input, advance_out, output;
+  DevArray<uint32_t> merge_stamp;
+  DevArray<uint32_t> big;       // advance big-vertex scratch (index list)
+  DevArray<unsigned long long> big_prefix;
+
+  // inbox arena (receiver side): [parity][src] slots + counts
+  int nva = 0, nvv = 0;
+  std::vector<uint64_t> slot_cap;  // per src
+  DevArray<uint8_t> arena;
+  SlotView slots[2][kMaxWorkers];
+  DevArray<uint32_t> inbox_cnt;    // [2][kMaxWorkers], written by senders
+  // sender side: where this worker's records for each peer go, per parity
+  DevArray<SlotView> send_table;   // [2][n]
+  DevArray<uint32_t*> send_cnt_ptr;  // [2][n] -> &inbox_cnt[parity][p] at peer
+
+  // primitive state arrays (|V_i| entries each), reused across runs; results
+  // of the last run stay here until the next run (mg_plan_fetch)
+  DevArray<uint32_t> su32[4];
+  DevArray<double> sf64[4];
+  DevArray<unsigned long long> su64[3];
+  std::vector<uint32_t> hosted_host;  // hosted local IDs (host copy)
+  DevArray<uint32_t> border_dst;      // PR: destination-local ID of every border entry
+
+  // counters
+  DevArray<Counters> ctr;
+  Counters* host_ctr = nullptr;  // pinned
+
+  GraphView graph() const { return {nv, ne, off.ptr, col.ptr, w.ptr}; }
+};
+
+struct Plan {
+  uint32_t n = 1;
+  int dup = 0;
+  uint32_t nv = 0;
+  uint64_t ne = 0;
+  bool weighted = false;
+  std::vector<int> devices;
+  std::vector<std::unique_ptr<Worker>> workers;  // only local workers are populated
+  std::vector<uint32_t> local_workers;           // partition ids driven by this process
+  std::vector<std::vector<uint64_t>> pair_border;  // |B_{i,j}|
+  std::vector<uint64_t> nlocal;                    // |L_i|
+  uint64_t edge_cut = 0;
+  std::vector<uint32_t> owner_host;  // global owner map (host copy)
+  bool multiprocess = false;
+  uint32_t rank = 0, world = 1;
+  // host copy of the global CSR (kept when built from a host graph)
+  std::shared_ptr<HostCsr> host_graph;
+  // device copy of the global CSR (device-built plans) on workers[0]'s device
+  DevArray<uint32_t> g_off, g_col, g_w;
+
+  // last run
+  mg_stats last{};
+  std::vector<std::vector<uint64_t>> h_matrix;
+  std::vector<std::vector<uint64_t>> h_per_iter;
+  std::vector<uint64_t> out_per_iter, edges_per_iter, combine_per_iter;
+  std::vector<std::vector<BufferStats>> last_buffers;  // [worker][role]
+  // device-resident results of the last run (global ID space, on workers[0].dev)
+  int last_result_kind = -1;
+
+  // multi-process bootstrap
+  std::vector<void*> peer_arena;    // mapped inbox arenas of peers
+  std::vector<uint64_t> peer_arena_bytes;
+};
+
+Worker& worker(Plan& P, uint32_t p);
+void plan_free(Plan* P);
+
+}  // namespace mgb

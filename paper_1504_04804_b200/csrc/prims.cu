@@ -1,0 +1,1071 @@
+// prims.cu — the six primitives of primitives.cpp as device functor sets +
+// host hooks for the enactor (engine.cuh), and their C-ABI entry points.
+//
+// Each primitive mirrors its reference PrimitiveSpec field by field:
+// init / iteration_body / combine / gather / send_filter / comm_selector /
+// stop_condition / finalize (engine.hpp:587-626).  Device functors implement
+// the per-vertex hooks with atomics whose outcome is independent of thread
+// order (atomicCAS / atomicMin / atomicExch stamps), so labels, distances and
+// components are bit-identical to the sequential reference.
+#include <cmath>
+#include <cstring>
+
+#include "engine.cuh"
+
+namespace mgb {
+
+void gather_u32(Plan& P, const std::vector<const uint32_t*>& pw, uint32_t* out);
+void gather_u64(Plan& P, const std::vector<const unsigned long long*>& pw, uint64_t* out);
+void gather_f64(Plan& P, const std::vector<const double*>& pw, double* out);
+
+namespace {
+
+// defaults of the PrimitiveSpec hooks
+struct PrimBase {
+  const char* name = "?";
+  int nva = 0, nvv = 0;
+  int communication = MG_COMM_SELECTIVE;
+  bool allow_comm_override = false;
+  int dup_required = MG_DUP_ALL;
+  bool has_stop_condition = false;
+  uint64_t inbox_bound(Plan& P, uint32_t src, uint32_t dst, int comm) const {
+    // selective: each proxy at most once per superstep (keep dedup) -> |B_{src,dst}|;
+    // broadcast: the whole output, bounded by |V_src| local IDs
+    return comm == MG_COMM_BROADCAST ? P.workers[src] ? P.workers[src]->nv : P.nv
+                                     : P.pair_border[src][dst];
+  }
+  int comm_selector(Ctx&, int comm) { return comm; }
+  bool stop_condition(const GlobalView&) { return false; }
+  void after_merge(Ctx&) {}
+  void finalize(Ctx&, const GlobalView&) {}
+};
+
+template <class T>
+void fill(DevArray<T>& a, uint64_t n, int byte, cudaStream_t s) {
+  if (a.n < n || !a.ptr) a.alloc(n ? n : 1);
+  MGB_CUDA(cudaMemsetAsync(a.ptr, byte, sizeof(T) * (n ? n : 1), s));
+}
+
+template <class T>
+__global__ void set_one_kernel(T* a, uint32_t i, T v) {
+  a[i] = v;
+}
+
+__global__ void fill_f64_kernel(double* a, uint32_t n, double v) {
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
+    a[i] = v;
+}
+
+__global__ void fill_hosted_f64_kernel(double* a, const uint32_t* hosted, uint32_t n, double v) {
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
+    a[hosted[i]] = v;
+}
+
+__global__ void iota_kernel(uint32_t* a, uint32_t n) {
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
+    a[i] = i;
+}
+
+// atomicMax on non-negative doubles through their ordered bit patterns
+__device__ __forceinline__ void atomic_max_pos_f64(double* addr, double v) {
+  atomicMax(reinterpret_cast<unsigned long long*>(addr),
+            static_cast<unsigned long long>(__double_as_longlong(v)));
+}
+
+// ===========================================================================
+// BFS (primitives.cpp:60-126)
+
+struct BfsDev {
+  uint32_t* labels;
+  uint32_t* preds;
+  uint32_t* seen;
+  OwnerView ow;
+  uint32_t iter;
+  int mark_preds;
+  // visit: unvisited -> label iter+1 (+pred); the CAS makes the discovery unique
+  __device__ bool visit(uint32_t u, uint32_t v, uint32_t) const {
+    if (labels[v] != kInfLabel) return false;
+    if (atomicCAS(&labels[v], kInfLabel, iter + 1) != kInfLabel) return false;
+    if (mark_preds) preds[v] = ow.to_global(u);
+    return true;
+  }
+  // keep: per-superstep stamp dedup (primitives.cpp:89-94)
+  __device__ bool keep(uint32_t v) const { return atomicExch(&seen[v], iter + 1) != iter + 1; }
+  // combine (primitives.cpp:98-107): iter+1 < label -> set, enqueue iff hosted
+  __device__ bool combine(uint32_t v, const uint32_t* va, const double*, uint32_t it) const {
+    uint32_t cand = it + 1;
+    uint32_t old = atomicMin(&labels[v], cand);
+    if (cand < old) {
+      if (mark_preds) preds[v] = va[0];
+      return ow.hosts(v);
+    }
+    return false;
+  }
+  __device__ void gather(uint32_t v, uint32_t* va, double*) const {
+    if (mark_preds) va[0] = preds[v];
+  }
+  __device__ bool send_filter(uint32_t, uint32_t) const { return true; }
+  __device__ uint32_t peer_id(uint32_t v, uint32_t, uint32_t) const { return v; }
+};
+
+struct BfsPrim : PrimBase {
+  uint32_t source;
+  bool mark_preds;
+  BfsPrim(uint32_t s, bool m) : source(s), mark_preds(m) {
+    name = "bfs";
+    nva = m ? 1 : 0;
+    allow_comm_override = true;
+  }
+  void init(Ctx& c) {  // primitives.cpp:71-79
+    Worker& w = *c.w;
+    fill(w.su32[0], w.nv, 0xFF, w.stream);  // labels = inf
+    fill(w.su32[2], w.nv, 0, w.stream);     // seen
+    if (mark_preds) fill(w.su32[1], w.nv, 0xFF, w.stream);
+    MGB_LAUNCH(set_one_kernel<uint32_t>, 1, 1, 0, w.stream, w.su32[0].ptr, source, 0u);
+    if (c.P->owner_host[source] == w.p) c.push_initial({source});
+  }
+  BfsDev dev(Ctx& c) {
+    Worker& w = *c.w;
+    return {w.su32[0].ptr, w.su32[1].ptr, w.su32[2].ptr, c.owner_view(), (uint32_t)c.iter,
+            mark_preds ? 1 : 0};
+  }
+  void body(Ctx& c) { c.pipeline(dev(c), c.w->nv); }
+};
+
+// ===========================================================================
+// DOBFS (primitives.cpp:131-289)
+
+struct DobfsDev {
+  uint32_t* labels;
+  uint32_t* preds;
+  OwnerView ow;
+  uint32_t iter;
+  int mark_preds;
+  __device__ bool visit(uint32_t u, uint32_t v, uint32_t) const {
+    if (labels[v] != kInfLabel) return false;
+    if (atomicCAS(&labels[v], kInfLabel, iter + 1) != kInfLabel) return false;
+    if (mark_preds) preds[v] = ow.to_global(u);
+    return true;
+  }
+  __device__ bool keep(uint32_t) const { return true; }
+  // combine (primitives.cpp:255-265): accepted remote discoveries join the
+  // (global) next frontier on every worker
+  __device__ bool combine(uint32_t v, const uint32_t* va, const double*, uint32_t it) const {
+    uint32_t cand = it + 1;
+    uint32_t old = atomicMin(&labels[v], cand);
+    if (cand < old) {
+      if (mark_preds) preds[v] = va[0];
+      return true;
+    }
+    return false;
+  }
+  __device__ void gather(uint32_t v, uint32_t* va, double*) const {
+    if (mark_preds) va[0] = preds[v];
+  }
+  __device__ bool send_filter(uint32_t, uint32_t) const { return true; }
+  __device__ uint32_t peer_id(uint32_t v, uint32_t, uint32_t) const { return v; }
+};
+
+__global__ void stamp_frontier_kernel(const uint32_t* __restrict__ in, uint32_t n,
+                                      uint32_t* stamp, uint32_t value) {
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
+    stamp[in[i]] = value;
+}
+
+// backward (pull) step (primitives.cpp:227-252): every hosted unvisited vertex
+// scans its arcs in order and stops at the first neighbour in the frontier.
+// One 8-lane group per vertex: each round the group tests 8 consecutive arcs
+// (one 32-byte sector of col_indices) and the first hit in arc order wins, so
+// the examined-edge count equals the reference's sequential count.
+constexpr int kPullGroup = 8;
+__global__ void __launch_bounds__(256)
+    dobfs_pull_kernel(GraphView g, const uint32_t* __restrict__ hosted, uint32_t nh,
+                      uint32_t* labels, uint32_t* preds, const uint32_t* __restrict__ in_frontier,
+                      uint32_t stamp, uint32_t next_label, int mark_preds, OwnerView ow,
+                      uint32_t* out, Counters* ctr) {
+  const unsigned lane = threadIdx.x & 31u;
+  const unsigned sub = lane & (kPullGroup - 1);
+  const unsigned gbase = lane & ~(kPullGroup - 1);
+  const unsigned gmask = ((1u << kPullGroup) - 1u) << gbase;
+  unsigned long long scanned = 0;
+  const uint32_t groups = (gridDim.x * blockDim.x) / kPullGroup;
+  const uint32_t gid = (blockIdx.x * blockDim.x + threadIdx.x) / kPullGroup;
+  const uint32_t rounds = (nh + groups - 1) / groups;
+  for (uint32_t r = 0; r < rounds; ++r) {
+    uint32_t i = r * groups + gid;
+    bool found = false;
+    uint32_t v = 0;
+    if (i < nh) {
+      v = hosted[i];
+      if (labels[v] == kInfLabel) {
+        uint32_t b = g.off[v], e = g.off[v + 1];
+        for (uint32_t k = b; k < e; k += kPullGroup) {
+          uint32_t idx = k + sub;
+          bool hit = idx < e && in_frontier[g.col[idx]] == stamp;
+          unsigned m = __ballot_sync(gmask, hit) & gmask;
+          if (m) {
+            unsigned first = __ffs(m) - 1 - gbase;
+            scanned += (sub == 0) ? (k - b + first + 1) : 0;
+            if (sub == 0) {
+              found = true;
+              uint32_t w = g.col[k + first];
+              labels[v] = next_label;
+              if (mark_preds) preds[v] = ow.to_global(w);
+            }
+            break;
+          }
+          if (sub == 0) scanned += (e - k < (uint32_t)kPullGroup) ? (e - k) : kPullGroup;
+        }
+      }
+    }
+    uint32_t slot = warp_append(&ctr->out_cnt, found);
+    if (found) out[slot] = v;
+  }
+  warp_add_u64(&ctr->edges, scanned);
+}
+
+struct DobfsPrim : PrimBase {
+  uint32_t source;
+  double do_a, do_b;
+  bool mark_preds;
+  // host-side mirror of the per-worker state (identical on every worker)
+  uint64_t visited = 1;
+  int dir = 0;
+  bool switched_once = false;
+  std::vector<int> dir_log;
+  std::vector<uint64_t> fwd, bwd;
+  DobfsPrim(uint32_t s, double a, double b, bool m) : source(s), do_a(a), do_b(b), mark_preds(m) {
+    name = "dobfs";
+    nva = m ? 1 : 0;
+    communication = MG_COMM_BROADCAST;
+  }
+  void init(Ctx& c) {  // primitives.cpp:185-195
+    Worker& w = *c.w;
+    fill(w.su32[0], w.nv, 0xFF, w.stream);  // labels
+    fill(w.su32[3], w.nv, 0, w.stream);     // in_frontier stamps
+    if (mark_preds) fill(w.su32[1], w.nv, 0xFF, w.stream);
+    MGB_LAUNCH(set_one_kernel<uint32_t>, 1, 1, 0, w.stream, w.su32[0].ptr, source, 0u);
+    if (c.P->owner_host[source] == w.p) c.push_initial({source});
+    if (fwd.empty()) {
+      fwd.assign(c.P->n, 0);
+      bwd.assign(c.P->n, 0);
+    }
+  }
+  DobfsDev dev(Ctx& c) {
+    Worker& w = *c.w;
+    return {w.su32[0].ptr, w.su32[1].ptr, c.owner_view(), (uint32_t)c.iter, mark_preds ? 1 : 0};
+  }
+  void body(Ctx& c) {  // primitives.cpp:197-253
+    Worker& w = *c.w;
+    const uint32_t stamp = (uint32_t)c.iter + 1;
+    if (c.in_count)
+      MGB_LAUNCH(stamp_frontier_kernel, grid_for(c.in_count, 256), 256, 0, w.stream,
+                 w.input.ptr, c.in_count, w.su32[3].ptr, stamp);
+    if (c.worker() == c.P->local_workers.front()) {
+      // decision on global quantities; identical on every worker
+      if (c.iter >= 1) {
+        if (c.prev) visited += c.prev->reports[c.worker()].next_frontier;
+        double fv = c.P->nv > 0 ? (double)c.in_count * (double)c.P->ne / (double)c.P->nv : 0.0;
+        double bv = visited > 0 ? (double)(c.P->nv - visited) * (double)c.P->nv / (double)visited
+                                : 0.0;
+        int next;
+        if (dir == 0) next = (!switched_once && fv > bv * do_a) ? 1 : 0;
+        else next = fv < bv * do_b ? 0 : 1;
+        if (next == 1 && dir == 0) switched_once = true;
+        dir = next;
+      }
+      dir_log.push_back(dir);
+    }
+    if (dir == 0) {
+      c.pipeline(dev(c), w.nv);
+    } else {
+      uint32_t nh = (uint32_t)w.hosted_host.size();
+      c.ensure_output(nh);
+      if (nh)
+        MGB_LAUNCH(dobfs_pull_kernel, grid_for((uint64_t)nh * kPullGroup, 256, kNumSMs * 16), 256,
+                   0, w.stream, w.graph(), w.hosted.ptr, nh, w.su32[0].ptr, w.su32[1].ptr,
+                   w.su32[3].ptr, stamp, stamp, mark_preds ? 1 : 0, c.owner_view(), w.output.ptr,
+                   c.ctr());
+    }
+  }
+  void after_merge(Ctx&) {}
+};
+
+// ===========================================================================
+// SSSP (primitives.cpp:307-397)
+
+struct SsspDev {
+  unsigned long long* dists;
+  const unsigned long long* fdist;
+  unsigned long long* last_sent;
+  uint32_t* preds;
+  uint32_t* seen;
+  const uint32_t* w;
+  OwnerView ow;
+  uint32_t iter;
+  int mark_preds;
+  // relax from the superstep-frozen source distance (primitives.cpp:340-348)
+  __device__ bool visit(uint32_t u, uint32_t v, uint32_t e) const {
+    unsigned long long nd = fdist[u] + w[e];
+    if (nd >= dists[v]) return false;
+    unsigned long long old = atomicMin(&dists[v], nd);
+    if (nd < old) {
+      if (mark_preds) preds[v] = ow.to_global(u);
+      return true;
+    }
+    return false;
+  }
+  __device__ bool keep(uint32_t v) const { return atomicExch(&seen[v], iter + 1) != iter + 1; }
+  __device__ bool combine(uint32_t v, const uint32_t* va, const double* vv, uint32_t) const {
+    unsigned long long nd = (unsigned long long)vv[0];
+    unsigned long long old = atomicMin(&dists[v], nd);
+    if (nd < old) {
+      if (mark_preds) preds[v] = va[0];
+      return ow.hosts(v);
+    }
+    return false;
+  }
+  __device__ void gather(uint32_t v, uint32_t* va, double* vv) const {
+    vv[0] = (double)dists[v];
+    if (mark_preds) va[0] = preds[v];
+  }
+  // pre-send suppression (primitives.cpp:377-383)
+  __device__ bool send_filter(uint32_t, uint32_t v) const {
+    if (dists[v] < last_sent[v]) {
+      last_sent[v] = dists[v];
+      return true;
+    }
+    return false;
+  }
+  __device__ uint32_t peer_id(uint32_t v, uint32_t, uint32_t) const { return v; }
+};
+
+__global__ void snapshot_kernel(const uint32_t* __restrict__ in, uint32_t n,
+                                const unsigned long long* dists, unsigned long long* fdist) {
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    uint32_t u = in[i];
+    fdist[u] = dists[u];
+  }
+}
+
+struct SsspPrim : PrimBase {
+  uint32_t source;
+  bool mark_preds;
+  SsspPrim(uint32_t s, bool m) : source(s), mark_preds(m) {
+    name = "sssp";
+    nva = m ? 1 : 0;
+    nvv = 1;
+    allow_comm_override = true;
+  }
+  void init(Ctx& c) {  // primitives.cpp:323-332
+    Worker& w = *c.w;
+    fill(w.su64[0], w.nv, 0xFF, w.stream);  // dists
+    fill(w.su64[1], w.nv, 0xFF, w.stream);  // frontier_dist
+    fill(w.su64[2], w.nv, 0xFF, w.stream);  // last_sent
+    fill(w.su32[2], w.nv, 0, w.stream);     // seen
+    if (mark_preds) fill(w.su32[1], w.nv, 0xFF, w.stream);
+    MGB_LAUNCH(set_one_kernel<unsigned long long>, 1, 1, 0, w.stream, w.su64[0].ptr, source,
+               0ull);
+    if (c.P->owner_host[source] == w.p) c.push_initial({source});
+  }
+  SsspDev dev(Ctx& c) {
+    Worker& w = *c.w;
+    return {w.su64[0].ptr, w.su64[1].ptr, w.su64[2].ptr, w.su32[1].ptr, w.su32[2].ptr,
+            w.w.ptr, c.owner_view(), (uint32_t)c.iter, mark_preds ? 1 : 0};
+  }
+  void body(Ctx& c) {
+    Worker& w = *c.w;
+    if (c.in_count)
+      MGB_LAUNCH(snapshot_kernel, grid_for(c.in_count, 256), 256, 0, w.stream, w.input.ptr,
+                 c.in_count, w.su64[0].ptr, w.su64[1].ptr);
+    c.pipeline(dev(c), w.nv);
+  }
+};
+
+// ===========================================================================
+// CC (primitives.cpp:416-495)
+
+struct CcDev {
+  uint32_t* comp;
+  uint32_t* snapshot;
+  __device__ bool visit(uint32_t, uint32_t, uint32_t) const { return false; }
+  __device__ bool keep(uint32_t) const { return true; }
+  __device__ bool combine(uint32_t v, const uint32_t* va, const double*, uint32_t) const {
+    uint32_t c = va[0];
+    uint32_t old = atomicMin(&comp[v], c);
+    if (c < old) {
+      atomicMin(&snapshot[v], c);  // the sender already broadcast it to everyone
+      return true;
+    }
+    return false;
+  }
+  __device__ void gather(uint32_t v, uint32_t* va, double*) const { va[0] = comp[v]; }
+  __device__ bool send_filter(uint32_t, uint32_t) const { return true; }
+  __device__ uint32_t peer_id(uint32_t v, uint32_t, uint32_t) const { return v; }
+};
+
+__device__ __forceinline__ uint32_t cc_root(const uint32_t* comp, uint32_t x) {
+  uint32_t y = comp[x];
+  while (y != x) {
+    x = y;
+    y = comp[x];
+  }
+  return x;
+}
+
+// hook the larger root under the smaller over every hosted arc (primitives.cpp:443-455)
+__global__ void __launch_bounds__(256)
+    cc_hook_kernel(GraphView g, const uint32_t* __restrict__ hosted, uint32_t nh, uint32_t* comp,
+                   uint32_t* hooked) {
+  // one warp per hosted vertex: lanes stride its arcs
+  const uint32_t warps = gridDim.x * blockDim.x / 32;
+  uint32_t wid = (blockIdx.x * blockDim.x + threadIdx.x) / 32;
+  bool any = false;
+  for (uint32_t i = wid; i < nh; i += warps) {
+    uint32_t u = hosted[i];
+    uint32_t b = g.off[u], e = g.off[u + 1];
+    for (uint32_t k = b + lane_id(); k < e; k += 32) {
+      uint32_t v = g.col[k];
+      uint32_t ru = cc_root(comp, u), rv = cc_root(comp, v);
+      if (ru == rv) continue;
+      uint32_t hi = ru > rv ? ru : rv, lo = ru < rv ? ru : rv;
+      atomicMin(&comp[hi], lo);
+      any = true;
+    }
+  }
+  if (__any_sync(__activemask(), any) && lane_id() == 0) *hooked = 1;
+}
+
+// full pointer jumping over every local vertex (primitives.cpp:456-457)
+__global__ void cc_jump_kernel(uint32_t* comp, uint32_t nv) {
+  for (uint32_t w = blockIdx.x * blockDim.x + threadIdx.x; w < nv; w += gridDim.x * blockDim.x)
+    comp[w] = cc_root(comp, w);
+}
+
+// delta encoding: emit local vertices whose value changed since the snapshot
+__global__ void cc_delta_kernel(uint32_t* comp, uint32_t* snapshot, uint32_t nv, uint32_t* out,
+                                Counters* ctr) {
+  for (uint32_t base = blockIdx.x * blockDim.x; base < nv; base += gridDim.x * blockDim.x) {
+    uint32_t w = base + threadIdx.x;
+    bool ch = false;
+    if (w < nv) {
+      uint32_t c = comp[w];
+      ch = c != snapshot[w];
+      if (ch) snapshot[w] = c;
+    }
+    uint32_t slot = warp_append(&ctr->out_cnt, ch);
+    if (ch) out[slot] = w;
+  }
+}
+
+struct CcPrim : PrimBase {
+  DevArray<uint32_t>* flag = nullptr;
+  CcPrim() {
+    name = "cc";
+    nva = 1;
+    communication = MG_COMM_BROADCAST;
+  }
+  void init(Ctx& c) {  // primitives.cpp:425-434
+    Worker& w = *c.w;
+    if (w.su32[0].n < w.nv || !w.su32[0].ptr) w.su32[0].alloc(w.nv ? w.nv : 1);
+    if (w.su32[1].n < w.nv || !w.su32[1].ptr) w.su32[1].alloc(w.nv ? w.nv : 1);
+    if (!w.su32[3].ptr) w.su32[3].alloc(1);
+    if (w.nv) {
+      MGB_LAUNCH(iota_kernel, grid_for(w.nv, 256), 256, 0, w.stream, w.su32[0].ptr, w.nv);
+      MGB_CUDA(cudaMemcpyAsync(w.su32[1].ptr, w.su32[0].ptr, 4ull * w.nv,
+                               cudaMemcpyDeviceToDevice, w.stream));
+    }
+    // a non-empty initial frontier keeps superstep 0 alive
+    uint32_t nh = (uint32_t)w.hosted_host.size();
+    uint32_t& nc = c.run->next_count[w.p];
+    w.next_input.ensure(nh, w.stream);
+    if (nh)
+      MGB_CUDA(cudaMemcpyAsync(w.next_input.ptr, w.hosted.ptr, 4ull * nh,
+                               cudaMemcpyDeviceToDevice, w.stream));
+    nc = nh;
+  }
+  CcDev dev(Ctx& c) { return {c.w->su32[0].ptr, c.w->su32[1].ptr}; }
+  void body(Ctx& c) {  // primitives.cpp:436-472: local fixpoint, then delta
+    Worker& w = *c.w;
+    uint32_t nh = (uint32_t)w.hosted_host.size();
+    uint32_t* hooked = w.su32[3].ptr;
+    uint32_t h = 1;
+    uint64_t scanned = 0;
+    const uint64_t local_edges = w.ne;  // every hosted arc once per hook pass
+    while (h) {
+      MGB_CUDA(cudaMemsetAsync(hooked, 0, 4, w.stream));
+      if (nh)
+        MGB_LAUNCH(cc_hook_kernel, grid_for((uint64_t)nh * 32, 256, kNumSMs * 16), 256, 0,
+                   w.stream, w.graph(), w.hosted.ptr, nh, w.su32[0].ptr, hooked);
+      if (w.nv)
+        MGB_LAUNCH(cc_jump_kernel, grid_for(w.nv, 256, kNumSMs * 16), 256, 0, w.stream,
+                   w.su32[0].ptr, w.nv);
+      MGB_CUDA(cudaMemcpyAsync(&h, hooked, 4, cudaMemcpyDeviceToHost, w.stream));
+      MGB_CUDA(cudaStreamSynchronize(w.stream));
+      scanned += local_edges;
+    }
+    c.ensure_output(w.nv);
+    if (w.nv)
+      MGB_LAUNCH(cc_delta_kernel, grid_for(w.nv, 256, kNumSMs * 16), 256, 0, w.stream,
+                 w.su32[0].ptr, w.su32[1].ptr, w.nv, w.output.ptr, c.ctr());
+    add_edges(c, scanned);
+  }
+  static void add_edges(Ctx& c, uint64_t k);
+};
+
+__global__ void add_u64_kernel(unsigned long long* dst, unsigned long long v) { *dst += v; }
+
+void CcPrim::add_edges(Ctx& c, uint64_t k) {
+  if (k) MGB_LAUNCH(add_u64_kernel, 1, 1, 0, c.w->stream, &c.ctr()->edges, k);
+}
+
+// ===========================================================================
+// BC (primitives.cpp:518-680)
+
+enum : uint64_t { kFwd = 0, kBwd = 1, kDone = 2 };
+
+struct BcDev {
+  uint32_t* labels;
+  double* sigma;
+  double* delta;
+  uint32_t* bstamp;
+  uint32_t* seen;
+  OwnerView ow;
+  uint32_t iter;
+  int phase;
+  // forward visit (primitives.cpp:559-567): sigma counts are integers, so the
+  // order of the atomic additions does not change the result
+  __device__ bool visit(uint32_t u, uint32_t v, uint32_t) const {
+    uint32_t cand = iter + 1;
+    uint32_t old = labels[v];
+    if (old == kInfLabel) old = atomicCAS(&labels[v], kInfLabel, cand);
+    if (old == kInfLabel || old == cand) atomicAdd(&sigma[v], sigma[u]);
+    return old == kInfLabel;
+  }
+  __device__ bool keep(uint32_t v) const { return atomicExch(&seen[v], iter + 1) != iter + 1; }
+  __device__ bool combine(uint32_t v, const uint32_t*, const double* vv, uint32_t it) const {
+    if (phase == kFwd) {  // primitives.cpp:639-648
+      uint32_t cand = it + 1;
+      uint32_t old = atomicMin(&labels[v], cand);
+      if (old >= cand) atomicAdd(&sigma[v], vv[0]);  // label was inf => sigma was 0
+      return old > cand && ow.hosts(v);
+    }
+    sigma[v] = vv[0];  // dependency phase (primitives.cpp:650-653)
+    delta[v] = vv[1];
+    bstamp[v] = it + 1;
+    return false;
+  }
+  __device__ void gather(uint32_t v, uint32_t*, double* vv) const {
+    vv[0] = sigma[v];
+    if (phase == kFwd) {
+      vv[1] = 0.0;
+      sigma[v] = 0.0;  // partial shipped; reset the proxy accumulator
+    } else {
+      vv[1] = delta[v];
+    }
+  }
+  __device__ bool send_filter(uint32_t, uint32_t) const { return true; }
+  __device__ uint32_t peer_id(uint32_t v, uint32_t, uint32_t) const { return v; }
+};
+
+__global__ void max_hosted_label_kernel(const uint32_t* labels, const uint32_t* hosted,
+                                        uint32_t nh, Counters* ctr) {
+  uint32_t m = 0;
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < nh; i += gridDim.x * blockDim.x) {
+    uint32_t l = labels[hosted[i]];
+    if (l != kInfLabel && l > m) m = l;
+  }
+  for (int o = 16; o > 0; o >>= 1) m = max(m, __shfl_xor_sync(0xffffffffu, m, o));
+  if (lane_id() == 0 && m) atomicMax(&ctr->u[0], (unsigned long long)m);
+}
+
+// backward level step (primitives.cpp:592-617).  Each vertex of the level is
+// handled by one thread walking its arcs in order with explicitly rounded
+// operations (no FMA contraction), so delta/bc match the reference bit for bit.
+__global__ void __launch_bounds__(256)
+    bc_backward_kernel(GraphView g, const uint32_t* __restrict__ hosted, uint32_t nh,
+                       const uint32_t* labels, const double* sigma, double* delta, double* bc,
+                       const uint32_t* bstamp, uint32_t level, uint32_t prev_stamp,
+                       uint32_t source, int accumulate, OwnerView ow, uint32_t* out,
+                       Counters* ctr) {
+  unsigned long long scanned = 0;
+  for (uint32_t base = blockIdx.x * blockDim.x; base < nh; base += gridDim.x * blockDim.x) {
+    uint32_t i = base + threadIdx.x;
+    bool emit = false;
+    uint32_t v = 0;
+    if (i < nh) {
+      v = hosted[i];
+      emit = labels[v] == level;
+      if (emit && accumulate) {
+        double acc = 0.0;
+        const double sv = sigma[v];
+        uint32_t b = g.off[v], e = g.off[v + 1];
+        for (uint32_t k = b; k < e; ++k) {
+          uint32_t w = g.col[k];
+          bool succ = ow.hosts(w) ? (labels[w] == level + 1) : (bstamp[w] == prev_stamp);
+          double sw = sigma[w];
+          if (succ && sw > 0.0)
+            acc = __dadd_rn(acc, __dmul_rn(__ddiv_rn(sv, sw), __dadd_rn(1.0, delta[w])));
+        }
+        scanned += e - b;
+        delta[v] = acc;
+        if (v != source) bc[v] = __dadd_rn(bc[v], acc);
+      }
+    }
+    uint32_t slot = warp_append(&ctr->out_cnt, emit);
+    if (emit) out[slot] = v;
+  }
+  warp_add_u64(&ctr->edges, scanned);
+}
+
+struct BcPrim : PrimBase {
+  uint32_t source;
+  int phase = kFwd;
+  uint32_t max_level = 0;
+  uint64_t backward_from = 0;
+  BcPrim(uint32_t s) : source(s) {
+    name = "bc";
+    nvv = 2;
+    has_stop_condition = true;
+  }
+  uint64_t inbox_bound(Plan& P, uint32_t src, uint32_t dst, int) const {
+    // forward: selective (|B|); backward: broadcast of one level of hosted vertices
+    uint64_t a = P.pair_border[src][dst], b = P.nlocal[src];
+    return a > b ? a : b;
+  }
+  void init(Ctx& c) {  // primitives.cpp:528-541
+    Worker& w = *c.w;
+    fill(w.su32[0], w.nv, 0xFF, w.stream);  // labels
+    fill(w.su32[2], w.nv, 0, w.stream);     // seen
+    fill(w.su32[3], w.nv, 0, w.stream);     // bstamp
+    fill(w.sf64[0], w.nv, 0, w.stream);     // sigma
+    fill(w.sf64[1], w.nv, 0, w.stream);     // delta
+    fill(w.sf64[2], w.nv, 0, w.stream);     // bc
+    MGB_LAUNCH(set_one_kernel<uint32_t>, 1, 1, 0, w.stream, w.su32[0].ptr, source, 0u);
+    if (c.P->owner_host[source] == w.p) {
+      MGB_LAUNCH(set_one_kernel<double>, 1, 1, 0, w.stream, w.sf64[0].ptr, source, 1.0);
+      c.push_initial({source});
+    }
+  }
+  BcDev dev(Ctx& c) {
+    Worker& w = *c.w;
+    return {w.su32[0].ptr, w.sf64[0].ptr, w.sf64[1].ptr, w.su32[3].ptr, w.su32[2].ptr,
+            c.owner_view(), (uint32_t)c.iter, phase};
+  }
+  int phase_at_body = kFwd;
+  void body(Ctx& c) {  // primitives.cpp:543-625
+    Worker& w = *c.w;
+    const bool first = c.worker() == c.P->local_workers.front();
+    if (first && phase == kFwd && c.prev && c.prev->total_next == 0 &&
+        c.prev->inflight_records == 0) {
+      phase = kBwd;
+      backward_from = c.iter;
+      max_level = (uint32_t)c.prev->max_u(0);
+    }
+    if (first && phase == kBwd && c.iter - backward_from >= max_level) phase = kDone;
+    uint32_t nh = (uint32_t)w.hosted_host.size();
+    if (phase == kFwd) {
+      c.pipeline(dev(c), w.nv);
+      if (nh)
+        MGB_LAUNCH(max_hosted_label_kernel, grid_for(nh, 256, kNumSMs * 4), 256, 0, w.stream,
+                   w.su32[0].ptr, w.hosted.ptr, nh, c.ctr());
+      c.report.u[1] = kFwd;
+      c.report.u[0] = 0;  // filled from the device counter
+      return;
+    }
+    if (phase == kBwd) {
+      uint32_t level = max_level - (uint32_t)(c.iter - backward_from);
+      c.ensure_output(nh);
+      if (nh)
+        MGB_LAUNCH(bc_backward_kernel, grid_for(nh, 256, kNumSMs * 16), 256, 0, w.stream,
+                   w.graph(), w.hosted.ptr, nh, w.su32[0].ptr, w.sf64[0].ptr, w.sf64[1].ptr,
+                   w.sf64[2].ptr, w.su32[3].ptr, level, (uint32_t)c.iter, source,
+                   level < max_level ? 1 : 0, c.owner_view(), w.output.ptr, c.ctr());
+      c.report.u[0] = max_level;
+      c.report.u[1] = kBwd;
+      return;
+    }
+    c.report.u[0] = max_level;
+    c.report.u[1] = kDone;
+  }
+  int comm_selector(Ctx&, int) {
+    return phase == kFwd ? MG_COMM_SELECTIVE : MG_COMM_BROADCAST;
+  }
+  bool stop_condition(const GlobalView& v) {  // primitives.cpp:632-635
+    return v.all_u_equal(1, kDone) && v.total_next == 0 && v.inflight_records == 0;
+  }
+};
+
+// ===========================================================================
+// PageRank (primitives.cpp:697-827)
+
+struct PrDev {
+  double* accum;
+  const uint32_t* border_dst;
+  __device__ bool visit(uint32_t, uint32_t, uint32_t) const { return false; }
+  __device__ bool keep(uint32_t) const { return true; }
+  __device__ bool combine(uint32_t v, const uint32_t*, const double* vv, uint32_t) const {
+    atomicAdd(&accum[v], vv[0]);
+    return false;  // ranks are combined, never enqueued
+  }
+  __device__ void gather(uint32_t v, uint32_t*, double* vv) const {
+    vv[0] = accum[v];
+    accum[v] = 0.0;  // partial shipped
+  }
+  __device__ bool send_filter(uint32_t, uint32_t) const { return true; }
+  // the output is the static border list: entry i's destination-local ID
+  __device__ uint32_t peer_id(uint32_t, uint32_t, uint32_t i) const { return border_dst[i]; }
+};
+
+// pr_update (primitives.cpp:697-711) fused with zeroing the hosted accumulators
+__global__ void pr_update_kernel(const uint32_t* __restrict__ hosted, uint32_t nh, double* rank,
+                                 double* accum, double base, double damping, double dangling_n,
+                                 int update, Counters* ctr) {
+  double dmax = 0.0, sum = 0.0;
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < nh; i += gridDim.x * blockDim.x) {
+    uint32_t v = hosted[i];
+    if (update) {
+      double nr = base + damping * (accum[v] + dangling_n);
+      double rel = fabs(nr - rank[v]) / fmax(nr, 1e-300);
+      dmax = fmax(dmax, rel);
+      rank[v] = nr;
+      sum += nr;
+    }
+    accum[v] = 0.0;
+  }
+  if (!update) return;
+  for (int o = 16; o > 0; o >>= 1) {
+    dmax = fmax(dmax, __shfl_xor_sync(0xffffffffu, dmax, o));
+    sum += __shfl_xor_sync(0xffffffffu, sum, o);
+  }
+  if (lane_id() == 0) {
+    atomic_max_pos_f64(&ctr->f[1], dmax);
+    atomicAdd(&ctr->f[2], sum);
+  }
+}
+
+// push rank/outdegree into every out-neighbour; dangling mass aside
+// (primitives.cpp:762-778).  One warp per hosted vertex, lanes over its arcs.
+__global__ void __launch_bounds__(256)
+    pr_push_kernel(GraphView g, const uint32_t* __restrict__ hosted, uint32_t nh,
+                   const double* rank, double* accum, Counters* ctr) {
+  const uint32_t warps = gridDim.x * blockDim.x / 32;
+  uint32_t wid = (blockIdx.x * blockDim.x + threadIdx.x) / 32;
+  double dangling = 0.0;
+  unsigned long long scanned = 0;
+  for (uint32_t i = wid; i < nh; i += warps) {
+    uint32_t v = hosted[i];
+    uint32_t b = g.off[v], e = g.off[v + 1];
+    if (e == b) {
+      if (lane_id() == 0) dangling += rank[v];
+      continue;
+    }
+    double contrib = rank[v] / (double)(e - b);
+    for (uint32_t k = b + lane_id(); k < e; k += 32) atomicAdd(&accum[g.col[k]], contrib);
+    if (lane_id() == 0) scanned += e - b;
+  }
+  for (int o = 16; o > 0; o >>= 1) dangling += __shfl_xor_sync(0xffffffffu, dangling, o);
+  if (lane_id() == 0) {
+    if (dangling != 0.0) atomicAdd(&ctr->f[0], dangling);
+    if (scanned) atomicAdd(&ctr->edges, scanned);
+  }
+}
+
+__global__ void copy_border_kernel(const uint32_t* border, uint32_t n, uint32_t* out,
+                                   Counters* ctr) {
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
+    out[i] = border[i];
+  if (blockIdx.x == 0 && threadIdx.x == 0) ctr->out_cnt = n;
+}
+
+struct PrPrim : PrimBase {
+  double damping, epsilon;
+  uint64_t max_iter;
+  uint64_t updates = 0;
+  std::vector<double> rank_sums;
+  PrPrim(double d, double e, uint64_t m) : damping(d), epsilon(e), max_iter(m) {
+    name = "pr";
+    nvv = 1;
+    dup_required = -1;  // duplicate-all or duplicate-1-hop
+    has_stop_condition = true;
+  }
+  uint64_t inbox_bound(Plan& P, uint32_t src, uint32_t dst, int) const {
+    return P.pair_border[src][dst];
+  }
+  void init(Ctx& c) {  // primitives.cpp:728-745
+    Worker& w = *c.w;
+    fill(w.sf64[0], w.nv, 0, w.stream);  // rank
+    fill(w.sf64[1], w.nv, 0, w.stream);  // accum
+    uint32_t nh = (uint32_t)w.hosted_host.size();
+    if (nh)
+      MGB_LAUNCH(fill_hosted_f64_kernel, grid_for(nh, 256), 256, 0, w.stream, w.sf64[0].ptr,
+                 w.hosted.ptr, nh, 1.0 / (double)c.P->nv);
+  }
+  PrDev dev(Ctx& c) { return {c.w->sf64[1].ptr, c.w->border_dst.ptr}; }
+  void update(Ctx& c, double dangling_prev, bool do_update) {
+    Worker& w = *c.w;
+    const double n = (double)c.P->nv;
+    uint32_t nh = (uint32_t)w.hosted_host.size();
+    if (nh)
+      MGB_LAUNCH(pr_update_kernel, grid_for(nh, 256, kNumSMs * 8), 256, 0, w.stream, w.hosted.ptr,
+                 nh, w.sf64[0].ptr, w.sf64[1].ptr, (1.0 - damping) / n, damping,
+                 dangling_prev / n, do_update ? 1 : 0, c.ctr());
+  }
+  void body(Ctx& c) {  // primitives.cpp:747-782
+    Worker& w = *c.w;
+    const bool first = c.worker() == c.P->local_workers.front();
+    if (c.iter >= 1) {
+      update(c, c.prev->sum_f(0), true);
+      if (first) ++updates;
+    } else {
+      update(c, 0.0, false);  // zero hosted accum only
+      c.report.f[1] = INFINITY;
+    }
+    if (first && c.worker() == 0 && c.prev && c.iter >= 2) rank_sums.push_back(c.prev->sum_f(2));
+    uint32_t nh = (uint32_t)w.hosted_host.size();
+    if (nh)
+      MGB_LAUNCH(pr_push_kernel, grid_for((uint64_t)nh * 32, 256, kNumSMs * 16), 256, 0,
+                 w.stream, w.graph(), w.hosted.ptr, nh, w.sf64[0].ptr, w.sf64[1].ptr, c.ctr());
+    uint32_t nb = (uint32_t)w.border.n;
+    c.ensure_output(nb);
+    if (nb)
+      MGB_LAUNCH(copy_border_kernel, grid_for(nb, 256), 256, 0, w.stream, w.border.ptr, nb,
+                 w.output.ptr, c.ctr());
+  }
+  bool stop_condition(const GlobalView& v) {  // primitives.cpp:796-799
+    if (v.iteration + 1 >= max_iter) return true;
+    return v.iteration >= 1 && v.max_f(1) < epsilon;
+  }
+  void finalize(Ctx& c, const GlobalView& last) {  // primitives.cpp:801-810
+    bool delta_stopped = last.iteration >= 1 && last.max_f(1) < epsilon;
+    const bool first = c.worker() == c.P->local_workers.front();
+    if (first && c.worker() == 0 && last.iteration >= 1) rank_sums.push_back(last.sum_f(2));
+    if (!delta_stopped) {
+      MGB_CUDA(cudaMemsetAsync(c.ctr(), 0, sizeof(Counters), c.w->stream));
+      update(c, last.sum_f(0), true);
+      if (first) ++updates;
+    }
+  }
+};
+
+// ---------------------------------------------------------------------------
+// C-ABI plumbing
+
+thread_local std::string t_err;
+
+template <class F>
+int guarded(F&& f) {
+  try {
+    f();
+    return MG_OK;
+  } catch (const Error& e) {
+    t_err = e.what();
+    return e.code;
+  } catch (const std::bad_alloc&) {
+    t_err = "host allocation failed";
+    return MG_ECAPACITY;
+  } catch (const std::exception& e) {
+    t_err = e.what();
+    return MG_EWORKER;
+  }
+}
+
+void check_source(Plan& P, uint32_t s, const char* prim) {  // primitives.cpp:27-30
+  if (s >= P.nv) throw Error(MG_EINVAL, std::string(prim) + ": source out of range");
+}
+
+mg_config cfg_or_default(const mg_config* c) {
+  mg_config d;
+  mg_config_default(&d);
+  return c ? *c : d;
+}
+
+void finish_stats(Plan& P, mg_stats* st) {
+  if (st) *st = P.last;
+}
+
+template <class T, size_t N>
+std::vector<const T*> pw(Plan& P, DevArray<T> (Worker::*arr)[N], int idx) {
+  std::vector<const T*> v(P.n, nullptr);
+  for (uint32_t p : P.local_workers) v[p] = (P.workers[p].get()->*arr)[idx].ptr;
+  return v;
+}
+
+}  // namespace
+
+void set_error(const std::string& msg) { t_err = msg; }
+const char* last_error() { return t_err.c_str(); }
+int run_guarded(const std::function<void()>& f) { return guarded(f); }
+
+}  // namespace mgb
+
+using namespace mgb;
+
+extern "C" {
+
+void mg_config_default(mg_config* cfg) {
+  std::memset(cfg, 0, sizeof(*cfg));
+  cfg->policy = MG_POLICY_JUST;
+  cfg->fused = MG_FUSED_AUTO;
+  cfg->comm_override = MG_COMM_DEFAULT;
+  cfg->h_inflation = 1;
+  cfg->max_supersteps = 1000000;
+}
+
+int mg_bfs(mg_plan* plan, uint32_t source, int mark_preds, const mg_config* cfg, uint32_t* labels,
+           uint32_t* preds, mg_stats* stats) {
+  return guarded([&] {
+    Plan& P = *reinterpret_cast<Plan*>(plan);
+    check_source(P, source, "bfs");
+    mg_config c = cfg_or_default(cfg);
+    BfsPrim prim(source, mark_preds != 0);
+    P.last = mg_stats{};
+    run_primitive(P, prim, c);
+    P.last_result_kind = 0;
+    gather_u32(P, pw(P, &Worker::su32, 0), labels);
+    if (mark_preds) gather_u32(P, pw(P, &Worker::su32, 1), preds);
+    finish_stats(P, stats);
+  });
+}
+
+void mg_make_direction_state(int current, uint64_t q, uint64_t u, uint64_t p, uint64_t edges,
+                             uint64_t vertices, double do_a, double do_b, int switched_once,
+                             mg_direction_state* s) {
+  std::memset(s, 0, sizeof(*s));
+  s->current = current;
+  s->q_size = q;
+  s->u_size = u;
+  s->p_size = p;
+  s->do_a = do_a;
+  s->do_b = do_b;
+  s->switched_to_backward_once = switched_once;
+  if (vertices > 0) s->fv = (double)q * (double)edges / (double)vertices;
+  if (p > 0) s->bv = (double)u * (double)vertices / (double)p;
+}
+
+int mg_direction_decide(const mg_direction_state* s) {
+  if (s->current == 0) return (!s->switched_to_backward_once && s->fv > s->bv * s->do_a) ? 1 : 0;
+  return s->fv < s->bv * s->do_b ? 0 : 1;
+}
+
+int mg_dobfs(mg_plan* plan, uint32_t source, double do_a, double do_b, int mark_preds,
+             const mg_config* cfg, uint32_t* labels, uint32_t* preds, int32_t* direction_log,
+             uint64_t cap, uint64_t* len, uint64_t* forward_edges, uint64_t* backward_edges,
+             mg_stats* stats) {
+  return guarded([&] {
+    Plan& P = *reinterpret_cast<Plan*>(plan);
+    check_source(P, source, "dobfs");
+    mg_config c = cfg_or_default(cfg);
+    DobfsPrim prim(source, do_a, do_b, mark_preds != 0);
+    P.last = mg_stats{};
+    run_primitive(P, prim, c);
+    P.last_result_kind = 0;
+    gather_u32(P, pw(P, &Worker::su32, 0), labels);
+    if (mark_preds) gather_u32(P, pw(P, &Worker::su32, 1), preds);
+    if (len) *len = prim.dir_log.size();
+    for (uint64_t i = 0; direction_log && i < prim.dir_log.size() && i < cap; ++i)
+      direction_log[i] = prim.dir_log[i];
+    uint64_t f = 0, b = 0;
+    for (size_t i = 0; i < prim.dir_log.size() && i < P.edges_per_iter.size(); ++i)
+      (prim.dir_log[i] ? b : f) += P.edges_per_iter[i];
+    if (forward_edges) *forward_edges = f;
+    if (backward_edges) *backward_edges = b;
+    finish_stats(P, stats);
+  });
+}
+
+int mg_sssp(mg_plan* plan, uint32_t source, int mark_preds, const mg_config* cfg, uint64_t* dists,
+            uint32_t* preds, mg_stats* stats) {
+  return guarded([&] {
+    Plan& P = *reinterpret_cast<Plan*>(plan);
+    check_source(P, source, "sssp");
+    if (!P.weighted && P.ne > 0) throw Error(MG_EINVAL, "sssp: graph has no edge weights");
+    mg_config c = cfg_or_default(cfg);
+    SsspPrim prim(source, mark_preds != 0);
+    P.last = mg_stats{};
+    run_primitive(P, prim, c);
+    P.last_result_kind = 2;
+    gather_u64(P, pw(P, &Worker::su64, 0), dists);
+    if (mark_preds) gather_u32(P, pw(P, &Worker::su32, 1), preds);
+    finish_stats(P, stats);
+  });
+}
+
+int mg_cc(mg_plan* plan, const mg_config* cfg, uint32_t* components, mg_stats* stats) {
+  return guarded([&] {
+    Plan& P = *reinterpret_cast<Plan*>(plan);
+    mg_config c = cfg_or_default(cfg);
+    CcPrim prim;
+    P.last = mg_stats{};
+    run_primitive(P, prim, c);
+    P.last_result_kind = 3;
+    gather_u32(P, pw(P, &Worker::su32, 0), components);
+    finish_stats(P, stats);
+  });
+}
+
+int mg_bc(mg_plan* plan, uint32_t source, const mg_config* cfg, double* bc, double* sigma,
+          uint32_t* labels, mg_stats* stats) {
+  return guarded([&] {
+    Plan& P = *reinterpret_cast<Plan*>(plan);
+    check_source(P, source, "bc");
+    mg_config c = cfg_or_default(cfg);
+    BcPrim prim(source);
+    P.last = mg_stats{};
+    run_primitive(P, prim, c);
+    P.last_result_kind = 4;
+    gather_f64(P, pw(P, &Worker::sf64, 2), bc);
+    gather_f64(P, pw(P, &Worker::sf64, 0), sigma);
+    gather_u32(P, pw(P, &Worker::su32, 0), labels);
+    finish_stats(P, stats);
+  });
+}
+
+int mg_pagerank(mg_plan* plan, double damping, double epsilon, uint64_t max_iter,
+                const mg_config* cfg, double* ranks, uint64_t* iterations, double* rank_sums,
+                uint64_t cap, uint64_t* len, mg_stats* stats) {
+  return guarded([&] {
+    Plan& P = *reinterpret_cast<Plan*>(plan);
+    if (!(damping > 0.0 && damping < 1.0))
+      throw Error(MG_EINVAL, "pagerank: damping must lie in (0,1)");
+    if (!(epsilon > 0.0)) throw Error(MG_EINVAL, "pagerank: epsilon must be positive");
+    if (max_iter < 1) throw Error(MG_EINVAL, "pagerank: max_iter must be >= 1");
+    mg_config c = cfg_or_default(cfg);
+    PrPrim prim(damping, epsilon, max_iter);
+    P.last = mg_stats{};
+    run_primitive(P, prim, c);
+    P.last_result_kind = 6;
+    std::vector<double> host(ranks ? 0 : P.nv);
+    double* out = ranks ? ranks : host.data();
+    gather_f64(P, pw(P, &Worker::sf64, 0), out);
+    std::vector<double> sums = prim.rank_sums;
+    bool finalized = prim.updates > P.last.supersteps - 1;  // primitives.cpp:820-825
+    if (finalized) {
+      double s = 0.0;
+      for (uint32_t v = 0; v < P.nv; ++v) s += out[v];
+      sums.push_back(s);
+    }
+    if (iterations) *iterations = prim.updates;
+    if (len) *len = sums.size();
+    for (uint64_t i = 0; rank_sums && i < sums.size() && i < cap; ++i) rank_sums[i] = sums[i];
+    finish_stats(P, stats);
+  });
+}
+
+int mg_plan_fetch(mg_plan* plan, int which, void* host_out) {
+  return guarded([&] {
+    Plan& P = *reinterpret_cast<Plan*>(plan);
+    switch (which) {
+      case MG_RES_LABELS: gather_u32(P, pw(P, &Worker::su32, 0), (uint32_t*)host_out); break;
+      case MG_RES_PREDS: gather_u32(P, pw(P, &Worker::su32, 1), (uint32_t*)host_out); break;
+      case MG_RES_DISTS: gather_u64(P, pw(P, &Worker::su64, 0), (uint64_t*)host_out); break;
+      case MG_RES_COMPONENTS: gather_u32(P, pw(P, &Worker::su32, 0), (uint32_t*)host_out); break;
+      case MG_RES_BC: gather_f64(P, pw(P, &Worker::sf64, 2), (double*)host_out); break;
+      case MG_RES_SIGMA: gather_f64(P, pw(P, &Worker::sf64, 0), (double*)host_out); break;
+      case MG_RES_RANKS: gather_f64(P, pw(P, &Worker::sf64, 0), (double*)host_out); break;
+      default: throw Error(MG_EINVAL, "mg_plan_fetch: unknown result kind");
+    }
+  });
+}
+
+}  // extern "C"
