@@ -416,7 +416,7 @@ void run_primitive(Plan& P, Prim& prim, const mg_config& cfg) {
         for (uint32_t s = 0; s < n; ++s)
           if (s != p && w.slot_cap[s] > maxcap) maxcap = w.slot_cap[s];
         dim3 grid(grid_for(maxcap, 256, kNumSMs * 2), n);
-        MGB_LAUNCH(merge_kernel<decltype(dev)>, grid, 256, 0, w.stream, dev, w.slots[parity],
+        MGB_LAUNCH(merge_kernel<decltype(dev)>, grid, 256, 0, w.stream, dev, w.recv_table.ptr + parity * n,
                    w.inbox_cnt.ptr + parity * kMaxWorkers, p, (uint32_t)(iter + 1),
                    (uint32_t)iter, w.merge_stamp.ptr, w.next_input.ptr, w.ctr.ptr, w.graph(),
                    prim.nva, prim.nvv, 1);

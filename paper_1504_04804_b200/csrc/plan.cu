@@ -18,7 +18,7 @@ static void free_worker(Worker& w) {
   w.border.free_(); w.border_dst.free_();
   w.input.release(); w.next_input.release(); w.advance_out.release(); w.output.release();
   w.merge_stamp.free_(); w.big.free_(); w.big_prefix.free_(); w.arena.free_();
-  w.inbox_cnt.free_(); w.send_table.free_(); w.send_cnt_ptr.free_(); w.ctr.free_();
+  w.inbox_cnt.free_(); w.send_table.free_(); w.send_cnt_ptr.free_(); w.recv_table.free_(); w.ctr.free_();
   for (auto& a : w.su32) a.free_();
   for (auto& a : w.sf64) a.free_();
   for (auto& a : w.su64) a.free_();
@@ -168,8 +168,10 @@ void ensure_inboxes(Plan& P, Worker& w, int nva, int nvv, const std::vector<uint
   MGB_CUDA(cudaStreamSynchronize(w.stream));
   int ka = nva > w.nva ? nva : w.nva, kv = nvv > w.nvv ? nvv : w.nvv;
   std::vector<uint64_t> newcap(caps.size());
-  for (size_t s = 0; s < caps.size(); ++s)
-    newcap[s] = caps[s] > (s < w.slot_cap.size() ? w.slot_cap[s] : 0) ? caps[s] : w.slot_cap[s];
+  for (size_t s = 0; s < caps.size(); ++s) {
+    uint64_t have = s < w.slot_cap.size() ? w.slot_cap[s] : 0;
+    newcap[s] = caps[s] > have ? caps[s] : have;
+  }
   uint64_t tot = 0;
   for (uint64_t c : newcap) tot += c;
   if (tot == 0) {  // single worker: no peers, no inbox memory
@@ -227,6 +229,12 @@ void build_send_tables(Plan& P) {
     MGB_CUDA(cudaMemcpy(w.send_table.ptr, table.data(), sizeof(SlotView) * 2 * n,
                         cudaMemcpyHostToDevice));
     MGB_CUDA(cudaMemcpy(w.send_cnt_ptr.ptr, cnt.data(), sizeof(uint32_t*) * 2 * n,
+                        cudaMemcpyHostToDevice));
+    std::vector<SlotView> recv(2 * n);
+    for (int par = 0; par < 2; ++par)
+      for (uint32_t s = 0; s < n; ++s) recv[par * n + s] = w.slots[par][s];
+    if (!w.recv_table.ptr || w.recv_table.n != 2 * n) w.recv_table.alloc(2 * n);
+    MGB_CUDA(cudaMemcpy(w.recv_table.ptr, recv.data(), sizeof(SlotView) * 2 * n,
                         cudaMemcpyHostToDevice));
   }
 }

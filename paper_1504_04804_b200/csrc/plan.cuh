@@ -103,6 +103,7 @@ struct Worker {
   // sender side: where this worker's records for each peer go, per parity
   DevArray<SlotView> send_table;   // [2][n]
   DevArray<uint32_t*> send_cnt_ptr;  // [2][n] -> &inbox_cnt[parity][p] at peer
+  DevArray<SlotView> recv_table;     // [2][n] device copy of `slots` (merge kernel)
 
   // primitive state arrays (|V_i| entries each), reused across runs; results
   // of the last run stay here until the next run (mg_plan_fetch)
