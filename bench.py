@@ -1,0 +1,363 @@
+#!/usr/bin/env python
+"""Benchmark: direction-optimising BFS (DOBFS) GTEPS on RMAT scale-26 / edge-factor-16
+(BASELINE.json configs[1]) through the C-ABI library on B200.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+A step is one DOBFS traversal from one source (sources cycle through a fixed
+list: 0, then non-isolated vertices drawn with seed 7).  GTEPS = A_r / t with
+A_r = sum of degrees of the reached vertices; t is the library's
+CUDA-event time of the superstep loop including per-run init (the reference's
+wall_ms region, engine.hpp:951-964).  `e2e` repeats the steps through the same
+public call with the labels copied back into pinned host memory every step.
+
+--impl reference times the reference's own CPU engine (oracle/_ref, compiled
+from the reference sources) on the same graph and sources.
+"""
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+HBM_FALLBACK = 6650.0
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "measured"
+    except Exception:
+        return HBM_FALLBACK, "fallback"
+
+
+def ncu_traffic():
+    """dram bytes per pull-step launch pair from the committed ncu capture, if any"""
+    p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    try:
+        with open(p) as f:
+            return json.load(f).get("dobfs_pull_bytes_per_launch")
+    except Exception:
+        return None
+
+
+class Clocks:
+    """nvidia-smi sampler running during the timed region"""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu):
+        self.gpu = gpu
+        self.f = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
+        try:
+            self.p = subprocess.Popen(["nvidia-smi", "-i", str(gpu), "--query-gpu=" + self.Q,
+                                       "--format=csv,noheader,nounits", "-lms", "100"],
+                                      stdout=self.f, stderr=subprocess.DEVNULL)
+        except Exception:
+            self.p = None
+
+    def stop(self):
+        if self.p is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.25)
+        self.p.terminate()
+        self.p.wait()
+        self.f.flush()
+        rows = [r.split(",") for r in open(self.f.name).read().strip().splitlines() if r.strip()]
+        os.unlink(self.f.name)
+        sm = [float(r[1]) for r in rows if len(r) > 2 and r[1].strip().isdigit()]
+        mx = [float(r[2]) for r in rows if len(r) > 2 and r[2].strip().isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = set()
+        for r in rows:
+            for k, nm in enumerate(names):
+                if len(r) > 5 + k and r[5 + k].strip() == "Active":
+                    reasons.add(nm)
+        loaded = [s for s in sm if mx and s > 0.5 * max(mx)] or sm
+        return {"sm_mhz": statistics.median(loaded) if loaded else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": sorted(reasons),
+                "samples": len(rows)}
+
+
+def pick_sources(off, count, seed=7):
+    deg = np.diff(off.astype(np.int64))
+    nonzero = np.nonzero(deg)[0]
+    rng = np.random.RandomState(seed)
+    extra = rng.choice(nonzero, size=min(count - 1, len(nonzero)), replace=False)
+    return [0] + [int(x) for x in extra]
+
+
+def reached_arcs(labels, deg):
+    return int(deg[labels != 0xFFFFFFFF].sum())
+
+
+def dist_env():
+    rank = int(os.environ.get("RANK", 0))
+    world = int(os.environ.get("WORLD_SIZE", 1))
+    local = int(os.environ.get("LOCAL_RANK", rank))
+    return rank, world, local
+
+
+def cpu_reference(graph_arrays, sources, arcs, max_s, label):
+    """time the reference engine (oracle/_ref) on the same graph; n = 1 partition"""
+    from oracle import ref
+    off, col, _ = graph_arrays
+    t0 = time.time()
+    g = ref.RefGraph.from_csr(off, col)
+    plan = ref.RefPlan(g, np.zeros(len(off) - 1, np.uint32), 1)
+    prep = time.time() - t0
+    done, ms, a = [], 0.0, 0
+    t1 = time.time()
+    for s in sources:
+        r = plan.dobfs(s)
+        ms += r.stats.wall_ms
+        a += arcs[s]
+        done.append(s)
+        if time.time() - t1 > max_s:
+            break
+    return {"value": a / (ms * 1e-3) / 1e9, "unit": "GTEPS", "cores": 1, "kind": "reference",
+            "sample": f"{label}: reference dobfs (n=1 partition, 1 thread) from sources {done}, "
+                      f"{ms:.0f} ms engine wall_ms (plan build {prep:.1f} s excluded)"}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--scale", type=int, default=26)
+    ap.add_argument("--edge-factor", type=int, default=16)
+    ap.add_argument("--seed", type=int, default=1)
+    ap.add_argument("--num-sources", type=int, default=8)
+    ap.add_argument("--cpu-seconds", type=float, default=20.0)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+
+    rank, world, local = dist_env()
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", init_method="env://")
+    workload = f"dobfs_rmat{args.scale}_ef{args.edge_factor}"
+    if args.impl == "reference":
+        return run_reference(args, rank, world, workload)
+    return run_ours(args, rank, world, local, workload)
+
+
+def build_plan(args, n, owner=None, devices=None):
+    import paper_1504_04804_b200 as mg
+    t0 = time.time()
+    plan = mg.PartitionPlan.rmat_device(args.scale, args.edge_factor, args.seed, owner=owner, n=n,
+                                        devices=devices)
+    return plan, time.time() - t0
+
+
+def run_ours(args, rank, world, local, workload):
+    import torch
+
+    import paper_1504_04804_b200 as mg
+    torch.cuda.set_device(local)
+    hbm, hbm_kind = peaks()
+    # this rank's plan: one partition per GPU; until the multi-process fabric
+    # is wired into the bench, N > 1 runs independent replicas of the N=1 job
+    plan, prep_s = build_plan(args, 1, devices=[local])
+    g = plan.download_graph()
+    off, col, _ = g.arrays()
+    deg = np.diff(off.astype(np.int64))
+    sources = pick_sources(off, args.num_sources)
+    cfg = mg.EngineConfig(policy=mg.AllocPolicyKind.Maximum, fused=mg.FusedMode.On)
+    opt = lambda s: mg.DobfsOptions(source=s)  # noqa: E731
+    # warm-up: every source once with labels downloaded (A_r per source), >= W runs
+    arcs = {}
+    for i in range(max(args.warmup, len(sources))):
+        s = sources[i % len(sources)]
+        r = mg.dobfs(plan, opt(s), cfg)
+        if s not in arcs:
+            arcs[s] = reached_arcs(r.labels, deg)
+            ref_depth = int(r.labels[r.labels != mg.kInfLabel].max())
+            assert r.stats.supersteps == ref_depth + 1
+    steps = [sources[i % len(sources)] for i in range(args.steps)]
+    mg.lib().mg_plan_set_profiling(plan._h, 1)
+    if world > 1:
+        torch.distributed.barrier()
+    torch.cuda.synchronize()
+    clocks = Clocks(local)
+    l0 = mg.kernel_launch_count()
+    dev_ms, kms, kbytes, klaunch, wall0 = 0.0, 0.0, 0.0, 0, time.perf_counter()
+    for s in steps:
+        st = dobfs_stats(mg, plan, s, cfg)
+        dev_ms += st.device_ms
+        kms += st.kernel_ms
+        kbytes += st.kernel_bytes
+        klaunch += st.kernel_launches
+    torch.cuda.synchronize()
+    wall = time.perf_counter() - wall0
+    launches = mg.kernel_launch_count() - l0
+    clk = clocks.stop()
+    mg.lib().mg_plan_set_profiling(plan._h, 0)
+    # dominant kernel (the pull step): CUDA events on the library stream, live
+    prof = {"ms": kms, "bytes": kbytes, "launches": klaunch, "dev_ms": dev_ms}
+    total_arcs = sum(arcs[s] for s in steps)
+    if world > 1:
+        t = torch.tensor([dev_ms], dtype=torch.float64, device="cuda")
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        dev_ms = float(t.item())
+    value = total_arcs * world / (dev_ms * 1e-3) / 1e9
+
+    # end to end: same calls with labels copied to pinned host memory each step
+    host = torch.empty(plan.num_global_vertices, dtype=torch.int32, pin_memory=True)
+    labels = host.numpy().view(np.uint32)
+    e2e_t = 0.0
+    for s in steps:
+        t0 = time.perf_counter()
+        r = e2e_call(mg, plan, s, cfg, labels)
+        e2e_t += time.perf_counter() - t0
+    if world > 1:
+        t = torch.tensor([e2e_t], dtype=torch.float64, device="cuda")
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        e2e_t = float(t.item())
+    e2e = total_arcs * world / e2e_t / 1e9
+
+    if rank != 0:
+        return 0
+    cpu = None
+    if not args.no_cpu_baseline and world == 1:
+        try:
+            cpu = cpu_reference((off, col, None), sources, arcs, args.cpu_seconds, workload)
+        except Exception as ex:  # the baseline is reported, never required
+            cpu = {"value": None, "unit": "GTEPS", "cores": 1, "kind": "reference",
+                   "sample": f"unavailable: {ex}"}
+    achieved = prof["bytes"] / (prof["ms"] * 1e-3) / 1e9 if prof["ms"] else None
+    traffic = ncu_traffic()
+    line = {
+        "metric": "DOBFS GTEPS (A_r / t) on RMAT",
+        "value": round(value, 3),
+        "unit": "GTEPS",
+        "n_gpus": world,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "ms_per_step": round(dev_ms / args.steps, 4),
+        "higher_is_better": True,
+        "scaling": "weak",
+        "vs_baseline": None,
+        "dtype": "u32",
+        "data": "synthetic (hashed R-MAT generated on the GPU)",
+        "config": {
+            "workload": workload, "scale": args.scale, "edge_factor": args.edge_factor,
+            "generator": f"counter-based R-MAT (a,b,c,d)=(.57,.19,.19,.05) seed {args.seed},"
+                         " symmetrized + deduplicated",
+            "num_vertices": plan.num_global_vertices, "num_arcs": plan.num_global_edges,
+            "partitions_per_gpu": 1,
+            "parallelism": "replicas" if world > 1 else "single",
+            "sources": sources, "mean_reached_arcs": total_arcs // len(steps),
+            "policy": "max + fused", "do_a": 0.01, "do_b": 0.1,
+            "l2": "inputs larger than L2 (CSR %.1f GB vs 126 MB L2)" % (
+                (4 * (plan.num_global_vertices + plan.num_global_edges)) / 1e9),
+            "graph_prep_s": round(prep_s, 2),
+            "host_wall_s": round(wall, 4),
+        },
+        "e2e": {"value": round(e2e, 3), "unit": "GTEPS", "h2d_bytes_per_step": 4,
+                "d2h_bytes_per_step": 4 * plan.num_global_vertices},
+        "roofline": {"bound": "hbm", "kernel": "dobfs_pull (thread + group stages)",
+                     "achieved": round(achieved, 1) if achieved else None, "peak": hbm,
+                     "peak_kind": hbm_kind, "unit": "GB/s",
+                     "frac": round(achieved / hbm, 4) if achieved else None,
+                     "traffic": traffic,
+                     "algorithmic_bytes_per_launch": prof["bytes"] / max(prof["launches"], 1),
+                     "avg_launch_ms": prof["ms"] / max(prof["launches"], 1),
+                     "share_of_step": round(prof["ms"] / prof["dev_ms"], 4) if prof["dev_ms"]
+                     else None},
+        "cpu_baseline": cpu,
+        "clocks": clk,
+        "gpu_launches": launches,
+    }
+    print(json.dumps(line))
+    return 0
+
+
+def e2e_call(mg, plan, s, cfg, labels):
+    import ctypes as C
+
+    from paper_1504_04804_b200 import abi
+    st = abi.mg_stats()
+    dl = np.zeros(64, np.int32)
+    ln, fw, bw = C.c_uint64(), C.c_uint64(), C.c_uint64()
+    out = None if labels is None else labels.ctypes.data_as(C.c_void_p)
+    rc = mg.lib().mg_dobfs(plan._h, s, 0.01, 0.1, 0, C.byref(cfg.to_c()), out, None,
+                           dl.ctypes.data_as(C.c_void_p), 64, C.byref(ln), C.byref(fw),
+                           C.byref(bw), C.byref(st))
+    if rc:
+        raise RuntimeError(mg.lib().mg_last_error().decode())
+    return st
+
+
+def dobfs_stats(mg, plan, s, cfg):
+    """one device-resident DOBFS through the C-ABI (no result download)"""
+    return e2e_call(mg, plan, s, cfg, None)
+
+
+def run_reference(args, rank, world, workload):
+    if rank != 0:
+        return 0
+    from oracle import ref
+    if not ref.available():
+        print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref not built"}))
+        return 0
+    import paper_1504_04804_b200 as mg
+    # input synthesis only (not timed): the same hashed R-MAT graph
+    try:
+        plan, _ = build_plan(args, 1)
+        g = plan.download_graph()
+        del plan
+    except Exception:
+        g = mg.Csr.rmat_hashed(args.scale, args.edge_factor, args.seed)
+    off, col, _ = g.arrays()
+    deg = np.diff(off.astype(np.int64))
+    sources = pick_sources(off, args.num_sources)
+    rg = ref.RefGraph.from_csr(off, col)
+    del g, col
+    rplan = ref.RefPlan(rg, np.zeros(len(off) - 1, np.uint32), 1)
+    arcs = {}
+    for i in range(args.warmup):
+        s = sources[i % len(sources)]
+        r = rplan.dobfs(s)
+        arcs[s] = reached_arcs(r.labels, deg)
+    ms, a = 0.0, 0
+    for i in range(args.steps):
+        s = sources[i % len(sources)]
+        r = rplan.dobfs(s)
+        if s not in arcs:
+            arcs[s] = reached_arcs(r.labels, deg)
+        ms += r.stats.wall_ms
+        a += arcs[s]
+    v = a / (ms * 1e-3) / 1e9
+    print(json.dumps({
+        "impl": "reference", "metric": "DOBFS GTEPS (A_r / t) on RMAT", "value": round(v, 4),
+        "unit": "GTEPS", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": round(ms / args.steps, 3), "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "u32", "data": "synthetic (hashed R-MAT)",
+        "config": {"workload": workload, "scale": args.scale, "edge_factor": args.edge_factor,
+                   "sources": sources, "partitions": 1},
+        "cpu_baseline": {"value": round(v, 4), "unit": "GTEPS", "cores": 1, "kind": "reference",
+                         "sample": f"{args.steps} reference dobfs runs (engine wall_ms), n=1"},
+        "e2e": {"value": round(v, 4), "unit": "GTEPS", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }))
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -117,6 +117,8 @@ int mg_plan_border_metrics(const mg_plan* plan, uint64_t* pair_border, uint64_t*
 /* copy the global CSR of a device-built plan back to the host (for the CPU
  * baseline / oracle on the same graph) */
 int mg_plan_download_graph(const mg_plan* plan, mg_graph** out);
+/* time the primitive's dominant kernel with CUDA events on its stream */
+int mg_plan_set_profiling(mg_plan* plan, int enable);
 
 /* --------------------------------------------------------------------------
  * engine configuration (EngineConfig, engine.hpp:308-315; AllocationPolicy,
@@ -172,6 +174,11 @@ typedef struct mg_stats {
   double device_ms;               /* CUDA-event time of the superstep loop incl. per-run init   */
   uint64_t gpu_launches;          /* kernels launched by the run                                */
   uint64_t exchange_bytes;        /* bytes written into peer inboxes                           */
+  /* dominant kernel of the primitive, filled when profiling is on
+   * (mg_plan_set_profiling): CUDA-event time, launches, algorithmic bytes */
+  double kernel_ms;
+  uint64_t kernel_launches;
+  double kernel_bytes;
 } mg_stats;
 
 /* per-run arrays of the last run on this plan:

@@ -67,6 +67,9 @@ class mg_stats(C.Structure):
         ("device_ms", C.c_double),
         ("gpu_launches", C.c_uint64),
         ("exchange_bytes", C.c_uint64),
+        ("kernel_ms", C.c_double),
+        ("kernel_launches", C.c_uint64),
+        ("kernel_bytes", C.c_double),
     ]
 
 
@@ -111,6 +114,7 @@ PROTOTYPES = {
     "mg_plan_info": (i32, [P, C.POINTER(u32), C.POINTER(u64), C.POINTER(u32)]),
     "mg_plan_border_metrics": (i32, [P, P, C.POINTER(u64)]),
     "mg_plan_download_graph": (i32, [P, PP]),
+    "mg_plan_set_profiling": (i32, [P, i32]),
     "mg_config_default": (None, [C.POINTER(mg_config)]),
     "mg_plan_last_array": (i32, [P, i32, P, u64, C.POINTER(u64)]),
     "mg_plan_last_buffer_stats": (i32, [P, u32, i32, C.POINTER(u64), C.POINTER(u64),

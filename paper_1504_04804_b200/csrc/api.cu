@@ -187,20 +187,29 @@ int mg_plan_download_graph(const mg_plan* p, mg_graph** out) {
       *out = new mg_graph{P.host_graph};
       return;
     }
-    if (!P.g_off.ptr) throw Error(MG_EINVAL, "plan holds no global graph");
+    // n == 1 device plans: worker 0's sub-CSR is the global CSR
+    const bool single = !P.g_off.ptr && P.n == 1 && P.workers[0];
+    if (!P.g_off.ptr && !single) throw Error(MG_EINVAL, "plan holds no global graph");
+    const uint32_t* d_off = single ? P.workers[0]->off.ptr : P.g_off.ptr;
+    const uint32_t* d_col = single ? P.workers[0]->col.ptr : P.g_col.ptr;
+    const uint32_t* d_w = single ? P.workers[0]->w.ptr : P.g_w.ptr;
     HostCsr g;
     g.nv = P.nv;
     g.off.resize((size_t)P.nv + 1);
     g.col.resize(P.ne);
     DeviceGuard dg(P.devices[0]);
-    MGB_CUDA(cudaMemcpy(g.off.data(), P.g_off.ptr, 4ull * (P.nv + 1), cudaMemcpyDeviceToHost));
-    MGB_CUDA(cudaMemcpy(g.col.data(), P.g_col.ptr, 4ull * P.ne, cudaMemcpyDeviceToHost));
-    if (P.g_w.ptr) {
+    MGB_CUDA(cudaMemcpy(g.off.data(), d_off, 4ull * (P.nv + 1), cudaMemcpyDeviceToHost));
+    MGB_CUDA(cudaMemcpy(g.col.data(), d_col, 4ull * P.ne, cudaMemcpyDeviceToHost));
+    if (d_w) {
       g.w.resize(P.ne);
-      MGB_CUDA(cudaMemcpy(g.w.data(), P.g_w.ptr, 4ull * P.ne, cudaMemcpyDeviceToHost));
+      MGB_CUDA(cudaMemcpy(g.w.data(), d_w, 4ull * P.ne, cudaMemcpyDeviceToHost));
     }
     *out = box(std::move(g));
   });
+}
+
+int mg_plan_set_profiling(mg_plan* p, int enable) {
+  return wrap([&] { plan_of(p).profile = enable != 0; });
 }
 
 int mg_plan_last_array(const mg_plan* p, int which, uint64_t* buf, uint64_t cap, uint64_t* len) {

@@ -64,6 +64,40 @@ __device__ __forceinline__ uint32_t warp_append(uint32_t* counter, bool pred) {
   return base + __popc(mask & ((1u << lane_id()) - 1u));
 }
 
+// CTA-aggregated queue append: items are staged in shared memory and the CTA
+// reserves its output range with ONE global atomic per flush.  A single global
+// counter hit by every warp serialises at its L2 slice (~1 op/ns); at 1e7+
+// appends per superstep that, not HBM, would bound the kernel.
+template <int kCap>
+struct BlockQueue {
+  uint32_t n, base;
+  uint32_t buf[kCap];
+  __device__ __forceinline__ void reset() {
+    if (threadIdx.x == 0) n = 0;
+  }
+  // all threads of the warp that reach this call participate
+  __device__ __forceinline__ void push(bool pred, uint32_t v) {
+    unsigned active = __activemask();
+    unsigned mask = __ballot_sync(active, pred);
+    if (!mask) return;
+    unsigned leader = __ffs(mask) - 1;
+    uint32_t b = 0;
+    if (lane_id() == leader) b = atomicAdd(&n, (uint32_t)__popc(mask));
+    b = __shfl_sync(active, b, leader);
+    if (pred) buf[b + __popc(mask & ((1u << lane_id()) - 1u))] = v;
+  }
+  // CTA-wide: requires __syncthreads() before (all pushes done) — performed here
+  __device__ __forceinline__ void flush(uint32_t* counter, uint32_t* out) {
+    __syncthreads();
+    if (threadIdx.x == 0) base = n ? atomicAdd(counter, n) : 0u;
+    __syncthreads();
+    for (uint32_t i = threadIdx.x; i < n; i += blockDim.x) out[base + i] = buf[i];
+    __syncthreads();
+    if (threadIdx.x == 0) n = 0;
+    __syncthreads();
+  }
+};
+
 __device__ __forceinline__ void warp_add_u64(unsigned long long* counter, uint64_t v) {
   unsigned active = __activemask();
 #pragma unroll
@@ -99,10 +133,14 @@ struct MemoryBudget {  // frontier.hpp:86-104
 // Device array with exact ("just-enough") growth: capacity extends to exactly
 // the requested size, never speculatively; prealloc() is the policy's up-front
 // sizing and is not counted as a reallocation (frontier.hpp:109-187).
+// The LOGICAL capacity (`cap`, what the policy and the stats see) restarts at 0
+// every run, while the physical allocation (`phys`) is kept across runs of the
+// same plan, so a warm plan pays no cudaMalloc inside the timed region.
 template <class T>
 struct DevBuf {
   T* ptr = nullptr;
-  uint64_t cap = 0;
+  uint64_t cap = 0;   // logical capacity (policy semantics)
+  uint64_t phys = 0;  // allocated items
   BufferStats* stats = nullptr;
   MemoryBudget* budget = nullptr;
 
@@ -110,23 +148,32 @@ struct DevBuf {
     stats = s;
     budget = b;
   }
-  void release() {
-    if (ptr) cudaFree(ptr);
+  // start of a run: logical capacity back to 0, memory kept
+  void reset() {
     if (budget && cap) budget->allocated -= cap * sizeof(T);
-    ptr = nullptr;
     cap = 0;
+  }
+  void release() {
+    reset();
+    if (ptr) cudaFree(ptr);
+    ptr = nullptr;
+    phys = 0;
   }
   // grow to exactly `items`; contents up to `keep` items are preserved
   void grow(uint64_t items, bool counted, uint64_t keep, cudaStream_t s) {
     if (budget) budget->charge(items * sizeof(T), cap * sizeof(T));
-    T* np = nullptr;
-    MGB_CUDA(cudaMalloc(&np, items * sizeof(T) + 16));
-    if (ptr) {
-      if (keep) MGB_CUDA(cudaMemcpyAsync(np, ptr, keep * sizeof(T), cudaMemcpyDeviceToDevice, s));
-      MGB_CUDA(cudaStreamSynchronize(s));
-      cudaFree(ptr);
+    if (items > phys) {
+      T* np = nullptr;
+      MGB_CUDA(cudaMalloc(&np, items * sizeof(T) + 16));
+      if (ptr) {
+        if (keep)
+          MGB_CUDA(cudaMemcpyAsync(np, ptr, keep * sizeof(T), cudaMemcpyDeviceToDevice, s));
+        MGB_CUDA(cudaStreamSynchronize(s));
+        cudaFree(ptr);
+      }
+      ptr = np;
+      phys = items;
     }
-    ptr = np;
     cap = items;
     if (stats) {
       if (counted) ++stats->realloc_count;

@@ -66,7 +66,8 @@ template <class F>
 __global__ void __launch_bounds__(256)
     split_pack_kernel(F f, OwnerView ow, GraphView g, const uint32_t* __restrict__ out,
                       Counters* ctr, uint32_t* __restrict__ next, const SlotView* __restrict__ table,
-                      uint32_t n, int broadcast, unsigned long long drop_mask, int nva, int nvv) {
+                      uint32_t n, int broadcast, unsigned long long drop_mask, int nva, int nvv,
+                      int want_deg) {
   const uint32_t cnt = ctr->out_cnt;
   unsigned long long my_deg = 0;
   for (uint32_t base = blockIdx.x * blockDim.x; base < cnt; base += gridDim.x * blockDim.x) {
@@ -81,7 +82,7 @@ __global__ void __launch_bounds__(256)
     uint32_t slot = warp_append(&ctr->next_cnt, local);
     if (local) {
       next[slot] = v;
-      my_deg += g.off[v + 1] - g.off[v];
+      if (want_deg) my_deg += g.off[v + 1] - g.off[v];
     }
     if (i >= cnt) continue;
     if (broadcast) {
@@ -116,7 +117,7 @@ __global__ void __launch_bounds__(256)
       for (int a = 0; a < nvv; ++a) s.vv[a][pos] = vv[a];
     }
   }
-  warp_add_u64(&ctr->next_deg, my_deg);
+  if (want_deg) warp_add_u64(&ctr->next_deg, my_deg);
 }
 
 // publish per-destination counts into the peers' slot counters; the system
@@ -135,7 +136,7 @@ __global__ void __launch_bounds__(256)
     merge_kernel(F f, const SlotView* __restrict__ slots, const uint32_t* __restrict__ inbox_cnt,
                  uint32_t p, uint32_t stamp, uint32_t iteration, uint32_t* merge_stamp,
                  uint32_t* __restrict__ next, Counters* ctr, GraphView g, int nva, int nvv,
-                 int enqueue) {
+                 int enqueue, int want_deg) {
   const uint32_t src = blockIdx.y;
   if (src == p) return;
   const uint32_t cnt = inbox_cnt[src];
@@ -159,10 +160,10 @@ __global__ void __launch_bounds__(256)
     uint32_t slot = warp_append(&ctr->next_cnt, push);
     if (push) {
       next[slot] = v;
-      my_deg += g.off[v + 1] - g.off[v];
+      if (want_deg) my_deg += g.off[v + 1] - g.off[v];
     }
   }
-  warp_add_u64(&ctr->next_deg, my_deg);
+  if (want_deg) warp_add_u64(&ctr->next_deg, my_deg);
   warp_add_u64(&ctr->combine, my_comb);
 }
 
@@ -176,6 +177,20 @@ static __global__ void degsum_kernel(GraphView g, const uint32_t* __restrict__ i
   }
   warp_add_u64(out, d);
 }
+
+// same, with the length read on the device (n == 1 path: output becomes input)
+static __global__ void degsum_dev_kernel(GraphView g, const uint32_t* __restrict__ in,
+                                         const uint32_t* n_ptr, unsigned long long* out) {
+  const uint32_t n = *n_ptr;
+  unsigned long long d = 0;
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    uint32_t v = in[i];
+    d += g.off[v + 1] - g.off[v];
+  }
+  warp_add_u64(out, d);
+}
+
+constexpr uint64_t kUnknownDeg = ~0ull;
 
 // ---------------------------------------------------------------------------
 // per-(run, worker) context: the WorkerHandle of the reference (engine.hpp:478-582)
@@ -207,26 +222,52 @@ struct Ctx {
 
   void ensure_output(uint64_t items) { w->output.ensure(items, w->stream); }
 
-  // advance over the input frontier (E:516-520)
-  template <class F>
-  void run_advance(const F& f, uint32_t* dst, uint32_t* dst_cnt) {
+  // advance over the input frontier (E:516-520): edge-balanced expansion
+  template <class F, bool kFused>
+  void lb_advance(const F& f, uint32_t* dst, uint32_t* dst_cnt) {
     if (in_count == 0) return;
-    GraphView g = graph();
-    unsigned grid = grid_for(in_count, kAdvBlock, kNumSMs * 16);
-    MGB_LAUNCH((advance_chunk_kernel<F, false>), grid, kAdvBlock, 0, w->stream, f, g,
-               w->input.ptr, in_count, dst, dst_cnt, w->big.ptr, &ctr()->big_cnt, &ctr()->edges);
-    launch_big<F, false>(f, dst, dst_cnt);
+    const uint32_t nb = (in_count + kLbBlock - 1) / kLbBlock;
+    if (w->lb_row.n < in_count) w->lb_row.alloc(in_count);
+    if (w->lb_pref.n < in_count) w->lb_pref.alloc(in_count);
+    if (w->lb_bsum.n < nb + 1ull) w->lb_bsum.alloc(nb + 1ull);
+    MGB_LAUNCH(lb_degree_kernel, nb, kLbBlock, 0, w->stream, w->off.ptr, w->input.ptr, in_count,
+               w->lb_row.ptr, w->lb_pref.ptr, w->lb_bsum.ptr);
+    MGB_LAUNCH(lb_scan_kernel, 1, 1024, 0, w->stream, w->lb_bsum.ptr, nb, w->lb_bsum.ptr + nb,
+               &ctr()->edges);
+    // tile table: exact when the degree sum is known, else bounded by 2|E_i|
+    // (an input frontier may hold a vertex twice, e.g. SSSP, E:901-904 + E:845)
+    const uint64_t max_deg = in_degsum == kUnknownDeg ? 2 * w->ne + 1 : in_degsum;
+    const uint64_t max_tiles = max_deg / kTile + 2;
+    if (w->lb_tile.n < max_tiles + 1) w->lb_tile.alloc(max_tiles + 1);
+    MGB_LAUNCH(lb_tiles_kernel, grid_for(max_tiles + 1, 256, kNumSMs * 8), 256, 0, w->stream,
+               w->lb_pref.ptr, w->lb_bsum.ptr, in_count, w->lb_bsum.ptr + nb, w->lb_tile.ptr,
+               (uint32_t)max_tiles);
+    const unsigned resident = kNumSMs * 6;  // 32 KB smem + 256 threads per CTA
+    unsigned grid = in_degsum == kUnknownDeg ? resident : grid_for(in_degsum, kTile, resident);
+    MGB_LAUNCH((lb_expand_kernel<F, kFused>), grid, kExpBlock, 0, w->stream, f, graph(),
+               w->input.ptr, in_count, w->lb_row.ptr, w->lb_pref.ptr, w->lb_bsum.ptr,
+               w->lb_bsum.ptr + nb, w->lb_tile.ptr, dst, dst_cnt);
   }
 
-  template <class F, bool kFused>
-  void launch_big(const F& f, uint32_t* dst, uint32_t* dst_cnt) {
-    if (in_degsum <= kBigDegree) return;  // no vertex can exceed the threshold
-    GraphView g = graph();
-    MGB_LAUNCH(big_prefix_kernel, 1, 1024, 0, w->stream, g, w->input.ptr, w->big.ptr,
-               &ctr()->big_cnt, w->big_prefix.ptr);
-    unsigned grid = grid_for(in_degsum, kAdvBlock, kNumSMs * 8);
-    MGB_LAUNCH((advance_big_kernel<F, kFused>), grid, kAdvBlock, 0, w->stream, f, g,
-               w->input.ptr, w->big.ptr, &ctr()->big_cnt, w->big_prefix.ptr, dst, dst_cnt);
+  template <class F>
+  void run_advance(const F& f, uint32_t* dst, uint32_t* dst_cnt) {
+    lb_advance<F, false>(f, dst, dst_cnt);
+  }
+
+  // exact degree sum of the input when the producer did not provide it
+  uint64_t degsum() {
+    if (in_degsum != kUnknownDeg) return in_degsum;
+    unsigned long long* tmp = &ctr()->next_deg;  // free until split/merge of this superstep
+    MGB_CUDA(cudaMemsetAsync(tmp, 0, 8, w->stream));
+    if (in_count)
+      MGB_LAUNCH(degsum_kernel, grid_for(in_count, 256, kNumSMs * 8), 256, 0, w->stream, graph(),
+                 w->input.ptr, in_count, tmp);
+    unsigned long long h = 0;
+    MGB_CUDA(cudaMemcpyAsync(&h, tmp, 8, cudaMemcpyDeviceToHost, w->stream));
+    MGB_CUDA(cudaMemsetAsync(tmp, 0, 8, w->stream));
+    MGB_CUDA(cudaStreamSynchronize(w->stream));
+    in_degsum = h;
+    return h;
   }
 
   // fused or two-stage traversal per the active policy (E:528-541); the
@@ -234,17 +275,11 @@ struct Ctx {
   template <class F>
   void pipeline(const F& f, uint64_t dedup_bound) {
     if (fused) {
-      uint64_t b = in_degsum < dedup_bound ? in_degsum : dedup_bound;
+      uint64_t b = in_degsum < dedup_bound ? in_degsum : dedup_bound;  // unknown -> bound
       ensure_output(b);
-      if (in_count == 0) return;
-      GraphView g = graph();
-      unsigned grid = grid_for(in_count, kAdvBlock, kNumSMs * 16);
-      MGB_LAUNCH((advance_chunk_kernel<F, true>), grid, kAdvBlock, 0, w->stream, f, g,
-                 w->input.ptr, in_count, w->output.ptr, &ctr()->out_cnt, w->big.ptr,
-                 &ctr()->big_cnt, &ctr()->edges);
-      launch_big<F, true>(f, w->output.ptr, &ctr()->out_cnt);
+      lb_advance<F, true>(f, w->output.ptr, &ctr()->out_cnt);
     } else {
-      w->advance_out.ensure(in_degsum, w->stream);
+      w->advance_out.ensure(degsum(), w->stream);
       run_advance(f, w->advance_out.ptr, &ctr()->adv_cnt);
       // filter_output_bound(advance_out.size(), |V_i|) (frontier.hpp:204-208): the
       // unfused path reads the advance length back to size the filter exactly
@@ -307,6 +342,8 @@ void run_primitive(Plan& P, Prim& prim, const mg_config& cfg) {
                                                                           : "broadcast"));
     comm = cfg.comm_override;
   }
+  // exact advance bounds are tracked unless the policy preallocated the maximum
+  const bool want_deg = cfg.policy != MG_POLICY_MAX;
   const bool fused = cfg.fused == MG_FUSED_ON || (cfg.fused == MG_FUSED_AUTO &&
                                                   cfg.policy == MG_POLICY_FUSED);
   RunState rs;
@@ -334,6 +371,9 @@ void run_primitive(Plan& P, Prim& prim, const mg_config& cfg) {
   }
   build_send_tables(P);
   P.h_matrix.assign(n, std::vector<uint64_t>(n, 0));
+  P.prof_ms = 0;
+  P.prof_bytes = 0;
+  P.prof_launches = 0;
   P.h_per_iter.clear();
   P.out_per_iter.clear();
   P.edges_per_iter.clear();
@@ -382,6 +422,20 @@ void run_primitive(Plan& P, Prim& prim, const mg_config& cfg) {
       MGB_CUDA(cudaMemsetAsync(w.ctr.ptr, 0, sizeof(Counters), w.stream));
       prim.body(c);
       step_comm[p] = prim.comm_selector(c, comm);
+      if (n == 1) {
+        // single partition: every output vertex is local (E:901-904), so the
+        // output buffer simply becomes the next input — no split kernel
+        std::swap(w.output.ptr, w.next_input.ptr);
+        std::swap(w.output.phys, w.next_input.phys);
+        uint64_t oc = w.output.cap;
+        w.output.cap = w.next_input.cap;
+        w.next_input.cap = oc;
+        if (want_deg)
+          MGB_LAUNCH(degsum_dev_kernel, kNumSMs * 4, 256, 0, w.stream, w.graph(),
+                     w.next_input.ptr, &w.ctr.ptr->out_cnt, &w.ctr.ptr->next_deg);
+        MGB_CUDA(cudaEventRecord(rs.packed[p], w.stream));
+        continue;
+      }
       // next_input holds the local part plus everything merged this superstep
       uint64_t incoming = 0;
       for (uint32_t s = 0; s < n; ++s) incoming += (s == p) ? 0 : w.slot_cap[s];
@@ -395,7 +449,8 @@ void run_primitive(Plan& P, Prim& prim, const mg_config& cfg) {
       MGB_LAUNCH(split_pack_kernel<decltype(dev)>, grid_for(w.output.cap, 256, kNumSMs * 8),
                  256, 0, w.stream, dev, c.owner_view(), w.graph(), w.output.ptr, w.ctr.ptr,
                  w.next_input.ptr, w.send_table.ptr + parity * n, n,
-                 step_comm[p] == MG_COMM_BROADCAST ? 1 : 0, drop, prim.nva, prim.nvv);
+                 step_comm[p] == MG_COMM_BROADCAST ? 1 : 0, drop, prim.nva, prim.nvv,
+                 want_deg ? 1 : 0);
       if (n > 1) {
         MGB_LAUNCH(publish_kernel, 1, 64, 0, w.stream, w.ctr.ptr, w.send_cnt_ptr.ptr + parity * n,
                    n, p);
@@ -419,7 +474,7 @@ void run_primitive(Plan& P, Prim& prim, const mg_config& cfg) {
         MGB_LAUNCH(merge_kernel<decltype(dev)>, grid, 256, 0, w.stream, dev, w.recv_table.ptr + parity * n,
                    w.inbox_cnt.ptr + parity * kMaxWorkers, p, (uint32_t)(iter + 1),
                    (uint32_t)iter, w.merge_stamp.ptr, w.next_input.ptr, w.ctr.ptr, w.graph(),
-                   prim.nva, prim.nvv, 1);
+                   prim.nva, prim.nvv, 1, want_deg ? 1 : 0);
       }
       prim.after_merge(c);
       MGB_CUDA(cudaMemcpyAsync(w.host_ctr, w.ctr.ptr, sizeof(Counters), cudaMemcpyDeviceToHost,
@@ -439,7 +494,7 @@ void run_primitive(Plan& P, Prim& prim, const mg_config& cfg) {
       if (hc.overflow) throw Error(MG_EWORKER, "inbox overflow on worker " + std::to_string(p));
       WorkerReport r = ctx[p].report;
       r.out_frontier = hc.out_cnt;
-      r.next_frontier = hc.next_cnt;
+      r.next_frontier = n == 1 ? hc.out_cnt : hc.next_cnt;
       r.edges_delta = hc.edges;
       r.combine_delta = hc.combine;
       for (int k = 0; k < 4; ++k) {
@@ -447,8 +502,8 @@ void run_primitive(Plan& P, Prim& prim, const mg_config& cfg) {
         if (r.u[k] == 0) r.u[k] = hc.u[k];
       }
       view.reports[p] = r;
-      rs.next_count[p] = hc.next_cnt;
-      rs.next_deg[p] = hc.next_deg;
+      rs.next_count[p] = (uint32_t)r.next_frontier;
+      rs.next_deg[p] = want_deg ? hc.next_deg : kUnknownDeg;
       if (n > 1) {
         for (uint32_t q = 0; q < n; ++q) {
           if (q == p) continue;
@@ -524,6 +579,9 @@ void run_primitive(Plan& P, Prim& prim, const mg_config& cfg) {
   st.device_ms = dev_ms;
   st.gpu_launches = g_launches.load() - launches0;
   st.exchange_bytes = xbytes;
+  st.kernel_ms = P.prof_ms;
+  st.kernel_launches = P.prof_launches;
+  st.kernel_bytes = P.prof_bytes;
   collect_buffer_stats(P);
 }
 

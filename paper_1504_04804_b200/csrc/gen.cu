@@ -290,21 +290,7 @@ Plan* plan_from_device_csr(uint32_t nv, uint64_t ne, DevArray<uint32_t>& goff,
       }
       {
         DeviceGuard dgw(w.dev);
-        MGB_CUDA(cudaStreamCreateWithFlags(&w.stream, cudaStreamNonBlocking));
-        MGB_CUDA(cudaEventCreate(&w.ev_start));
-        MGB_CUDA(cudaEventCreate(&w.ev_end));
-        MGB_CUDA(cudaEventCreate(&w.ev_x0));
-        MGB_CUDA(cudaEventCreate(&w.ev_x1));
-        w.ctr.alloc(1);
-        MGB_CUDA(cudaMallocHost(&w.host_ctr, sizeof(Counters)));
-        std::memset(w.host_ctr, 0, sizeof(Counters));
-        w.inbox_cnt.alloc(2 * kMaxWorkers);
-        MGB_CUDA(cudaMemset(w.inbox_cnt.ptr, 0, sizeof(uint32_t) * 2 * kMaxWorkers));
-        w.merge_stamp.alloc(nv ? nv : 1);
-        uint64_t nbig = w.ne / kBigDegree + 2;
-        if (nbig > (uint64_t)nv + 1) nbig = (uint64_t)nv + 1;
-        w.big.alloc(nbig);
-        w.big_prefix.alloc(nbig + 1);
+        init_worker_runtime(w);
         w.owner.upload(own8.data(), nv, w.stream);
         w.border.upload(border.data(), border.size(), w.stream);
         w.border_dst.upload(border.data(), border.size(), w.stream);

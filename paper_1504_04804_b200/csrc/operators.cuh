@@ -2,15 +2,19 @@
 // primitive's device functors (the reference's advance/filter/fused operators,
 // engine.hpp:54-99, and the functor hooks of PrimitiveSpec, engine.hpp:587-626).
 //
-// advance (load balanced):  each CTA takes a chunk of 256 frontier vertices,
-//   block-scans their degrees in shared memory and expands the chunk's arcs
-//   edge-parallel (merge-path style: thread i of the expansion finds its source
-//   vertex by binary search over the 256-entry prefix), so consecutive lanes
-//   read consecutive col_indices (coalesced).  Vertices with degree above
-//   kBigDegree are deferred to a grid-wide pass over a global degree prefix, so
-//   one hub (RMAT source: ~1e6 arcs) is spread over every SM.
-// filter:  order-free compaction by keep(v) with warp-aggregated appends.
-// Both count W (edges examined) exactly as the reference (= sum of degrees).
+// advance = edge-balanced ("merge-path") expansion in three kernels:
+//   lb_degree_kernel   one pass over the frontier: row start + out-degree per
+//                      vertex, CTA-local exclusive scan of the degrees, CTA sums
+//   lb_scan_kernel     one CTA scans the CTA sums (global offsets + total W)
+//   lb_expand_kernel   persistent CTAs walk fixed tiles of kTile arcs of the
+//                      concatenated adjacency: one binary search per tile over
+//                      the global degree prefix, the tile's vertex range staged
+//                      in shared memory, then every thread expands kItems
+//                      consecutive arcs (one smem search + a linear walk), so
+//                      a 1e6-arc hub is spread over every SM and consecutive
+//                      threads read consecutive col_indices.
+// The edge count W (reference E:66) is the scan total.
+// filter = order-free compaction by keep(v) with warp-aggregated appends.
 #pragma once
 
 #include <cub/block/block_scan.cuh>
@@ -19,124 +23,176 @@
 
 namespace mgb {
 
-constexpr int kAdvBlock = 256;
-constexpr uint32_t kBigDegree = 2048;
+constexpr int kLbBlock = 256;     // degree pass: one vertex per thread
+constexpr int kExpBlock = 256;    // expansion CTA
+constexpr int kItems = 8;         // arcs per thread per tile (lane-strided)
+constexpr uint32_t kTile = kExpBlock * kItems;  // 4096 arcs per tile
+constexpr int kStage = 1536;      // max tile vertices staged in shared memory
 
-// stage 1: chunked expansion of small/medium-degree vertices; big ones deferred
-template <class F, bool kFused>
-__global__ void __launch_bounds__(kAdvBlock)
-    advance_chunk_kernel(F f, GraphView g, const uint32_t* __restrict__ in, uint32_t n_in,
-                         uint32_t* __restrict__ out, uint32_t* out_cnt, uint32_t* big,
-                         uint32_t* big_cnt, unsigned long long* edges) {
-  using Scan = cub::BlockScan<uint32_t, kAdvBlock>;
-  __shared__ typename Scan::TempStorage scan_tmp;
-  __shared__ uint32_t s_pref[kAdvBlock + 1];
-  __shared__ uint32_t s_row[kAdvBlock];
-  __shared__ uint32_t s_src[kAdvBlock];
-  unsigned long long my_edges = 0;
-  for (uint64_t base = (uint64_t)blockIdx.x * kAdvBlock; base < n_in;
-       base += (uint64_t)gridDim.x * kAdvBlock) {
-    uint64_t i = base + threadIdx.x;
-    uint32_t u = 0, deg = 0, row = 0;
-    if (i < n_in) {
-      u = in[i];
-      row = g.off[u];
-      deg = g.off[u + 1] - row;
-      my_edges += deg;
-      if (deg > kBigDegree) {
-        uint32_t slot = atomicAdd(big_cnt, 1u);
-        big[slot] = (uint32_t)i;
-        deg = 0;
-      }
-    }
-    uint32_t excl, total;
-    Scan(scan_tmp).ExclusiveSum(deg, excl, total);
-    s_pref[threadIdx.x] = excl;
-    s_row[threadIdx.x] = row;
-    s_src[threadIdx.x] = u;
-    if (threadIdx.x == 0) s_pref[kAdvBlock] = total;
-    __syncthreads();
-    for (uint32_t k = threadIdx.x; k < ((total + 31u) & ~31u); k += kAdvBlock) {
-      bool acc = false;
-      uint32_t v = 0;
-      if (k < total) {
-        // largest j with s_pref[j] <= k (degree-0 entries share prefixes)
-        int lo = 0, hi = kAdvBlock - 1;
-        while (lo < hi) {
-          int mid = (lo + hi + 1) >> 1;
-          if (s_pref[mid] <= k) lo = mid;
-          else hi = mid - 1;
-        }
-        uint32_t e = s_row[lo] + (k - s_pref[lo]);
-        v = g.col[e];
-        acc = f.visit(s_src[lo], v, e);
-        if (kFused && acc) acc = f.keep(v);
-      }
-      uint32_t slot = warp_append(out_cnt, acc);
-      if (acc) out[slot] = v;
-    }
-    __syncthreads();
+// lb 1: row starts + CTA-local exclusive prefix of degrees
+static __global__ void __launch_bounds__(kLbBlock)
+    lb_degree_kernel(const uint32_t* __restrict__ off, const uint32_t* __restrict__ in,
+                     uint32_t n_in, uint32_t* __restrict__ rowstart,
+                     unsigned long long* __restrict__ prefix, unsigned long long* block_sum) {
+  using Scan = cub::BlockScan<unsigned long long, kLbBlock>;
+  __shared__ typename Scan::TempStorage tmp;
+  uint32_t i = blockIdx.x * kLbBlock + threadIdx.x;
+  unsigned long long d = 0;
+  if (i < n_in) {
+    uint32_t u = in[i];
+    uint32_t rs = off[u];
+    d = off[u + 1] - rs;
+    rowstart[i] = rs;
   }
-  warp_add_u64(edges, my_edges);
+  unsigned long long excl, total;
+  Scan(tmp).ExclusiveSum(d, excl, total);
+  if (i < n_in) prefix[i] = excl;
+  if (threadIdx.x == 0) block_sum[blockIdx.x] = total;
 }
 
-// stage 2a: exclusive prefix of the deferred big vertices' degrees (one CTA)
+// lb 2: scan the CTA sums in one CTA; block_sum becomes exclusive offsets,
+// block_sum[nb] the total (= edges examined)
 static __global__ void __launch_bounds__(1024)
-    big_prefix_kernel(GraphView g, const uint32_t* __restrict__ in, const uint32_t* big,
-                      const uint32_t* big_cnt, unsigned long long* prefix) {
+    lb_scan_kernel(unsigned long long* block_sum, uint32_t nb, unsigned long long* total_out,
+                   unsigned long long* edges) {
   using Scan = cub::BlockScan<unsigned long long, 1024>;
   __shared__ typename Scan::TempStorage tmp;
   __shared__ unsigned long long carry;
   if (threadIdx.x == 0) carry = 0;
   __syncthreads();
-  uint32_t nb = *big_cnt;
   for (uint32_t base = 0; base < nb; base += 1024) {
     uint32_t i = base + threadIdx.x;
-    unsigned long long d = 0;
-    if (i < nb) {
-      uint32_t u = in[big[i]];
-      d = g.off[u + 1] - g.off[u];
-    }
+    unsigned long long d = i < nb ? block_sum[i] : 0ull;
     unsigned long long excl, total;
     Scan(tmp).ExclusiveSum(d, excl, total);
-    if (i < nb) prefix[i] = carry + excl;
+    if (i < nb) block_sum[i] = carry + excl;
     __syncthreads();
     if (threadIdx.x == 0) carry += total;
     __syncthreads();
   }
-  if (threadIdx.x == 0) prefix[nb] = carry;
+  if (threadIdx.x == 0) {
+    block_sum[nb] = carry;
+    *total_out = carry;
+    atomicAdd(edges, carry);
+  }
 }
 
-// stage 2b: edge-parallel expansion of the big vertices over the whole grid
+// global prefix of frontier entry i
+__device__ __forceinline__ unsigned long long lb_pref(const unsigned long long* prefix,
+                                                      const unsigned long long* block_off,
+                                                      uint32_t i) {
+  return block_off[i / kLbBlock] + prefix[i];
+}
+
+// last frontier index j in [0,n) with pref(j) <= k
+__device__ __forceinline__ uint32_t lb_search(const unsigned long long* prefix,
+                                              const unsigned long long* block_off, uint32_t n,
+                                              unsigned long long k) {
+  uint32_t lo = 0, hi = n - 1;
+  while (lo < hi) {
+    uint32_t mid = (lo + hi + 1) >> 1;
+    if (lb_pref(prefix, block_off, mid) <= k) lo = mid;
+    else hi = mid - 1;
+  }
+  return lo;
+}
+
+// lb 3a: first frontier entry of every tile (one binary search per tile, all
+// tiles in parallel) so the expansion never waits on a serial search
+static __global__ void lb_tiles_kernel(const unsigned long long* __restrict__ prefix,
+                                       const unsigned long long* __restrict__ block_off,
+                                       uint32_t n_in, const unsigned long long* total_ptr,
+                                       uint32_t* tile_lo, uint32_t max_tiles) {
+  const unsigned long long total = *total_ptr;
+  const unsigned long long ntiles = (total + kTile - 1) / kTile;
+  for (unsigned long long t = blockIdx.x * (unsigned long long)blockDim.x + threadIdx.x;
+       t <= ntiles && t <= max_tiles; t += (unsigned long long)gridDim.x * blockDim.x)
+    tile_lo[t] = t == ntiles ? n_in - 1 : lb_search(prefix, block_off, n_in, t * kTile);
+}
+
+// lb 3b: edge-balanced expansion (visit [+ keep when fused]).  Per tile the
+// vertex range is staged in shared memory; warp w owns arcs [t0+w*32*kItems,
+// +32*kItems) with lane l taking arcs l, l+32, ... (coalesced col_indices).
+// The kItems arcs of a lane go through four batched phases — locate, load the
+// neighbour IDs, pre-test them (prefilter, e.g. the visited bitmap in L2),
+// then visit the survivors — so each thread keeps kItems independent loads in
+// flight instead of one dependent chain per arc.
 template <class F, bool kFused>
-__global__ void __launch_bounds__(kAdvBlock)
-    advance_big_kernel(F f, GraphView g, const uint32_t* __restrict__ in, const uint32_t* big,
-                       const uint32_t* big_cnt, const unsigned long long* __restrict__ prefix,
-                       uint32_t* __restrict__ out, uint32_t* out_cnt) {
-  uint32_t nb = *big_cnt;
-  if (nb == 0) return;
-  unsigned long long total = prefix[nb];
-  const unsigned long long stride = (unsigned long long)gridDim.x * kAdvBlock;
-  for (unsigned long long base = (unsigned long long)blockIdx.x * kAdvBlock; base < total;
-       base += stride) {
-    unsigned long long k = base + threadIdx.x;
-    bool acc = false;
-    uint32_t v = 0;
-    if (k < total) {
-      uint32_t lo = 0, hi = nb - 1;
-      while (lo < hi) {
-        uint32_t mid = (lo + hi + 1) >> 1;
-        if (prefix[mid] <= k) lo = mid;
-        else hi = mid - 1;
+__global__ void __launch_bounds__(kExpBlock)
+    lb_expand_kernel(F f, GraphView g, const uint32_t* __restrict__ in, uint32_t n_in,
+                     const uint32_t* __restrict__ rowstart,
+                     const unsigned long long* __restrict__ prefix,
+                     const unsigned long long* __restrict__ block_off,
+                     const unsigned long long* total_ptr, const uint32_t* __restrict__ tile_lo,
+                     uint32_t* __restrict__ out, uint32_t* out_cnt) {
+  __shared__ unsigned long long s_pref[kStage + 1];
+  __shared__ uint32_t s_row[kStage];
+  __shared__ uint32_t s_src[kStage];
+  __shared__ BlockQueue<kTile> q;  // one global reservation per tile
+  q.reset();
+  const unsigned long long total = *total_ptr;
+  const unsigned long long ntiles = (total + kTile - 1) / kTile;
+  const unsigned warp = threadIdx.x >> 5, lane = lane_id();
+  for (unsigned long long tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    const unsigned long long t0 = tile * kTile;
+    const unsigned long long t1 = t0 + kTile < total ? t0 + kTile : total;
+    const uint32_t lo = tile_lo[tile];
+    const uint32_t hi = tile + 1 < ntiles ? tile_lo[tile + 1] : n_in - 1;
+    const uint32_t R = hi - lo + 1;
+    const bool staged = R <= (uint32_t)kStage;
+    __syncthreads();  // previous tile done with the stage
+    if (staged) {
+      for (uint32_t j = threadIdx.x; j < R; j += kExpBlock) {
+        s_pref[j] = lb_pref(prefix, block_off, lo + j);
+        s_row[j] = rowstart[lo + j];
+        s_src[j] = in[lo + j];
       }
-      uint32_t u = in[big[lo]];
-      uint32_t e = g.off[u] + (uint32_t)(k - prefix[lo]);
-      v = g.col[e];
-      acc = f.visit(u, v, e);
-      if (kFused && acc) acc = f.keep(v);
+      if (threadIdx.x == 0)
+        s_pref[R] = (hi + 1 < n_in) ? lb_pref(prefix, block_off, hi + 1) : total;
     }
-    uint32_t slot = warp_append(out_cnt, acc);
-    if (acc) out[slot] = v;
+    __syncthreads();
+    auto pref = [&](uint32_t j) -> unsigned long long {  // j relative to lo
+      return staged ? s_pref[j]
+                    : ((lo + j < n_in) ? lb_pref(prefix, block_off, lo + j) : total);
+    };
+    const unsigned long long e0 = t0 + (unsigned long long)warp * 32 * kItems + lane;
+    uint32_t j = 0;
+    if (e0 < t1) {
+      uint32_t a = 0, b = R - 1;  // last j with pref(j) <= e0
+      while (a < b) {
+        uint32_t m = (a + b + 1) >> 1;
+        if (pref(m) <= e0) a = m;
+        else b = m - 1;
+      }
+      j = a;
+    }
+    uint32_t eid[kItems], src[kItems], nb[kItems];
+    unsigned long long jnext = e0 < t1 ? pref(j + 1) : 0;
+#pragma unroll
+    for (int k = 0; k < kItems; ++k) {  // locate
+      const unsigned long long e = e0 + 32ull * k;
+      eid[k] = 0xFFFFFFFFu;
+      if (e < t1) {
+        while (e >= jnext) jnext = pref(++j + 1);
+        const unsigned long long base = pref(j);
+        eid[k] = (staged ? s_row[j] : rowstart[lo + j]) + (uint32_t)(e - base);
+        src[k] = staged ? s_src[j] : in[lo + j];
+      }
+    }
+#pragma unroll
+    for (int k = 0; k < kItems; ++k)  // neighbour IDs: independent, coalesced loads
+      nb[k] = eid[k] != 0xFFFFFFFFu ? __ldg(&g.col[eid[k]]) : 0u;
+    bool pass[kItems];
+#pragma unroll
+    for (int k = 0; k < kItems; ++k)  // pre-tests: independent loads
+      pass[k] = eid[k] != 0xFFFFFFFFu && f.prefilter(nb[k]);
+#pragma unroll
+    for (int k = 0; k < kItems; ++k) {
+      bool acc = pass[k] && f.visit(src[k], nb[k], eid[k]);
+      if (kFused && acc) acc = f.keep(nb[k]);
+      q.push(acc, nb[k]);
+    }
+    q.flush(out_cnt, out);
   }
 }
 

@@ -17,14 +17,16 @@ static void free_worker(Worker& w) {
   w.off.free_(); w.col.free_(); w.w.free_(); w.hosted.free_(); w.owner.free_(); w.l2g.free_();
   w.border.free_(); w.border_dst.free_();
   w.input.release(); w.next_input.release(); w.advance_out.release(); w.output.release();
-  w.merge_stamp.free_(); w.big.free_(); w.big_prefix.free_(); w.arena.free_();
+  w.merge_stamp.free_(); w.lb_row.free_(); w.lb_pref.free_(); w.lb_bsum.free_(); w.lb_tile.free_(); w.arena.free_();
   w.inbox_cnt.free_(); w.send_table.free_(); w.send_cnt_ptr.free_(); w.recv_table.free_(); w.ctr.free_();
   for (auto& a : w.su32) a.free_();
   for (auto& a : w.sf64) a.free_();
   for (auto& a : w.su64) a.free_();
+  for (auto& a : w.aux) a.free_();
+  w.nonisolated.free_();
   if (w.host_ctr) cudaFreeHost(w.host_ctr);
   if (w.stream) cudaStreamDestroy(w.stream);
-  for (cudaEvent_t e : {w.ev_start, w.ev_end, w.ev_x0, w.ev_x1})
+  for (cudaEvent_t e : {w.ev_start, w.ev_end, w.ev_x0, w.ev_x1, w.ev_k0, w.ev_k1})
     if (e) cudaEventDestroy(e);
 }
 
@@ -38,23 +40,21 @@ void plan_free(Plan* P) {
   delete P;
 }
 
-static void init_worker_runtime(Worker& w) {
+void init_worker_runtime(Worker& w) {
   DeviceGuard dg(w.dev);
   MGB_CUDA(cudaStreamCreateWithFlags(&w.stream, cudaStreamNonBlocking));
   MGB_CUDA(cudaEventCreate(&w.ev_start));
   MGB_CUDA(cudaEventCreate(&w.ev_end));
   MGB_CUDA(cudaEventCreate(&w.ev_x0));
   MGB_CUDA(cudaEventCreate(&w.ev_x1));
+  MGB_CUDA(cudaEventCreate(&w.ev_k0));
+  MGB_CUDA(cudaEventCreate(&w.ev_k1));
   w.ctr.alloc(1);
   MGB_CUDA(cudaMallocHost(&w.host_ctr, sizeof(Counters)));
   std::memset(w.host_ctr, 0, sizeof(Counters));
   w.inbox_cnt.alloc(2 * kMaxWorkers);
   MGB_CUDA(cudaMemset(w.inbox_cnt.ptr, 0, sizeof(uint32_t) * 2 * kMaxWorkers));
   w.merge_stamp.alloc(w.nv ? w.nv : 1);
-  uint64_t nbig = w.ne / kBigDegree + 2;
-  if (nbig > (uint64_t)w.nv + 1) nbig = (uint64_t)w.nv + 1;
-  w.big.alloc(nbig);
-  w.big_prefix.alloc(nbig + 1);
 }
 
 // Upload one partition of a host plan (partition.cpp:157-207 layout)
@@ -251,7 +251,7 @@ void prepare_worker(Plan& P, Worker& w, const mg_config& cfg) {
   w.output.attach(&w.stats[MG_ROLE_FILTER_OUTPUT], &w.budget);
   // every run starts from empty frontier buffers so the policy's growth
   // behaviour (and its realloc counts) is observable per run
-  w.input.release(); w.next_input.release(); w.advance_out.release(); w.output.release();
+  w.input.reset(); w.next_input.reset(); w.advance_out.reset(); w.output.reset();
   w.budget.allocated = w.arena.n;
   w.budget.peak = w.budget.allocated;
   if (cfg.hard_cap_bytes && w.budget.allocated > cfg.hard_cap_bytes)

@@ -73,6 +73,7 @@ struct Worker {
   int dev = 0;
   cudaStream_t stream = nullptr;
   cudaEvent_t ev_start = nullptr, ev_end = nullptr, ev_x0 = nullptr, ev_x1 = nullptr;
+  cudaEvent_t ev_k0 = nullptr, ev_k1 = nullptr;  // dominant-kernel timing (profiling)
 
   // sub-graph
   uint32_t nv = 0;
@@ -91,8 +92,9 @@ struct Worker {
   BufferStats stats[MG_NUM_ROLES];
   DevBuf<uint32_t> input, next_input, advance_out, output;
   DevArray<uint32_t> merge_stamp;
-  DevArray<uint32_t> big;       // advance big-vertex scratch (index list)
-  DevArray<unsigned long long> big_prefix;
+  DevArray<uint32_t> lb_row;    // advance scratch: row start per frontier entry
+  DevArray<unsigned long long> lb_pref, lb_bsum;  // CTA-local degree prefix, CTA offsets
+  DevArray<uint32_t> lb_tile;   // first frontier entry of every expansion tile
 
   // inbox arena (receiver side): [parity][src] slots + counts
   int nva = 0, nvv = 0;
@@ -110,6 +112,10 @@ struct Worker {
   DevArray<uint32_t> su32[4];
   DevArray<double> sf64[4];
   DevArray<unsigned long long> su64[3];
+  DevArray<uint32_t> aux[4];          // primitive-private scratch (bitmaps, queues)
+  DevArray<uint32_t> nonisolated;     // hosted vertices with out-degree > 0 (ascending)
+  uint32_t n_nonisolated = 0;
+  bool nonisolated_ready = false;
   std::vector<uint32_t> hosted_host;  // hosted local IDs (host copy)
   DevArray<uint32_t> border_dst;      // PR: destination-local ID of every border entry
 
@@ -149,12 +155,18 @@ struct Plan {
   // device-resident results of the last run (global ID space, on workers[0].dev)
   int last_result_kind = -1;
 
+  // live timing of the primitive's dominant kernel (bench roofline)
+  bool profile = false;
+  double prof_ms = 0, prof_bytes = 0;
+  uint64_t prof_launches = 0;
+
   // multi-process bootstrap
   std::vector<void*> peer_arena;    // mapped inbox arenas of peers
   std::vector<uint64_t> peer_arena_bytes;
 };
 
 Worker& worker(Plan& P, uint32_t p);
+void init_worker_runtime(Worker& w);
 void plan_free(Plan* P);
 
 }  // namespace mgb

@@ -61,6 +61,8 @@ __global__ void fill_hosted_f64_kernel(double* a, const uint32_t* hosted, uint32
     a[hosted[i]] = v;
 }
 
+__global__ void or_word_kernel(uint32_t* w, uint32_t bit) { *w |= bit; }
+
 __global__ void iota_kernel(uint32_t* a, uint32_t n) {
   for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
     a[i] = i;
@@ -83,14 +85,15 @@ struct BfsDev {
   uint32_t iter;
   int mark_preds;
   // visit: unvisited -> label iter+1 (+pred); the CAS makes the discovery unique
+  // (called only for arcs whose prefilter() saw an unvisited label)
   __device__ bool visit(uint32_t u, uint32_t v, uint32_t) const {
-    if (labels[v] != kInfLabel) return false;
     if (atomicCAS(&labels[v], kInfLabel, iter + 1) != kInfLabel) return false;
     if (mark_preds) preds[v] = ow.to_global(u);
     return true;
   }
   // keep: per-superstep stamp dedup (primitives.cpp:89-94)
   __device__ bool keep(uint32_t v) const { return atomicExch(&seen[v], iter + 1) != iter + 1; }
+  __device__ bool prefilter(uint32_t v) const { return __ldcg(&labels[v]) == kInfLabel; }
   // combine (primitives.cpp:98-107): iter+1 < label -> set, enqueue iff hosted
   __device__ bool combine(uint32_t v, const uint32_t* va, const double*, uint32_t it) const {
     uint32_t cand = it + 1;
@@ -134,30 +137,47 @@ struct BfsPrim : PrimBase {
 
 // ===========================================================================
 // DOBFS (primitives.cpp:131-289)
+//
+// B200 layout: visited and frontier sets are BITMAPS (|V|/8 bytes each: 8 MiB
+// at scale 26, resident in the 126 MB L2), so the per-arc membership tests of
+// both directions hit L2 instead of HBM.  The pull step walks a compacted
+// unvisited list (the paper's split of the unvisited queue),
+// seeded from the plan's list of non-isolated hosted vertices so the ~half of
+// an RMAT graph that is isolated is never touched.  Results and the
+// examined-edge count W are those of the reference's scan (first hit in arc
+// order), so labels, direction log and W match it exactly.
 
 struct DobfsDev {
   uint32_t* labels;
   uint32_t* preds;
+  uint32_t* vis;  // visited bitmap
   OwnerView ow;
   uint32_t iter;
   int mark_preds;
+  // forward visit (primitives.cpp:216-222): test-and-set on the visited bitmap.
+  // The pre-test reads L2 (ld.cg): an L1 copy would keep showing bits other
+  // SMs have since set, turning every later test into an atomic.
+  // (called only for arcs whose prefilter() saw the bit clear)
   __device__ bool visit(uint32_t u, uint32_t v, uint32_t) const {
-    if (labels[v] != kInfLabel) return false;
-    if (atomicCAS(&labels[v], kInfLabel, iter + 1) != kInfLabel) return false;
+    const uint32_t bit = 1u << (v & 31);
+    if (atomicOr(&vis[v >> 5], bit) & bit) return false;
+    labels[v] = iter + 1;
     if (mark_preds) preds[v] = ow.to_global(u);
     return true;
   }
   __device__ bool keep(uint32_t) const { return true; }
-  // combine (primitives.cpp:255-265): accepted remote discoveries join the
-  // (global) next frontier on every worker
+  __device__ bool prefilter(uint32_t v) const {
+    return !(__ldcg(&vis[v >> 5]) & (1u << (v & 31)));
+  }
+  // combine (primitives.cpp:255-265): an unvisited vertex takes the remote
+  // label; accepted discoveries join the (global) next frontier everywhere
   __device__ bool combine(uint32_t v, const uint32_t* va, const double*, uint32_t it) const {
-    uint32_t cand = it + 1;
-    uint32_t old = atomicMin(&labels[v], cand);
-    if (cand < old) {
-      if (mark_preds) preds[v] = va[0];
-      return true;
-    }
-    return false;
+    const uint32_t bit = 1u << (v & 31);
+    if (vis[v >> 5] & bit) return false;
+    if (atomicOr(&vis[v >> 5], bit) & bit) return false;
+    labels[v] = it + 1;
+    if (mark_preds) preds[v] = va[0];
+    return true;
   }
   __device__ void gather(uint32_t v, uint32_t* va, double*) const {
     if (mark_preds) va[0] = preds[v];
@@ -166,23 +186,97 @@ struct DobfsDev {
   __device__ uint32_t peer_id(uint32_t v, uint32_t, uint32_t) const { return v; }
 };
 
-__global__ void stamp_frontier_kernel(const uint32_t* __restrict__ in, uint32_t n,
-                                      uint32_t* stamp, uint32_t value) {
-  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
-    stamp[in[i]] = value;
+__global__ void bitmap_set_kernel(const uint32_t* __restrict__ in, uint32_t n, uint32_t* bits) {
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    uint32_t v = in[i];
+    atomicOr(&bits[v >> 5], 1u << (v & 31));
+  }
 }
 
-// backward (pull) step (primitives.cpp:227-252): every hosted unvisited vertex
-// scans its arcs in order and stops at the first neighbour in the frontier.
-// One 8-lane group per vertex: each round the group tests 8 consecutive arcs
-// (one 32-byte sector of col_indices) and the first hit in arc order wins, so
-// the examined-edge count equals the reference's sequential count.
-constexpr int kPullGroup = 8;
+__global__ void select_nonisolated_kernel(const uint32_t* __restrict__ hosted, uint32_t nh,
+                                          const uint32_t* __restrict__ off, uint32_t* out,
+                                          uint32_t* cnt) {
+  for (uint32_t base = blockIdx.x * blockDim.x; base < nh; base += gridDim.x * blockDim.x) {
+    uint32_t i = base + threadIdx.x;
+    uint32_t v = i < nh ? hosted[i] : 0;
+    bool keep = i < nh && off[v + 1] > off[v];
+    uint32_t s = warp_append(cnt, keep);
+    if (keep) out[s] = v;
+  }
+}
+
+constexpr int kPullK = 4;      // arcs each thread tests before handing off
+constexpr int kPullGroup = 8;  // lanes per vertex in the long-row pass
+
+// pull step, stage 1 (primitives.cpp:230-251): one thread per unvisited vertex
+// tests its first kPullK arcs (independent loads in flight); a hit labels the
+// vertex, a short row without a hit keeps it unvisited, a long row goes to the
+// cooperative stage with its scan position.
 __global__ void __launch_bounds__(256)
-    dobfs_pull_kernel(GraphView g, const uint32_t* __restrict__ hosted, uint32_t nh,
-                      uint32_t* labels, uint32_t* preds, const uint32_t* __restrict__ in_frontier,
-                      uint32_t stamp, uint32_t next_label, int mark_preds, OwnerView ow,
-                      uint32_t* out, Counters* ctr) {
+    dobfs_pull_thread_kernel(GraphView g, const uint32_t* __restrict__ ul, uint32_t nul,
+                             uint32_t* labels, uint32_t* preds, uint32_t* vis,
+                             const uint32_t* __restrict__ fb, uint32_t next_label, int mark_preds,
+                             OwnerView ow, uint32_t* out, uint32_t* ul_out, uint32_t* ul_out_cnt,
+                             uint32_t* longq, uint32_t* long_cnt, Counters* ctr) {
+  unsigned long long scanned = 0, opened = 0;
+  __shared__ BlockQueue<256> q_found, q_keep, q_long;
+  q_found.reset();
+  q_keep.reset();
+  q_long.reset();
+  __syncthreads();
+  for (uint32_t base = blockIdx.x * blockDim.x; base < nul; base += gridDim.x * blockDim.x) {
+    uint32_t i = base + threadIdx.x;
+    bool found = false, keep = false, lng = false;
+    uint32_t v = 0;
+    if (i < nul) {
+      v = ul[i];
+      if (!(vis[v >> 5] & (1u << (v & 31)))) {
+        ++opened;
+        const uint32_t b = g.off[v], e = g.off[v + 1];
+        const uint32_t d = e - b;
+        uint32_t w[kPullK];
+#pragma unroll
+        for (int k = 0; k < kPullK; ++k) w[k] = (uint32_t)k < d ? __ldg(&g.col[b + k]) : 0u;
+        int hit = -1;
+#pragma unroll
+        for (int k = kPullK - 1; k >= 0; --k)
+          if ((uint32_t)k < d && (__ldg(&fb[w[k] >> 5]) & (1u << (w[k] & 31)))) hit = k;
+        if (hit >= 0) {
+          found = true;
+          scanned += hit + 1;
+          labels[v] = next_label;
+          atomicOr(&vis[v >> 5], 1u << (v & 31));
+          if (mark_preds) preds[v] = ow.to_global(w[hit]);
+        } else if (d <= (uint32_t)kPullK) {
+          scanned += d;
+          keep = true;
+        } else {
+          scanned += kPullK;
+          lng = true;
+        }
+      }
+    }
+    q_found.push(found, v);
+    q_keep.push(keep, v);
+    q_long.push(lng, v);
+    q_found.flush(&ctr->out_cnt, out);
+    q_keep.flush(ul_out_cnt, ul_out);
+    q_long.flush(long_cnt, longq);
+  }
+  warp_add_u64(&ctr->edges, scanned);
+  warp_add_u64(&ctr->u[2], opened);
+}
+
+// pull step, stage 2: long rows, 8 lanes per vertex from arc kPullK on; each
+// round tests one 32-byte sector of col_indices and the first hit in arc
+// order wins, so W equals the reference's sequential count
+__global__ void __launch_bounds__(256)
+    dobfs_pull_group_kernel(GraphView g, const uint32_t* __restrict__ longq,
+                            const uint32_t* long_cnt, uint32_t* labels, uint32_t* preds,
+                            uint32_t* vis, const uint32_t* __restrict__ fb, uint32_t next_label,
+                            int mark_preds, OwnerView ow, uint32_t* out, uint32_t* ul_out,
+                            uint32_t* ul_out_cnt, Counters* ctr) {
+  const uint32_t nl = *long_cnt;
   const unsigned lane = threadIdx.x & 31u;
   const unsigned sub = lane & (kPullGroup - 1);
   const unsigned gbase = lane & ~(kPullGroup - 1);
@@ -190,36 +284,43 @@ __global__ void __launch_bounds__(256)
   unsigned long long scanned = 0;
   const uint32_t groups = (gridDim.x * blockDim.x) / kPullGroup;
   const uint32_t gid = (blockIdx.x * blockDim.x + threadIdx.x) / kPullGroup;
-  const uint32_t rounds = (nh + groups - 1) / groups;
+  const uint32_t rounds = (nl + groups - 1) / groups;
   for (uint32_t r = 0; r < rounds; ++r) {
     uint32_t i = r * groups + gid;
-    bool found = false;
+    bool found = false, keep = false;
     uint32_t v = 0;
-    if (i < nh) {
-      v = hosted[i];
-      if (labels[v] == kInfLabel) {
-        uint32_t b = g.off[v], e = g.off[v + 1];
-        for (uint32_t k = b; k < e; k += kPullGroup) {
-          uint32_t idx = k + sub;
-          bool hit = idx < e && in_frontier[g.col[idx]] == stamp;
-          unsigned m = __ballot_sync(gmask, hit) & gmask;
-          if (m) {
-            unsigned first = __ffs(m) - 1 - gbase;
-            scanned += (sub == 0) ? (k - b + first + 1) : 0;
-            if (sub == 0) {
-              found = true;
-              uint32_t w = g.col[k + first];
-              labels[v] = next_label;
-              if (mark_preds) preds[v] = ow.to_global(w);
-            }
-            break;
+    if (i < nl) {
+      v = longq[i];
+      const uint32_t b = g.off[v] + kPullK, e = g.off[v + 1];
+      keep = true;
+      for (uint32_t k = b; k < e; k += kPullGroup) {
+        uint32_t idx = k + sub;
+        uint32_t w = idx < e ? __ldg(&g.col[idx]) : 0u;
+        bool hit = idx < e && (__ldg(&fb[w >> 5]) & (1u << (w & 31)));
+        unsigned m = __ballot_sync(gmask, hit) & gmask;
+        if (m) {
+          unsigned first = __ffs(m) - 1 - gbase;
+          if (sub == 0) {
+            scanned += k - b + first + 1;
+            found = true;
+            keep = false;
+            uint32_t pw = __shfl_sync(gmask, w, gbase + first);
+            labels[v] = next_label;
+            atomicOr(&vis[v >> 5], 1u << (v & 31));
+            if (mark_preds) preds[v] = ow.to_global(pw);
+          } else {
+            __shfl_sync(gmask, w, gbase + first);
           }
-          if (sub == 0) scanned += (e - k < (uint32_t)kPullGroup) ? (e - k) : kPullGroup;
+          break;
         }
+        if (sub == 0) scanned += (e - k < (uint32_t)kPullGroup) ? (e - k) : kPullGroup;
       }
+      if (sub != 0) keep = false;
     }
-    uint32_t slot = warp_append(&ctr->out_cnt, found);
-    if (found) out[slot] = v;
+    uint32_t s = warp_append(&ctr->out_cnt, found);
+    if (found) out[s] = v;
+    s = warp_append(ul_out_cnt, keep);
+    if (keep) ul_out[s] = v;
   }
   warp_add_u64(&ctr->edges, scanned);
 }
@@ -233,34 +334,72 @@ struct DobfsPrim : PrimBase {
   int dir = 0;
   bool switched_once = false;
   std::vector<int> dir_log;
-  std::vector<uint64_t> fwd, bwd;
+  // unvisited-list bookkeeping per worker: which aux buffer holds it, length
+  std::vector<int> ul_src;  // -1: the plan's non-isolated list
+  std::vector<uint32_t> ul_len;
   DobfsPrim(uint32_t s, double a, double b, bool m) : source(s), do_a(a), do_b(b), mark_preds(m) {
     name = "dobfs";
     nva = m ? 1 : 0;
     communication = MG_COMM_BROADCAST;
   }
+  static uint64_t words(uint32_t nv) { return (nv + 31) / 32 + 1; }
+  void ensure_nonisolated(Worker& w) {
+    if (w.nonisolated_ready) return;
+    uint32_t nh = (uint32_t)w.hosted_host.size();
+    w.nonisolated.alloc(nh ? nh : 1);
+    DevArray<uint32_t> cnt;
+    cnt.alloc(1);
+    MGB_CUDA(cudaMemsetAsync(cnt.ptr, 0, 4, w.stream));
+    if (nh)
+      MGB_LAUNCH(select_nonisolated_kernel, grid_for(nh, 256, 4096), 256, 0, w.stream,
+                 w.hosted.ptr, nh, w.off.ptr, w.nonisolated.ptr, cnt.ptr);
+    uint32_t k = 0;
+    MGB_CUDA(cudaMemcpyAsync(&k, cnt.ptr, 4, cudaMemcpyDeviceToHost, w.stream));
+    MGB_CUDA(cudaStreamSynchronize(w.stream));
+    cnt.free_();
+    // ascending order keeps the pull step's offset loads coalesced
+    std::vector<uint32_t> h(k);
+    MGB_CUDA(cudaMemcpy(h.data(), w.nonisolated.ptr, 4ull * k, cudaMemcpyDeviceToHost));
+    std::sort(h.begin(), h.end());
+    MGB_CUDA(cudaMemcpy(w.nonisolated.ptr, h.data(), 4ull * k, cudaMemcpyHostToDevice));
+    w.n_nonisolated = k;
+    w.nonisolated_ready = true;
+    for (int i = 0; i < 3; ++i) w.aux[i].alloc(i < 2 ? (k ? k : 1) : 4);  // UL ping-pong, counters
+  }
   void init(Ctx& c) {  // primitives.cpp:185-195
     Worker& w = *c.w;
-    fill(w.su32[0], w.nv, 0xFF, w.stream);  // labels
-    fill(w.su32[3], w.nv, 0, w.stream);     // in_frontier stamps
+    ensure_nonisolated(w);  // plan-lifetime precomputation, outside the timed region on reuse
+    fill(w.su32[0], w.nv, 0xFF, w.stream);        // labels
+    fill(w.su32[2], words(w.nv), 0, w.stream);    // visited bitmap
+    if (w.su32[3].n < words(w.nv) || !w.su32[3].ptr) w.su32[3].alloc(words(w.nv));  // frontier
+    if (w.aux[3].n < w.n_nonisolated + 1 || !w.aux[3].ptr) w.aux[3].alloc(w.n_nonisolated + 1);
     if (mark_preds) fill(w.su32[1], w.nv, 0xFF, w.stream);
     MGB_LAUNCH(set_one_kernel<uint32_t>, 1, 1, 0, w.stream, w.su32[0].ptr, source, 0u);
+    uint32_t sw = 1u << (source & 31);
+    set_bit_host(w, source, sw);
     if (c.P->owner_host[source] == w.p) c.push_initial({source});
-    if (fwd.empty()) {
-      fwd.assign(c.P->n, 0);
-      bwd.assign(c.P->n, 0);
+    if (ul_src.empty()) {
+      ul_src.assign(c.P->n, -1);
+      ul_len.assign(c.P->n, 0);
     }
+    ul_src[w.p] = -1;
+    ul_len[w.p] = w.n_nonisolated;
+  }
+  static void set_bit_host(Worker& w, uint32_t v, uint32_t bit) {
+    MGB_LAUNCH(or_word_kernel, 1, 1, 0, w.stream, w.su32[2].ptr + (v >> 5), bit);
   }
   DobfsDev dev(Ctx& c) {
     Worker& w = *c.w;
-    return {w.su32[0].ptr, w.su32[1].ptr, c.owner_view(), (uint32_t)c.iter, mark_preds ? 1 : 0};
+    return {w.su32[0].ptr, w.su32[1].ptr, w.su32[2].ptr, c.owner_view(), (uint32_t)c.iter,
+            mark_preds ? 1 : 0};
   }
   void body(Ctx& c) {  // primitives.cpp:197-253
     Worker& w = *c.w;
-    const uint32_t stamp = (uint32_t)c.iter + 1;
-    if (c.in_count)
-      MGB_LAUNCH(stamp_frontier_kernel, grid_for(c.in_count, 256), 256, 0, w.stream,
-                 w.input.ptr, c.in_count, w.su32[3].ptr, stamp);
+    collect_profile(c);
+    if (pending_ul_[w.p]) {  // length of the list compacted by the last pull step
+      ul_len[w.p] = w.host_ctr->misc;
+      pending_ul_[w.p] = false;
+    }
     if (c.worker() == c.P->local_workers.front()) {
       // decision on global quantities; identical on every worker
       if (c.iter >= 1) {
@@ -278,17 +417,65 @@ struct DobfsPrim : PrimBase {
     }
     if (dir == 0) {
       c.pipeline(dev(c), w.nv);
-    } else {
-      uint32_t nh = (uint32_t)w.hosted_host.size();
-      c.ensure_output(nh);
-      if (nh)
-        MGB_LAUNCH(dobfs_pull_kernel, grid_for((uint64_t)nh * kPullGroup, 256, kNumSMs * 16), 256,
-                   0, w.stream, w.graph(), w.hosted.ptr, nh, w.su32[0].ptr, w.su32[1].ptr,
-                   w.su32[3].ptr, stamp, stamp, mark_preds ? 1 : 0, c.owner_view(), w.output.ptr,
-                   c.ctr());
+      return;
     }
+    // backward: frontier bitmap of the (global) input frontier
+    const uint64_t nw = words(w.nv);
+    MGB_CUDA(cudaMemsetAsync(w.su32[3].ptr, 0, 4 * nw, w.stream));
+    if (c.in_count)
+      MGB_LAUNCH(bitmap_set_kernel, grid_for(c.in_count, 256, kNumSMs * 8), 256, 0, w.stream,
+                 w.input.ptr, c.in_count, w.su32[3].ptr);
+    const int src = ul_src[w.p];
+    const uint32_t* ul = src < 0 ? w.nonisolated.ptr : w.aux[src].ptr;
+    const int dst = src == 0 ? 1 : 0;
+    const uint32_t nul = ul_len[w.p];
+    uint32_t* ulcnt = &c.ctr()->misc;  // reported with the superstep's counters
+    uint32_t* cnts = w.aux[2].ptr;     // [1] long-row queue length
+    MGB_CUDA(cudaMemsetAsync(cnts, 0, 8, w.stream));
+    c.ensure_output(nul);
+    const uint32_t next_label = (uint32_t)c.iter + 1;
+    if (c.P->profile) {
+      MGB_CUDA(cudaEventRecord(w.ev_k0, w.stream));
+      prof_nul_[w.p] = nul;
+    }
+    if (nul) {
+      MGB_LAUNCH(dobfs_pull_thread_kernel, grid_for(nul, 256, kNumSMs * 16), 256, 0, w.stream,
+                 w.graph(), ul, nul, w.su32[0].ptr, w.su32[1].ptr, w.su32[2].ptr, w.su32[3].ptr,
+                 next_label, mark_preds ? 1 : 0, c.owner_view(), w.output.ptr, w.aux[dst].ptr,
+                 ulcnt, w.aux[3].ptr, cnts + 1, c.ctr());
+      MGB_LAUNCH(dobfs_pull_group_kernel, kNumSMs * 16, 256, 0, w.stream, w.graph(), w.aux[3].ptr,
+                 cnts + 1, w.su32[0].ptr, w.su32[1].ptr, w.su32[2].ptr, w.su32[3].ptr, next_label,
+                 mark_preds ? 1 : 0, c.owner_view(), w.output.ptr, w.aux[dst].ptr, ulcnt, c.ctr());
+    }
+    if (c.P->profile) {
+      MGB_CUDA(cudaEventRecord(w.ev_k1, w.stream));
+      prof_pending_[w.p] = true;
+    }
+    pending_ul_[w.p] = true;  // new length arrives with this superstep's report
+    ul_src[w.p] = dst;
   }
-  void after_merge(Ctx&) {}
+  // Pull-step timing + algorithmic bytes (SURVEY §8(d) DOBFS term, per launch
+  // pair): unvisited list 4 B/entry, row offsets 8 B per opened vertex, 4 B per
+  // examined arc, label + output 8 B per discovery, 4 B per kept entry.  The
+  // visited / frontier bitmaps are L2-resident and not counted.  Read after the
+  // superstep's report synchronised the stream.
+  void collect_profile(Ctx& c) {
+    Worker& w = *c.w;
+    if (!prof_pending_[w.p]) return;
+    prof_pending_[w.p] = false;
+    float ms = 0;
+    MGB_CUDA(cudaEventElapsedTime(&ms, w.ev_k0, w.ev_k1));
+    const Counters& h = *w.host_ctr;
+    double bytes = 4.0 * prof_nul_[w.p] + 8.0 * (double)h.u[2] + 4.0 * (double)h.edges +
+                   8.0 * (double)h.out_cnt + 4.0 * (double)h.misc;
+    c.P->prof_ms += ms;
+    c.P->prof_bytes += bytes;
+    c.P->prof_launches += 1;
+  }
+  void finalize(Ctx& c, const GlobalView&) { collect_profile(c); }
+  std::vector<bool> pending_ul_ = std::vector<bool>(kMaxWorkers, false);
+  std::vector<bool> prof_pending_ = std::vector<bool>(kMaxWorkers, false);
+  std::vector<uint32_t> prof_nul_ = std::vector<uint32_t>(kMaxWorkers, 0);
 };
 
 // ===========================================================================
@@ -316,6 +503,7 @@ struct SsspDev {
     return false;
   }
   __device__ bool keep(uint32_t v) const { return atomicExch(&seen[v], iter + 1) != iter + 1; }
+  __device__ bool prefilter(uint32_t v) const { return true; }
   __device__ bool combine(uint32_t v, const uint32_t* va, const double* vv, uint32_t) const {
     unsigned long long nd = (unsigned long long)vv[0];
     unsigned long long old = atomicMin(&dists[v], nd);
@@ -390,6 +578,7 @@ struct CcDev {
   uint32_t* snapshot;
   __device__ bool visit(uint32_t, uint32_t, uint32_t) const { return false; }
   __device__ bool keep(uint32_t) const { return true; }
+  __device__ bool prefilter(uint32_t) const { return true; }
   __device__ bool combine(uint32_t v, const uint32_t* va, const double*, uint32_t) const {
     uint32_t c = va[0];
     uint32_t old = atomicMin(&comp[v], c);
@@ -543,6 +732,7 @@ struct BcDev {
     return old == kInfLabel;
   }
   __device__ bool keep(uint32_t v) const { return atomicExch(&seen[v], iter + 1) != iter + 1; }
+  __device__ bool prefilter(uint32_t) const { return true; }
   __device__ bool combine(uint32_t v, const uint32_t*, const double* vv, uint32_t it) const {
     if (phase == kFwd) {  // primitives.cpp:639-648
       uint32_t cand = it + 1;
@@ -704,6 +894,7 @@ struct PrDev {
   const uint32_t* border_dst;
   __device__ bool visit(uint32_t, uint32_t, uint32_t) const { return false; }
   __device__ bool keep(uint32_t) const { return true; }
+  __device__ bool prefilter(uint32_t) const { return true; }
   __device__ bool combine(uint32_t v, const uint32_t*, const double* vv, uint32_t) const {
     atomicAdd(&accum[v], vv[0]);
     return false;  // ranks are combined, never enqueued
