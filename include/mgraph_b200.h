@@ -179,6 +179,11 @@ typedef struct mg_stats {
   double kernel_ms;
   uint64_t kernel_launches;
   double kernel_bytes;
+  /* second timed kernel class (DOBFS: kernel_* = pull step, kernel2_* = the
+   * load-balanced push advance) */
+  double kernel2_ms;
+  uint64_t kernel2_launches;
+  double kernel2_bytes;
 } mg_stats;
 
 /* per-run arrays of the last run on this plan:

@@ -70,6 +70,9 @@ class mg_stats(C.Structure):
         ("kernel_ms", C.c_double),
         ("kernel_launches", C.c_uint64),
         ("kernel_bytes", C.c_double),
+        ("kernel2_ms", C.c_double),
+        ("kernel2_launches", C.c_uint64),
+        ("kernel2_bytes", C.c_double),
     ]
 
 

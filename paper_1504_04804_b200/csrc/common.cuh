@@ -98,6 +98,35 @@ struct BlockQueue {
   }
 };
 
+// Warp-private staging queue in shared memory: no CTA barrier is involved;
+// the warp reserves global space with one atomic per >= kFlush items, so the
+// shared output counter sees ~items/kFlush atomics in total.
+template <int kCap, int kFlush>
+struct WarpQueue {
+  uint32_t* buf;  // this warp's kCap-entry region of shared memory
+  uint32_t n;     // warp-uniform fill level
+  __device__ __forceinline__ void init(uint32_t* region) {
+    buf = region;
+    n = 0;
+  }
+  // every lane of the (full) warp must call push
+  __device__ __forceinline__ void push(bool pred, uint32_t v) {
+    unsigned mask = __ballot_sync(0xffffffffu, pred);
+    if (pred) buf[n + __popc(mask & ((1u << lane_id()) - 1u))] = v;
+    n += __popc(mask);
+  }
+  __device__ __forceinline__ void flush(uint32_t* counter, uint32_t* out, bool force) {
+    if (n == 0 || (!force && n < (uint32_t)kFlush)) return;
+    __syncwarp();
+    uint32_t base = 0;
+    if (lane_id() == 0) base = atomicAdd(counter, n);
+    base = __shfl_sync(0xffffffffu, base, 0);
+    for (uint32_t i = lane_id(); i < n; i += 32) out[base + i] = buf[i];
+    __syncwarp();
+    n = 0;
+  }
+};
+
 __device__ __forceinline__ void warp_add_u64(unsigned long long* counter, uint64_t v) {
   unsigned active = __activemask();
 #pragma unroll

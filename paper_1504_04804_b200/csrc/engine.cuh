@@ -374,6 +374,9 @@ void run_primitive(Plan& P, Prim& prim, const mg_config& cfg) {
   P.prof_ms = 0;
   P.prof_bytes = 0;
   P.prof_launches = 0;
+  P.prof2_ms = 0;
+  P.prof2_bytes = 0;
+  P.prof2_launches = 0;
   P.h_per_iter.clear();
   P.out_per_iter.clear();
   P.edges_per_iter.clear();
@@ -582,6 +585,9 @@ void run_primitive(Plan& P, Prim& prim, const mg_config& cfg) {
   st.kernel_ms = P.prof_ms;
   st.kernel_launches = P.prof_launches;
   st.kernel_bytes = P.prof_bytes;
+  st.kernel2_ms = P.prof2_ms;
+  st.kernel2_launches = P.prof2_launches;
+  st.kernel2_bytes = P.prof2_bytes;
   collect_buffer_stats(P);
 }
 

@@ -25,8 +25,11 @@ namespace mgb {
 
 constexpr int kLbBlock = 256;     // degree pass: one vertex per thread
 constexpr int kExpBlock = 256;    // expansion CTA
-constexpr int kItems = 8;         // arcs per thread per tile (lane-strided)
-constexpr uint32_t kTile = kExpBlock * kItems;  // 4096 arcs per tile
+constexpr int kItems = 8;         // arcs per thread per batch (lane-strided)
+constexpr int kBatches = 4;       // batches per warp per tile
+constexpr uint32_t kWarpArcs = 32 * kItems * kBatches;     // 1024
+constexpr uint32_t kTile = (kExpBlock / 32) * kWarpArcs;   // 8192 arcs per tile
+constexpr int kWarpQ = 384;       // warp-private output staging entries
 constexpr int kStage = 1536;      // max tile vertices staged in shared memory
 
 // lb 1: row starts + CTA-local exclusive prefix of degrees
@@ -97,6 +100,17 @@ __device__ __forceinline__ uint32_t lb_search(const unsigned long long* prefix,
   return lo;
 }
 
+// Visit a batch of pre-tested arcs.  The generic form calls visit() per arc; a
+// functor may provide an overload (found by argument-dependent lookup) that
+// issues its atomics for the whole batch before consuming any result, so a
+// thread keeps several atomics in flight.
+template <int K, class F>
+__device__ __forceinline__ void visit_batch(const F& f, const uint32_t* src, const uint32_t* nb,
+                                            const uint32_t* eid, const bool* pass, bool* acc) {
+#pragma unroll
+  for (int k = 0; k < K; ++k) acc[k] = pass[k] && f.visit(src[k], nb[k], eid[k]);
+}
+
 // lb 3a: first frontier entry of every tile (one binary search per tile, all
 // tiles in parallel) so the expansion never waits on a serial search
 static __global__ void lb_tiles_kernel(const unsigned long long* __restrict__ prefix,
@@ -128,11 +142,12 @@ __global__ void __launch_bounds__(kExpBlock)
   __shared__ unsigned long long s_pref[kStage + 1];
   __shared__ uint32_t s_row[kStage];
   __shared__ uint32_t s_src[kStage];
-  __shared__ BlockQueue<kTile> q;  // one global reservation per tile
-  q.reset();
+  __shared__ uint32_t s_q[kExpBlock / 32][kWarpQ];
   const unsigned long long total = *total_ptr;
   const unsigned long long ntiles = (total + kTile - 1) / kTile;
   const unsigned warp = threadIdx.x >> 5, lane = lane_id();
+  WarpQueue<kWarpQ, kWarpQ - 32 * kItems> q;
+  q.init(s_q[warp]);
   for (unsigned long long tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
     const unsigned long long t0 = tile * kTile;
     const unsigned long long t1 = t0 + kTile < total ? t0 + kTile : total;
@@ -155,45 +170,53 @@ __global__ void __launch_bounds__(kExpBlock)
       return staged ? s_pref[j]
                     : ((lo + j < n_in) ? lb_pref(prefix, block_off, lo + j) : total);
     };
-    const unsigned long long e0 = t0 + (unsigned long long)warp * 32 * kItems + lane;
+    // warp w owns arcs [t0 + w*kWarpArcs, +kWarpArcs), processed in kBatches
+    // batches of 32*kItems; lane l takes arcs l, l+32, ... of each batch
+    const unsigned long long w0 = t0 + (unsigned long long)warp * kWarpArcs + lane;
     uint32_t j = 0;
-    if (e0 < t1) {
-      uint32_t a = 0, b = R - 1;  // last j with pref(j) <= e0
+    if (w0 < t1) {
+      uint32_t a = 0, b = R - 1;  // last j with pref(j) <= w0
       while (a < b) {
         uint32_t m = (a + b + 1) >> 1;
-        if (pref(m) <= e0) a = m;
+        if (pref(m) <= w0) a = m;
         else b = m - 1;
       }
       j = a;
     }
-    uint32_t eid[kItems], src[kItems], nb[kItems];
-    unsigned long long jnext = e0 < t1 ? pref(j + 1) : 0;
+    unsigned long long jnext = w0 < t1 ? pref(j + 1) : 0;
+    for (int batch = 0; batch < kBatches; ++batch) {
+      const unsigned long long e0 = w0 + (unsigned long long)batch * 32 * kItems;
+      uint32_t eid[kItems], src[kItems], nb[kItems];
 #pragma unroll
-    for (int k = 0; k < kItems; ++k) {  // locate
-      const unsigned long long e = e0 + 32ull * k;
-      eid[k] = 0xFFFFFFFFu;
-      if (e < t1) {
-        while (e >= jnext) jnext = pref(++j + 1);
-        const unsigned long long base = pref(j);
-        eid[k] = (staged ? s_row[j] : rowstart[lo + j]) + (uint32_t)(e - base);
-        src[k] = staged ? s_src[j] : in[lo + j];
+      for (int k = 0; k < kItems; ++k) {  // locate
+        const unsigned long long e = e0 + 32ull * k;
+        eid[k] = 0xFFFFFFFFu;
+        if (e < t1) {
+          while (e >= jnext) jnext = pref(++j + 1);
+          const unsigned long long base = pref(j);
+          eid[k] = (staged ? s_row[j] : rowstart[lo + j]) + (uint32_t)(e - base);
+          src[k] = staged ? s_src[j] : in[lo + j];
+        }
       }
+#pragma unroll
+      for (int k = 0; k < kItems; ++k)  // neighbour IDs: independent, coalesced loads
+        nb[k] = eid[k] != 0xFFFFFFFFu ? __ldg(&g.col[eid[k]]) : 0u;
+      bool pass[kItems];
+#pragma unroll
+      for (int k = 0; k < kItems; ++k)  // pre-tests: independent loads
+        pass[k] = eid[k] != 0xFFFFFFFFu && f.prefilter(nb[k]);
+      bool acc[kItems];
+      visit_batch<kItems>(f, src, nb, eid, pass, acc);
+#pragma unroll
+      for (int k = 0; k < kItems; ++k) {
+        bool a = acc[k];
+        if (kFused && a) a = f.keep(nb[k]);
+        q.push(a, nb[k]);
+      }
+      q.flush(out_cnt, out, false);
     }
-#pragma unroll
-    for (int k = 0; k < kItems; ++k)  // neighbour IDs: independent, coalesced loads
-      nb[k] = eid[k] != 0xFFFFFFFFu ? __ldg(&g.col[eid[k]]) : 0u;
-    bool pass[kItems];
-#pragma unroll
-    for (int k = 0; k < kItems; ++k)  // pre-tests: independent loads
-      pass[k] = eid[k] != 0xFFFFFFFFu && f.prefilter(nb[k]);
-#pragma unroll
-    for (int k = 0; k < kItems; ++k) {
-      bool acc = pass[k] && f.visit(src[k], nb[k], eid[k]);
-      if (kFused && acc) acc = f.keep(nb[k]);
-      q.push(acc, nb[k]);
-    }
-    q.flush(out_cnt, out);
   }
+  q.flush(out_cnt, out, true);
 }
 
 // filter (engine.hpp:71-79): compaction by keep(v); input length read on device

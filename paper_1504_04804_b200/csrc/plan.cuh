@@ -112,7 +112,7 @@ struct Worker {
   DevArray<uint32_t> su32[4];
   DevArray<double> sf64[4];
   DevArray<unsigned long long> su64[3];
-  DevArray<uint32_t> aux[4];          // primitive-private scratch (bitmaps, queues)
+  DevArray<uint32_t> aux[6];          // primitive-private scratch (bitmaps, queues)
   DevArray<uint32_t> nonisolated;     // hosted vertices with out-degree > 0 (ascending)
   uint32_t n_nonisolated = 0;
   bool nonisolated_ready = false;
@@ -159,6 +159,8 @@ struct Plan {
   bool profile = false;
   double prof_ms = 0, prof_bytes = 0;
   uint64_t prof_launches = 0;
+  double prof2_ms = 0, prof2_bytes = 0;
+  uint64_t prof2_launches = 0;
 
   // multi-process bootstrap
   std::vector<void*> peer_arena;    // mapped inbox arenas of peers

@@ -150,7 +150,8 @@ struct BfsPrim : PrimBase {
 struct DobfsDev {
   uint32_t* labels;
   uint32_t* preds;
-  uint32_t* vis;  // visited bitmap
+  uint32_t* vis;             // visited bitmap (live)
+  const uint32_t* vis_snap;  // visited bitmap as of the start of the superstep
   OwnerView ow;
   uint32_t iter;
   int mark_preds;
@@ -166,6 +167,7 @@ struct DobfsDev {
     return true;
   }
   __device__ bool keep(uint32_t) const { return true; }
+  // pre-test on the live bitmap in L2 (an L1 copy would go stale)
   __device__ bool prefilter(uint32_t v) const {
     return !(__ldcg(&vis[v >> 5]) & (1u << (v & 31)));
   }
@@ -185,6 +187,45 @@ struct DobfsDev {
   __device__ bool send_filter(uint32_t, uint32_t) const { return true; }
   __device__ uint32_t peer_id(uint32_t v, uint32_t, uint32_t) const { return v; }
 };
+
+// batched forward visit: all test-and-set atomics of the batch in flight
+// before any result is consumed (see visit_batch in operators.cuh)
+template <int K>
+__device__ __forceinline__ void visit_batch(const DobfsDev& f, const uint32_t* src,
+                                            const uint32_t* nb, const uint32_t*,
+                                            const bool* pass, bool* acc) {
+  uint32_t old[K];
+#pragma unroll
+  for (int k = 0; k < K; ++k)
+    old[k] = pass[k] ? atomicOr(&f.vis[nb[k] >> 5], 1u << (nb[k] & 31)) : ~0u;
+#pragma unroll
+  for (int k = 0; k < K; ++k) {
+    acc[k] = !(old[k] & (1u << (nb[k] & 31)));
+    if (acc[k]) {
+      f.labels[nb[k]] = f.iter + 1;
+      if (f.mark_preds) f.preds[nb[k]] = f.ow.to_global(src[k]);
+    }
+  }
+}
+
+// fb = vis & ~prev (the level just discovered); prev = vis
+__global__ void frontier_diff_kernel(const uint32_t* __restrict__ vis, uint32_t* prev,
+                                     uint32_t* __restrict__ fb, uint32_t nw) {
+  const uint4* v4 = reinterpret_cast<const uint4*>(vis);
+  uint4* p4 = reinterpret_cast<uint4*>(prev);
+  uint4* f4 = reinterpret_cast<uint4*>(fb);
+  const uint32_t n4 = nw / 4;
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n4; i += gridDim.x * blockDim.x) {
+    uint4 a = v4[i], b = p4[i];
+    f4[i] = make_uint4(a.x & ~b.x, a.y & ~b.y, a.z & ~b.z, a.w & ~b.w);
+    p4[i] = a;
+  }
+  for (uint32_t i = n4 * 4 + blockIdx.x * blockDim.x + threadIdx.x; i < nw;
+       i += gridDim.x * blockDim.x) {
+    fb[i] = vis[i] & ~prev[i];
+    prev[i] = vis[i];
+  }
+}
 
 __global__ void bitmap_set_kernel(const uint32_t* __restrict__ in, uint32_t n, uint32_t* bits) {
   for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
@@ -371,6 +412,7 @@ struct DobfsPrim : PrimBase {
     ensure_nonisolated(w);  // plan-lifetime precomputation, outside the timed region on reuse
     fill(w.su32[0], w.nv, 0xFF, w.stream);        // labels
     fill(w.su32[2], words(w.nv), 0, w.stream);    // visited bitmap
+    fill(w.aux[4], words(w.nv), 0, w.stream);     // visited as of the previous superstep
     if (w.su32[3].n < words(w.nv) || !w.su32[3].ptr) w.su32[3].alloc(words(w.nv));  // frontier
     if (w.aux[3].n < w.n_nonisolated + 1 || !w.aux[3].ptr) w.aux[3].alloc(w.n_nonisolated + 1);
     if (mark_preds) fill(w.su32[1], w.nv, 0xFF, w.stream);
@@ -390,8 +432,8 @@ struct DobfsPrim : PrimBase {
   }
   DobfsDev dev(Ctx& c) {
     Worker& w = *c.w;
-    return {w.su32[0].ptr, w.su32[1].ptr, w.su32[2].ptr, c.owner_view(), (uint32_t)c.iter,
-            mark_preds ? 1 : 0};
+    return {w.su32[0].ptr, w.su32[1].ptr, w.su32[2].ptr, w.su32[3].ptr, c.owner_view(),
+            (uint32_t)c.iter, mark_preds ? 1 : 0};
   }
   void body(Ctx& c) {  // primitives.cpp:197-253
     Worker& w = *c.w;
@@ -415,16 +457,25 @@ struct DobfsPrim : PrimBase {
       }
       dir_log.push_back(dir);
     }
+    const uint64_t nw = words(w.nv);
     if (dir == 0) {
+      MGB_CUDA(cudaMemcpyAsync(w.aux[4].ptr, w.su32[2].ptr, 4 * nw, cudaMemcpyDeviceToDevice,
+                               w.stream));
+      if (c.P->profile) MGB_CUDA(cudaEventRecord(w.ev_k0, w.stream));
       c.pipeline(dev(c), w.nv);
+      if (c.P->profile) {
+        MGB_CUDA(cudaEventRecord(w.ev_k1, w.stream));
+        prof_pending_[w.p] = true;
+        prof_kind_[w.p] = 1;
+        prof_nul_[w.p] = c.in_count;
+      }
       return;
     }
-    // backward: frontier bitmap of the (global) input frontier
-    const uint64_t nw = words(w.nv);
-    MGB_CUDA(cudaMemsetAsync(w.su32[3].ptr, 0, 4 * nw, w.stream));
-    if (c.in_count)
-      MGB_LAUNCH(bitmap_set_kernel, grid_for(c.in_count, 256, kNumSMs * 8), 256, 0, w.stream,
-                 w.input.ptr, c.in_count, w.su32[3].ptr);
+    // backward: the (global) input frontier is exactly what became visited in
+    // the previous superstep, so its bitmap is vis & ~vis_prev — one streaming
+    // pass over |V|/32 words instead of an atomic per frontier vertex
+    MGB_LAUNCH(frontier_diff_kernel, grid_for(nw, 256, kNumSMs * 8), 256, 0, w.stream,
+               w.su32[2].ptr, w.aux[4].ptr, w.su32[3].ptr, (uint32_t)nw);
     const int src = ul_src[w.p];
     const uint32_t* ul = src < 0 ? w.nonisolated.ptr : w.aux[src].ptr;
     const int dst = src == 0 ? 1 : 0;
@@ -437,6 +488,7 @@ struct DobfsPrim : PrimBase {
     if (c.P->profile) {
       MGB_CUDA(cudaEventRecord(w.ev_k0, w.stream));
       prof_nul_[w.p] = nul;
+      prof_kind_[w.p] = 0;
     }
     if (nul) {
       MGB_LAUNCH(dobfs_pull_thread_kernel, grid_for(nul, 256, kNumSMs * 16), 256, 0, w.stream,
@@ -466,12 +518,22 @@ struct DobfsPrim : PrimBase {
     float ms = 0;
     MGB_CUDA(cudaEventElapsedTime(&ms, w.ev_k0, w.ev_k1));
     const Counters& h = *w.host_ctr;
+    if (prof_kind_[w.p] == 1) {
+      // push advance: frontier IDs 4 B + row offsets 8 B per frontier vertex,
+      // 4 B per examined arc, label + output 8 B per discovery
+      double bytes = 12.0 * prof_nul_[w.p] + 4.0 * (double)h.edges + 8.0 * (double)h.out_cnt;
+      c.P->prof2_ms += ms;
+      c.P->prof2_bytes += bytes;
+      c.P->prof2_launches += 1;
+      return;
+    }
     double bytes = 4.0 * prof_nul_[w.p] + 8.0 * (double)h.u[2] + 4.0 * (double)h.edges +
                    8.0 * (double)h.out_cnt + 4.0 * (double)h.misc;
     c.P->prof_ms += ms;
     c.P->prof_bytes += bytes;
     c.P->prof_launches += 1;
   }
+  std::vector<int> prof_kind_ = std::vector<int>(kMaxWorkers, 0);
   void finalize(Ctx& c, const GlobalView&) { collect_profile(c); }
   std::vector<bool> pending_ul_ = std::vector<bool>(kMaxWorkers, false);
   std::vector<bool> prof_pending_ = std::vector<bool>(kMaxWorkers, false);

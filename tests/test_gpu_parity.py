@@ -136,14 +136,15 @@ def test_bfs_isolated_source_and_errors():
 # --------------------------------------------------------------------------- DOBFS
 @pytest.mark.parametrize("n", [1, 2, 3, 4])
 @pytest.mark.parametrize("name", ["p4", "star5", "tri_iso", "rmat12"])
-def test_dobfs_labels_direction_log_and_work(G, name, n):
+@pytest.mark.parametrize("do_a,do_b", [(0.01, 0.1), (0.001, 0.1), (0.5, 0.9)])
+def test_dobfs_labels_direction_log_and_work(G, name, n, do_a, do_b):
     g = G[name]
     off, col, _ = g.arrays()
     plan, owner = plan_for(g, n, seed=n + 3)
-    r = mg.dobfs(plan, mg.DobfsOptions(source=0))
+    r = mg.dobfs(plan, mg.DobfsOptions(source=0, do_a=do_a, do_b=do_b))
     assert np.array_equal(r.labels, seq.bfs_levels(off, col, 0))
     if ref.available():
-        rr = ref.RefPlan(ref.RefGraph.from_csr(off, col), owner, n).dobfs(0)
+        rr = ref.RefPlan(ref.RefGraph.from_csr(off, col), owner, n).dobfs(0, do_a, do_b)
         assert list(r.direction_log) == list(rr.direction_log)
         assert r.stats.supersteps == rr.stats.supersteps
         assert r.stats.edges_examined == rr.stats.edges_examined  # first-hit scan count
