@@ -98,6 +98,16 @@ def pick_sources(off, count, seed=7):
     return [0] + [int(x) for x in extra]
 
 
+def allreduce(x, op):
+    """scalar all-reduce over ranks (device tensor under NCCL, host under gloo)"""
+    import torch
+    import torch.distributed as dist
+    dev = "cuda" if dist.get_backend() == "nccl" else "cpu"
+    t = torch.tensor([x], dtype=torch.float64, device=dev)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX if op == "max" else dist.ReduceOp.SUM)
+    return float(t.item())
+
+
 def reached_arcs(labels, deg):
     return int(deg[labels != 0xFFFFFFFF].sum())
 
@@ -106,6 +116,9 @@ def dist_env():
     rank = int(os.environ.get("RANK", 0))
     world = int(os.environ.get("WORLD_SIZE", 1))
     local = int(os.environ.get("LOCAL_RANK", rank))
+    # MG_BENCH_DEVICE pins every rank to one GPU (exercises the multi-process
+    # IPC path on a single-GPU box); default: one GPU per local rank
+    local = int(os.environ.get("MG_BENCH_DEVICE", local))
     return rank, world, local
 
 
@@ -150,7 +163,10 @@ def main():
         import torch
         import torch.distributed as dist
         torch.cuda.set_device(local)
-        dist.init_process_group("nccl", init_method="env://")
+        # NCCL for the bench plumbing (barrier / max-over-ranks); gloo when every
+        # rank is pinned to one GPU (NCCL refuses duplicate devices)
+        backend = "gloo" if "MG_BENCH_DEVICE" in os.environ else "nccl"
+        dist.init_process_group(backend, init_method="env://")
     workload = f"dobfs_rmat{args.scale}_ef{args.edge_factor}"
     if args.impl == "reference":
         return run_reference(args, rank, world, workload)
@@ -171,11 +187,25 @@ def run_ours(args, rank, world, local, workload):
     import paper_1504_04804_b200 as mg
     torch.cuda.set_device(local)
     hbm, hbm_kind = peaks()
-    # this rank's plan: one partition per GPU; until the multi-process fabric
-    # is wired into the bench, N > 1 runs independent replicas of the N=1 job
-    plan, prep_s = build_plan(args, 1, devices=[local])
+    # one partition per GPU: N = 1 is the single-partition plan; N > 1 is one
+    # process per GPU, partition_random(|V|, N, 7) (partition.cpp:31-40), ranks
+    # exchanging records through CUDA-IPC-mapped inboxes over NVLink
+    if world > 1:
+        import uuid
+        owner = mg.partition_random(1 << args.scale, world, 7)
+        key = [uuid.uuid4().hex if rank == 0 else None]
+        torch.distributed.broadcast_object_list(key, src=0)
+        t0 = time.time()
+        plan = mg.PartitionPlan.rmat_device_multiprocess(args.scale, args.edge_factor, args.seed,
+                                                         owner, world, rank, local, key[0])
+        prep_s = time.time() - t0
+        hosted = owner == rank
+    else:
+        plan, prep_s = build_plan(args, 1, devices=[local])
+        hosted = None
     g = plan.download_graph()
     off, col, _ = g.arrays()
+    del g
     deg = np.diff(off.astype(np.int64))
     sources = pick_sources(off, args.num_sources)
     cfg = mg.EngineConfig(policy=mg.AllocPolicyKind.Maximum, fused=mg.FusedMode.On)
@@ -186,9 +216,11 @@ def run_ours(args, rank, world, local, workload):
         s = sources[i % len(sources)]
         r = mg.dobfs(plan, opt(s), cfg)
         if s not in arcs:
-            arcs[s] = reached_arcs(r.labels, deg)
-            ref_depth = int(r.labels[r.labels != mg.kInfLabel].max())
-            assert r.stats.supersteps == ref_depth + 1
+            lab = r.labels if hosted is None else np.where(hosted, r.labels, 0xFFFFFFFF)
+            a = reached_arcs(lab, deg)
+            if world > 1:  # each rank holds its hosted labels only
+                a = int(allreduce(a, "sum"))
+            arcs[s] = a
     steps = [sources[i % len(sources)] for i in range(args.steps)]
     total_arcs = sum(arcs[s] for s in steps)
 
@@ -220,11 +252,9 @@ def run_ours(args, rank, world, local, workload):
         mg.lib().mg_plan_set_profiling(plan._h, 0)
         dev = acc["dev_ms"]
         if world > 1:
-            t = torch.tensor([dev], dtype=torch.float64, device="cuda")
-            torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
-            dev = float(t.item())
+            dev = allreduce(dev, "max")
         acc["dev_max_ms"] = dev
-        acc["value"] = total_arcs * world / (dev * 1e-3) / 1e9
+        acc["value"] = total_arcs / (dev * 1e-3) / 1e9
         # end to end: same calls, labels copied into pinned host memory each step
         e2e_t = 0.0
         for s in steps:
@@ -232,10 +262,8 @@ def run_ours(args, rank, world, local, workload):
             e2e_call(mg, plan, s, cfg, labels, do_a, do_b)
             e2e_t += time.perf_counter() - t0
         if world > 1:
-            t = torch.tensor([e2e_t], dtype=torch.float64, device="cuda")
-            torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
-            e2e_t = float(t.item())
-        acc["e2e"] = total_arcs * world / e2e_t / 1e9
+            e2e_t = allreduce(e2e_t, "max")
+        acc["e2e"] = total_arcs / e2e_t / 1e9
         return acc
 
     host = torch.empty(plan.num_global_vertices, dtype=torch.int32, pin_memory=True)
@@ -269,7 +297,7 @@ def run_ours(args, rank, world, local, workload):
         "warmup": args.warmup,
         "ms_per_step": round(dev_ms / args.steps, 4),
         "higher_is_better": True,
-        "scaling": "weak",
+        "scaling": "strong",
         "vs_baseline": None,
         "dtype": "u32",
         "data": "synthetic (hashed R-MAT generated on the GPU)",
@@ -279,7 +307,8 @@ def run_ours(args, rank, world, local, workload):
                          " symmetrized + deduplicated",
             "num_vertices": plan.num_global_vertices, "num_arcs": plan.num_global_edges,
             "partitions_per_gpu": 1,
-            "parallelism": "replicas" if world > 1 else "single",
+            "parallelism": f"partitioned x{world} (random, seed 7), CUDA IPC P2P exchange"
+            if world > 1 else "single partition",
             "sources": sources, "mean_reached_arcs": total_arcs // len(steps),
             "policy": "max + fused", "do_a": 0.01, "do_b": 0.1,
             "l2": "inputs larger than L2 (CSR %.1f GB vs 126 MB L2)" % (
@@ -360,7 +389,10 @@ def run_reference(args, rank, world, workload):
     sources = pick_sources(off, args.num_sources)
     rg = ref.RefGraph.from_csr(off, col)
     del g, col
-    rplan = ref.RefPlan(rg, np.zeros(len(off) - 1, np.uint32), 1)
+    # same partitioning as our arm: one reference worker thread per GPU rank
+    owner = (mg.partition_random(len(off) - 1, world, 7) if world > 1
+             else np.zeros(len(off) - 1, np.uint32))
+    rplan = ref.RefPlan(rg, owner, world)
     arcs = {}
     for i in range(args.warmup):
         s = sources[i % len(sources)]
@@ -381,9 +413,11 @@ def run_reference(args, rank, world, workload):
         "ms_per_step": round(ms / args.steps, 3), "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "u32", "data": "synthetic (hashed R-MAT)",
         "config": {"workload": workload, "scale": args.scale, "edge_factor": args.edge_factor,
-                   "sources": sources, "partitions": 1},
-        "cpu_baseline": {"value": round(v, 4), "unit": "GTEPS", "cores": 1, "kind": "reference",
-                         "sample": f"{args.steps} reference dobfs runs (engine wall_ms), n=1"},
+                   "sources": sources, "partitions": world},
+        "cpu_baseline": {"value": round(v, 4), "unit": "GTEPS", "cores": world,
+                         "kind": "reference",
+                         "sample": f"{args.steps} reference dobfs runs (engine wall_ms), "
+                                   f"n={world} partitions = {world} worker threads"},
         "e2e": {"value": round(v, 4), "unit": "GTEPS", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
     }))

@@ -245,14 +245,25 @@ enum { MG_RES_LABELS = 0, MG_RES_PREDS = 1, MG_RES_DISTS = 2, MG_RES_COMPONENTS 
 int mg_plan_fetch(mg_plan* plan, int which, void* host_out);
 
 /* --------------------------------------------------------------------------
- * multi-process fabric (one process per GPU, torchrun): the host bootstrap
- * exchanges the opaque per-rank handle blobs (CUDA IPC handles of the inbox
- * arenas) with any transport (torch.distributed all_gather), then every
- * rank attaches its peers.  Returns MG_EINVAL when called on a plan that
- * holds more than one local worker. */
-int mg_fabric_local_blob_size(const mg_plan* plan, uint64_t* bytes);
-int mg_fabric_local_blob(mg_plan* plan, void* blob);
-int mg_fabric_attach(mg_plan* plan, uint32_t rank, uint32_t world, const void* all_blobs);
+ * multi-process fabric (one process per GPU on one node, e.g. torchrun).
+ * Every rank calls the same constructor with the same partition map and the
+ * same job-unique `fabric_key`; rank r uploads only partition r to `device`.
+ * The ranks rendezvous through a POSIX shared-memory segment named after the
+ * key (host barrier + WorkerReport all-gather, the reference's Barrier and
+ * completion callback, engine.hpp:449-473/784-820) and map each other's inbox
+ * arenas with CUDA IPC, so the pack kernels store records straight into the
+ * peer GPU's HBM over NVLink.  Result buffers of a multi-process run receive
+ * this rank's hosted vertices only. */
+int mg_plan_create_mp(const mg_graph* g, const uint32_t* owner, uint32_t num_partitions,
+                      int duplication, uint32_t rank, int device, const char* fabric_key,
+                      mg_plan** out);
+int mg_plan_create_rmat_device_mp(int scale, int edge_factor, uint64_t seed, int with_weights,
+                                  uint32_t w_lo, uint32_t w_hi, uint64_t w_seed,
+                                  const uint32_t* owner, uint32_t num_partitions, uint32_t rank,
+                                  int device, const char* fabric_key, mg_plan** out);
+/* host protocol self-test (no GPU): `rounds` barriers + all-gathers among
+ * `world` processes; returns MG_OK when every gathered value checks out */
+int mg_fabric_selftest(const char* fabric_key, uint32_t rank, uint32_t world, uint32_t rounds);
 
 /* number of kernels this library has launched since load (evidence counter) */
 uint64_t mg_kernel_launch_count(void);

@@ -275,6 +275,32 @@ class PartitionPlan:
                                                 hi, ws, _p(own), n, devs, C.byref(out)))
         return cls(None, _handle=out.value)
 
+    @classmethod
+    def multiprocess(cls, g: Csr, owner, n, rank, device, key, duplication=MG_DUP_ALL):
+        """One process per GPU: this rank uploads partition `rank` to `device`
+        and rendezvous with its peers through the job-unique `key`
+        (include/mgraph_b200.h, mg_plan_create_mp)."""
+        own = np.ascontiguousarray(owner, np.uint32)
+        out = C.c_void_p()
+        _check(lib().mg_plan_create_mp(g._h, _p(own), n, duplication, rank, device,
+                                       key.encode(), C.byref(out)))
+        p = cls(None, _handle=out.value)
+        p.rank = rank
+        return p
+
+    @classmethod
+    def rmat_device_multiprocess(cls, scale, edge_factor, seed, owner, n, rank, device, key,
+                                 weights=None):
+        own = np.ascontiguousarray(owner, np.uint32)
+        lo, hi, ws = weights if weights else (0, 0, 0)
+        out = C.c_void_p()
+        _check(lib().mg_plan_create_rmat_device_mp(scale, edge_factor, seed, int(bool(weights)),
+                                                   lo, hi, ws, _p(own), n, rank, device,
+                                                   key.encode(), C.byref(out)))
+        p = cls(None, _handle=out.value)
+        p.rank = rank
+        return p
+
     def __del__(self):
         if getattr(self, "_h", None) and _lib is not None:
             _lib.mg_plan_destroy(self._h)

@@ -134,9 +134,10 @@ PROTOTYPES = {
     "mg_pagerank": (i32, [P, dbl, dbl, u64, C.POINTER(mg_config), P, C.POINTER(u64), P, u64,
                           C.POINTER(u64), C.POINTER(mg_stats)]),
     "mg_plan_fetch": (i32, [P, i32, P]),
-    "mg_fabric_local_blob_size": (i32, [P, C.POINTER(u64)]),
-    "mg_fabric_local_blob": (i32, [P, P]),
-    "mg_fabric_attach": (i32, [P, u32, u32, P]),
+    "mg_plan_create_mp": (i32, [P, P, u32, i32, u32, i32, C.c_char_p, PP]),
+    "mg_plan_create_rmat_device_mp": (i32, [i32, i32, u64, i32, u32, u32, u64, P, u32, u32, i32,
+                                            C.c_char_p, PP]),
+    "mg_fabric_selftest": (i32, [C.c_char_p, u32, u32, u32]),
     "mg_kernel_launch_count": (u64, []),
 }
 

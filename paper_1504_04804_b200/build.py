@@ -24,7 +24,7 @@ CXXFLAGS = ["-O3", "-std=c++17", "-fPIC", "-pthread", "-I" + CSRC,
             "-I" + os.path.join(ROOT, "include"), "-I/usr/local/cuda/include"]
 
 CU = ["plan.cu", "prims.cu", "api.cu", "gen.cu", "fabric.cu"]
-CPP = ["host_graph.cpp"]
+CPP = ["host_graph.cpp", "shm_fabric.cpp"]
 
 
 def _headers():

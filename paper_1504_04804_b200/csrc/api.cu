@@ -9,14 +9,11 @@
 namespace mgb {
 const char* last_error();
 int run_guarded(const std::function<void()>& f);
-Plan* plan_from_host(const HostPlan& H, const int* devices, std::shared_ptr<HostCsr> g);
+Plan* plan_from_host(const HostPlan& H, const int* devices, std::shared_ptr<HostCsr> g, int only);
 }  // namespace mgb
 
 using namespace mgb;
 
-struct mg_graph {
-  std::shared_ptr<HostCsr> g;
-};
 
 namespace {
 int wrap(const std::function<void()>& f) { return run_guarded(f); }
@@ -131,7 +128,7 @@ int mg_plan_create(const mg_graph* g, const uint32_t* owner, uint32_t n, int dup
     if (owner) own.assign(owner, owner + g->g->nv);
     else if (n != 1) throw Error(MG_EINVAL, "mg_plan_create: owner map required for n > 1");
     HostPlan H = build_plan(*g->g, own, n, dup);
-    *out = reinterpret_cast<mg_plan*>(plan_from_host(H, devices, g->g));
+    *out = reinterpret_cast<mg_plan*>(plan_from_host(H, devices, g->g, -1));
   });
 }
 

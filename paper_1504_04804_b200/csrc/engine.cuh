@@ -58,6 +58,11 @@ struct GlobalView {  // engine.hpp:225-253
   }
 };
 
+// multi-process report all-gather (fabric.cu)
+void fabric_exchange_reports(Plan& P, const WorkerReport& r, const Counters& c,
+                             std::vector<WorkerReport>& reports,
+                             std::vector<std::vector<uint32_t>>& sends, bool& overflow);
+
 // ---------------------------------------------------------------------------
 // split + pack: route every output vertex (engine.hpp:880-909) and store the
 // remote records directly into the destination inbox slot
@@ -369,6 +374,7 @@ void run_primitive(Plan& P, Prim& prim, const mg_config& cfg) {
     ctx[p].run = &rs;
     ctx[p].fused = fused;
   }
+  if (P.shm) fabric_sync(P);  // collective: map peers' (possibly regrown) arenas
   build_send_tables(P);
   P.h_matrix.assign(n, std::vector<uint64_t>(n, 0));
   P.prof_ms = 0;
@@ -461,6 +467,12 @@ void run_primitive(Plan& P, Prim& prim, const mg_config& cfg) {
       }
       MGB_CUDA(cudaEventRecord(rs.packed[p], w.stream));
     }
+    if (P.shm) {
+      // peers in other processes: their pack + publish kernels must have
+      // completed (system-scope fenced) before this rank merges (E:922)
+      for (uint32_t p : P.local_workers) MGB_CUDA(cudaStreamSynchronize(P.workers[p]->stream));
+      P.shm->barrier();
+    }
     // merge (after every peer's pack: event dependencies, no host barrier)
     for (uint32_t p : P.local_workers) {
       Worker& w = *P.workers[p];
@@ -522,6 +534,30 @@ void run_primitive(Plan& P, Prim& prim, const mg_config& cfg) {
       }
       it_edges += hc.edges;
       it_comb += hc.combine;
+    }
+    if (P.shm) {
+      // multi-process: every rank contributes its report; all ranks then hold
+      // the same GlobalView and reach the same stop decision (E:784-820)
+      const uint32_t me = P.rank;
+      std::vector<WorkerReport> reports;
+      std::vector<std::vector<uint32_t>> sends;
+      bool overflow = false;
+      fabric_exchange_reports(P, view.reports[me], *P.workers[me]->host_ctr, reports, sends,
+                              overflow);
+      if (overflow) throw Error(MG_EWORKER, "inbox overflow on a peer worker");
+      view.reports = reports;
+      it_edges = it_comb = 0;
+      for (uint32_t q = 0; q < n; ++q) {
+        it_edges += reports[q].edges_delta;
+        it_comb += reports[q].combine_delta;
+        if (q == me) continue;
+        h_src[q] = 0;
+        for (uint32_t d = 0; d < n; ++d) {
+          if (d == q) continue;
+          P.h_matrix[q][d] += sends[q][d];
+          h_src[q] += sends[q][d];
+        }
+      }
     }
     for (auto& r : view.reports) {
       view.total_out += r.out_frontier;

@@ -156,13 +156,13 @@ struct Scratch {
 
 }  // namespace
 
-Plan* plan_from_host(const HostPlan& H, const int* devices, std::shared_ptr<HostCsr> g);
 
 // Device plan from a device-resident global CSR (goff/gcol/gw on dev0; the
 // arrays are adopted by the plan).  Duplicate-All only.
 Plan* plan_from_device_csr(uint32_t nv, uint64_t ne, DevArray<uint32_t>& goff,
                            DevArray<uint32_t>& gcol, DevArray<uint32_t>& gw,
-                           const std::vector<uint32_t>& owner, uint32_t n, const int* devices) {
+                           const std::vector<uint32_t>& owner, uint32_t n, const int* devices,
+                           int only) {
   int ndev = 0;
   MGB_CUDA(cudaGetDeviceCount(&ndev));
   auto P = new Plan();
@@ -179,7 +179,12 @@ Plan* plan_from_device_csr(uint32_t nv, uint64_t ne, DevArray<uint32_t>& goff,
       if (P->devices[p] < 0 || P->devices[p] >= ndev)
         throw Error(MG_EINVAL, "mg_plan_create: device ordinal out of range");
     }
-    const int dev0 = P->devices[0];
+    if (only >= 0) {
+      P->multiprocess = true;
+      P->rank = (uint32_t)only;
+      P->world = n;
+    }
+    const int dev0 = P->devices[only >= 0 ? only : 0];
     DeviceGuard dg(dev0);
     cudaStream_t s;
     MGB_CUDA(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
@@ -216,6 +221,37 @@ Plan* plan_from_device_csr(uint32_t nv, uint64_t ne, DevArray<uint32_t>& goff,
       MGB_CUDA(cudaMemcpy(hosted.ptr, w.hosted_host.data(), 4ull * nh, cudaMemcpyHostToDevice));
       w.nlocal = nh;
       P->nlocal[p] = nh;
+      // borders of p (all p, so every rank knows every |B_{p,q}|): distinct
+      // neighbours owned by q != p, from the global rows of p's vertices
+      std::vector<uint32_t> border;
+      w.border_len.assign(n, 0);
+      w.border_off.assign(n, 0);
+      if (n > 1) {
+        MGB_CUDA(cudaMemsetAsync(bits.ptr, 0, 4ull * ((nv + 31) / 32 + 1), s));
+        if (nh)
+          MGB_LAUNCH(border_mark_kernel, grid_for((uint64_t)nh * 32, 256, 8192), 256, 0, s,
+                     goff.ptr, gcol.ptr, hosted.ptr, nh, down.ptr, p, bits.ptr);
+        for (uint32_t q = 0; q < n; ++q) {
+          w.border_off[q] = border.size();
+          if (q == p) continue;
+          MGB_CUDA(cudaMemsetAsync(cnt.ptr, 0, 4, s));
+          MGB_LAUNCH(border_collect_kernel, grid_for((nv + 31) / 32, 256, 4096), 256, 0, s,
+                     bits.ptr, nv, down.ptr, q, tmp.ptr, cnt.ptr);
+          uint32_t nb = 0;
+          MGB_CUDA(cudaMemcpyAsync(&nb, cnt.ptr, 4, cudaMemcpyDeviceToHost, s));
+          MGB_CUDA(cudaStreamSynchronize(s));
+          size_t at = border.size();
+          border.resize(at + nb);
+          MGB_CUDA(cudaMemcpy(border.data() + at, tmp.ptr, 4ull * nb, cudaMemcpyDeviceToHost));
+          std::sort(border.begin() + at, border.end());
+          w.border_len[q] = nb;
+          P->pair_border[p][q] = nb;
+        }
+      }
+      if (only >= 0 && (int)p != only) {  // another process owns this partition
+        hosted.free_();
+        continue;
+      }
       // sub-CSR
       DevArray<uint32_t> soff, scol, sw;
       if (n == 1) {
@@ -242,32 +278,6 @@ Plan* plan_from_device_csr(uint32_t nv, uint64_t ne, DevArray<uint32_t>& goff,
         w.ne = sne;
       }
       if (n == 1) w.ne = ne;
-      // borders of p: distinct neighbours owned by q != p (counts + lists)
-      std::vector<uint32_t> border;
-      w.border_len.assign(n, 0);
-      w.border_off.assign(n, 0);
-      if (n > 1) {
-        MGB_CUDA(cudaMemsetAsync(bits.ptr, 0, 4ull * ((nv + 31) / 32 + 1), s));
-        if (nh)
-          MGB_LAUNCH(border_mark_kernel, grid_for((uint64_t)nh * 32, 256, 8192), 256, 0, s,
-                     soff.ptr, scol.ptr, hosted.ptr, nh, down.ptr, p, bits.ptr);
-        for (uint32_t q = 0; q < n; ++q) {
-          w.border_off[q] = border.size();
-          if (q == p) continue;
-          MGB_CUDA(cudaMemsetAsync(cnt.ptr, 0, 4, s));
-          MGB_LAUNCH(border_collect_kernel, grid_for((nv + 31) / 32, 256, 4096), 256, 0, s,
-                     bits.ptr, nv, down.ptr, q, tmp.ptr, cnt.ptr);
-          uint32_t nb = 0;
-          MGB_CUDA(cudaMemcpyAsync(&nb, cnt.ptr, 4, cudaMemcpyDeviceToHost, s));
-          MGB_CUDA(cudaStreamSynchronize(s));
-          size_t at = border.size();
-          border.resize(at + nb);
-          MGB_CUDA(cudaMemcpy(border.data() + at, tmp.ptr, 4ull * nb, cudaMemcpyDeviceToHost));
-          std::sort(border.begin() + at, border.end());
-          w.border_len[q] = nb;
-          P->pair_border[p][q] = nb;
-        }
-      }
       // move the partition to its device
       if (w.dev == dev0) {
         w.off = soff;
@@ -402,6 +412,7 @@ extern "C" int mg_plan_create_rmat_device(int scale, int ef, uint64_t seed, int 
     uint64_t ne = 0;
     device_rmat_csr(devices ? devices[0] : 0, scale, ef, seed, with_w, lo, hi, wseed, off, col, w,
                     &ne);
-    *out = reinterpret_cast<mg_plan*>(plan_from_device_csr(nv, ne, off, col, w, own, n, devices));
+    *out = reinterpret_cast<mg_plan*>(
+        plan_from_device_csr(nv, ne, off, col, w, own, n, devices, -1));
   });
 }

@@ -32,10 +32,21 @@ static void free_worker(Worker& w) {
 
 void plan_free(Plan* P) {
   if (!P) return;
+  if (P->shm) {
+    // peers may still be writing into this rank's inboxes: free only after
+    // every rank stopped using the fabric
+    try {
+      for (uint32_t p : P->local_workers) cudaStreamSynchronize(P->workers[p]->stream);
+      P->shm->barrier();
+    } catch (...) {
+    }
+  }
   for (auto& w : P->workers)
     if (w) free_worker(*w);
   for (size_t i = 0; i < P->peer_arena.size(); ++i)
     if (P->peer_arena[i]) cudaIpcCloseMemHandle(P->peer_arena[i]);
+  for (size_t i = 0; i < P->peer_cnt.size(); ++i)
+    if (P->peer_cnt[i]) cudaIpcCloseMemHandle(P->peer_cnt[i]);
   P->g_off.free_(); P->g_col.free_(); P->g_w.free_();
   delete P;
 }
@@ -102,7 +113,9 @@ static void upload_worker(Plan& P, const HostPlan& H, uint32_t p) {
   P.workers[p] = std::move(wp);
 }
 
-Plan* plan_from_host(const HostPlan& H, const int* devices, std::shared_ptr<HostCsr> g) {
+// only >= 0: multi-process mode, upload partition `only` to devices[only]
+Plan* plan_from_host(const HostPlan& H, const int* devices, std::shared_ptr<HostCsr> g,
+                     int only) {
   if (H.n > 255 || H.n > kMaxWorkers)
     throw Error(MG_EINVAL, "mg_plan_create: at most 64 partitions are supported");
   int ndev = 0;
@@ -119,8 +132,13 @@ Plan* plan_from_host(const HostPlan& H, const int* devices, std::shared_ptr<Host
     P->devices.resize(H.n);
     for (uint32_t p = 0; p < H.n; ++p) {
       P->devices[p] = devices ? devices[p] : 0;
-      if (P->devices[p] < 0 || P->devices[p] >= ndev)
+      if ((only < 0 || (int)p == only) && (P->devices[p] < 0 || P->devices[p] >= ndev))
         throw Error(MG_EINVAL, "mg_plan_create: device ordinal out of range");
+    }
+    if (only >= 0) {
+      P->multiprocess = true;
+      P->rank = (uint32_t)only;
+      P->world = H.n;
     }
     P->workers.resize(H.n);
     P->pair_border.assign(H.n, std::vector<uint64_t>(H.n, 0));
@@ -130,7 +148,7 @@ Plan* plan_from_host(const HostPlan& H, const int* devices, std::shared_ptr<Host
       for (uint32_t j = 0; j < H.n; ++j) P->pair_border[i][j] = H.borders[i][j].size();
     }
     // enable peer access between distinct devices used by this plan
-    for (uint32_t a = 0; a < H.n; ++a)
+    for (uint32_t a = 0; a < H.n && only < 0; ++a)
       for (uint32_t b = 0; b < H.n; ++b) {
         int da = P->devices[a], db = P->devices[b];
         if (da == db) continue;
@@ -145,6 +163,7 @@ Plan* plan_from_host(const HostPlan& H, const int* devices, std::shared_ptr<Host
         }
       }
     for (uint32_t p = 0; p < H.n; ++p) {
+      if (only >= 0 && (int)p != only) continue;
       upload_worker(*P, H, p);
       P->local_workers.push_back(p);
     }
@@ -188,6 +207,7 @@ void ensure_inboxes(Plan& P, Worker& w, int nva, int nvv, const std::vector<uint
   // inbox memory is charged to the receiving worker's budget (engine.hpp:340-344)
   w.budget.charge(bytes, w.arena.n);
   w.arena.alloc(bytes ? bytes : 256);
+  ++w.arena_gen;
   uint8_t* base = w.arena.ptr;
   auto carve = [&](uint64_t b) {
     uint8_t* r = base;
@@ -219,7 +239,13 @@ void build_send_tables(Plan& P) {
     std::vector<uint32_t*> cnt(2 * n, nullptr);
     for (int par = 0; par < 2; ++par)
       for (uint32_t q = 0; q < n; ++q) {
-        if (q == p || !P.workers[q]) continue;  // multi-process peers: see fabric.cu
+        if (q == p) continue;
+        if (P.shm) {  // peer in another process: IPC mappings (fabric.cu)
+          table[par * n + q] = P.peer_slots[par * n + q];
+          cnt[par * n + q] =
+              static_cast<uint32_t*>(P.peer_cnt[q]) + par * kMaxWorkers + p;
+          continue;
+        }
         Worker& d = *P.workers[q];
         table[par * n + q] = d.slots[par][p];
         cnt[par * n + q] = d.inbox_cnt.ptr + par * kMaxWorkers + p;

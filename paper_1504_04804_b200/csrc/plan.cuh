@@ -13,6 +13,7 @@
 #include <vector>
 
 #include "common.cuh"
+#include "shm_fabric.hpp"
 
 namespace mgb {
 
@@ -100,6 +101,7 @@ struct Worker {
   int nva = 0, nvv = 0;
   std::vector<uint64_t> slot_cap;  // per src
   DevArray<uint8_t> arena;
+  uint64_t arena_gen = 0;          // bumped whenever the arena is reallocated
   SlotView slots[2][kMaxWorkers];
   DevArray<uint32_t> inbox_cnt;    // [2][kMaxWorkers], written by senders
   // sender side: where this worker's records for each peer go, per parity
@@ -162,13 +164,26 @@ struct Plan {
   double prof2_ms = 0, prof2_bytes = 0;
   uint64_t prof2_launches = 0;
 
-  // multi-process bootstrap
-  std::vector<void*> peer_arena;    // mapped inbox arenas of peers
-  std::vector<uint64_t> peer_arena_bytes;
+  // multi-process fabric (one worker per process): shared-memory rendezvous +
+  // CUDA IPC mappings of the peers' inbox arenas and slot counters
+  std::unique_ptr<ShmFabric> shm;
+  std::vector<void*> peer_arena;     // mapped inbox arenas of peers (by rank)
+  std::vector<void*> peer_cnt;       // mapped inbox counters of peers
+  std::vector<uint64_t> peer_gen;    // arena generation each mapping belongs to
+  std::vector<SlotView> peer_slots;  // [2][n]: peer q's slot for records from this rank
 };
+
+struct WorkerReport;
+// multi-process fabric (fabric.cu)
+void fabric_sync(Plan& P);
 
 Worker& worker(Plan& P, uint32_t p);
 void init_worker_runtime(Worker& w);
 void plan_free(Plan* P);
 
 }  // namespace mgb
+
+// the C-ABI's opaque host graph (include/mgraph_b200.h)
+struct mg_graph {
+  std::shared_ptr<mgb::HostCsr> g;
+};
