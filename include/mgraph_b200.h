@@ -109,6 +109,11 @@ int mg_plan_create_rmat_device(int scale, int edge_factor, uint64_t seed, int wi
                                uint32_t w_lo, uint32_t w_hi, uint64_t w_seed,
                                const uint32_t* owner, uint32_t num_partitions,
                                const int* devices, mg_plan** out);
+/* device-generated random geometric graph:
+ * n_vertices points uniform in the unit square, edge iff distance <
+ * 0.55*sqrt(ln n / n); vertex IDs in generation order */
+int mg_plan_create_rgg_device(uint32_t n_vertices, uint64_t seed, const uint32_t* owner,
+                              uint32_t num_partitions, const int* devices, mg_plan** out);
 void mg_plan_destroy(mg_plan* plan);
 int mg_plan_info(const mg_plan* plan, uint32_t* num_vertices, uint64_t* num_edges,
                  uint32_t* num_partitions);

@@ -276,6 +276,16 @@ class PartitionPlan:
         return cls(None, _handle=out.value)
 
     @classmethod
+    def rgg_device(cls, num_vertices, seed, owner=None, n=1, devices=None):
+        """random geometric graph generated + partitioned on the GPU (r = 0.55 sqrt(ln n/n))"""
+        own = None if owner is None else np.ascontiguousarray(owner, np.uint32)
+        devs = None if devices is None else (C.c_int * n)(*devices)
+        out = C.c_void_p()
+        _check(lib().mg_plan_create_rgg_device(num_vertices, seed, _p(own), n, devs,
+                                               C.byref(out)))
+        return cls(None, _handle=out.value)
+
+    @classmethod
     def multiprocess(cls, g: Csr, owner, n, rank, device, key, duplication=MG_DUP_ALL):
         """One process per GPU: this rank uploads partition `rank` to `device`
         and rendezvous with its peers through the job-unique `key`

@@ -113,6 +113,7 @@ PROTOTYPES = {
     "mg_partition_biased_random": (i32, [P, u32, u64, dbl, P]),
     "mg_plan_create": (i32, [P, P, u32, i32, P, PP]),
     "mg_plan_create_rmat_device": (i32, [i32, i32, u64, i32, u32, u32, u64, P, u32, P, PP]),
+    "mg_plan_create_rgg_device": (i32, [u32, u64, P, u32, P, PP]),
     "mg_plan_destroy": (None, [P]),
     "mg_plan_info": (i32, [P, C.POINTER(u32), C.POINTER(u64), C.POINTER(u32)]),
     "mg_plan_border_metrics": (i32, [P, P, C.POINTER(u64)]),

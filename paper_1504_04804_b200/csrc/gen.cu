@@ -9,6 +9,7 @@
 #include <cub/device/device_scan.cuh>
 #include <cub/device/device_select.cuh>
 
+#include <cmath>
 #include <cstring>
 #include <functional>
 #include <memory>
@@ -391,9 +392,172 @@ void device_rmat_csr(int dev, int scale, int ef, uint64_t seed, int with_w, uint
   *ne_out = ne;
 }
 
+// ---------------------------------------------------------------------------
+// random geometric graph: n points
+// i.i.d. uniform in the unit square, an edge iff Euclidean distance < r,
+// r = 0.55 * sqrt(ln n / n).  Point i = (u(mix64(s+2i)), u(mix64(s+2i+1))),
+// so vertex numbering is the generation order (random w.r.t. space).  Points
+// are bucketed into an r-grid; each point tests the 9 surrounding cells.
+
+__device__ __forceinline__ double rgg_coord(uint64_t sm, uint64_t k) {
+  return (double)(mix64_hd(sm + k) >> 11) * (1.0 / 9007199254740992.0);
+}
+
+__global__ void rgg_cells_kernel(uint64_t sm, uint32_t n, double r, uint32_t G,
+                                 uint32_t* cell, uint32_t* idx) {
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    double x = rgg_coord(sm, 2ull * i), y = rgg_coord(sm, 2ull * i + 1);
+    uint32_t cx = min((uint32_t)(x / r), G - 1), cy = min((uint32_t)(y / r), G - 1);
+    cell[i] = cy * G + cx;
+    idx[i] = i;
+  }
+}
+
+__global__ void rgg_cell_start_kernel(const uint32_t* sorted_cell, uint32_t n, uint32_t ncell,
+                                      uint32_t* start) {
+  for (uint32_t c = blockIdx.x * blockDim.x + threadIdx.x; c <= ncell;
+       c += gridDim.x * blockDim.x) {
+    uint32_t lo = 0, hi = n;  // first i with sorted_cell[i] >= c
+    while (lo < hi) {
+      uint32_t m = (lo + hi) >> 1;
+      if (sorted_cell[m] < c) lo = m + 1;
+      else hi = m;
+    }
+    start[c] = lo;
+  }
+}
+
+// pass 0: count neighbours; pass 1: emit (i << 32 | j) keys at key_off[i]
+template <int kPass>
+__global__ void rgg_pairs_kernel(uint64_t sm, uint32_t n, double r, uint32_t G,
+                                 const uint32_t* cell_start, const uint32_t* order,
+                                 uint32_t* deg, const unsigned long long* key_off,
+                                 unsigned long long* keys) {
+  const double r2 = r * r;
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    double x = rgg_coord(sm, 2ull * i), y = rgg_coord(sm, 2ull * i + 1);
+    int cx = min((int)(x / r), (int)G - 1), cy = min((int)(y / r), (int)G - 1);
+    uint32_t cnt = 0;
+    unsigned long long at = kPass ? key_off[i] : 0;
+    for (int dy = -1; dy <= 1; ++dy)
+      for (int dx = -1; dx <= 1; ++dx) {
+        int X = cx + dx, Y = cy + dy;
+        if (X < 0 || Y < 0 || X >= (int)G || Y >= (int)G) continue;
+        uint32_t c = (uint32_t)Y * G + (uint32_t)X;
+        for (uint32_t k = cell_start[c]; k < cell_start[c + 1]; ++k) {
+          uint32_t j = order[k];
+          if (j == i) continue;
+          double ddx = rgg_coord(sm, 2ull * j) - x, ddy = rgg_coord(sm, 2ull * j + 1) - y;
+          if (ddx * ddx + ddy * ddy < r2) {
+            if (kPass) keys[at++] = ((unsigned long long)i << 32) | j;
+            ++cnt;
+          }
+        }
+      }
+    if (!kPass) deg[i] = cnt;
+  }
+}
+
+__global__ void csr_from_sorted_pairs_kernel(const unsigned long long* keys, uint64_t ne,
+                                             uint32_t* col) {
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < ne;
+       i += (uint64_t)gridDim.x * blockDim.x)
+    col[i] = (uint32_t)keys[i];
+}
+
+void device_rgg_csr(int dev, uint32_t n, uint64_t seed, DevArray<uint32_t>& off,
+                    DevArray<uint32_t>& col, uint64_t* ne_out) {
+  if (n < 2) throw Error(MG_EINVAL, "rgg: need at least 2 vertices");
+  DeviceGuard dg(dev);
+  cudaStream_t s;
+  MGB_CUDA(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+  const double r = 0.55 * std::sqrt(std::log((double)n) / (double)n);
+  const uint32_t G = (uint32_t)std::ceil(1.0 / r);
+  const uint32_t ncell = G * G;
+  const uint64_t sm = mix64_hd(seed);
+  DevArray<uint32_t> cell, idx, cell2, order, start, deg;
+  cell.alloc(n);
+  idx.alloc(n);
+  cell2.alloc(n);
+  order.alloc(n);
+  start.alloc(ncell + 1ull);
+  deg.alloc(n + 1ull);
+  MGB_LAUNCH(rgg_cells_kernel, grid_for(n, 256, 148 * 32), 256, 0, s, sm, n, r, G, cell.ptr,
+             idx.ptr);
+  Scratch scr;
+  size_t tb = 0;
+  cub::DeviceRadixSort::SortPairs(nullptr, tb, cell.ptr, cell2.ptr, idx.ptr, order.ptr, n, 0, 32,
+                                  s);
+  scr.need(tb);
+  cub::DeviceRadixSort::SortPairs(scr.p, tb, cell.ptr, cell2.ptr, idx.ptr, order.ptr, n, 0, 32,
+                                  s);
+  MGB_LAUNCH(rgg_cell_start_kernel, grid_for(ncell + 1ull, 256, 148 * 32), 256, 0, s, cell2.ptr,
+             n, ncell, start.ptr);
+  MGB_LAUNCH(rgg_pairs_kernel<0>, grid_for(n, 256, 148 * 32), 256, 0, s, sm, n, r, G, start.ptr,
+             order.ptr, deg.ptr, (const unsigned long long*)nullptr,
+             (unsigned long long*)nullptr);
+  DevArray<unsigned long long> koff;
+  koff.alloc(n + 1ull);
+  // exclusive scan of the degrees (u32 -> u64 offsets)
+  MGB_CUDA(cudaMemsetAsync(deg.ptr + n, 0, 4, s));
+  tb = 0;
+  cub::DeviceScan::ExclusiveSum(nullptr, tb, deg.ptr, koff.ptr, n + 1, s);
+  scr.need(tb);
+  cub::DeviceScan::ExclusiveSum(scr.p, tb, deg.ptr, koff.ptr, n + 1, s);
+  unsigned long long ne = 0;
+  MGB_CUDA(cudaMemcpyAsync(&ne, koff.ptr + n, 8, cudaMemcpyDeviceToHost, s));
+  MGB_CUDA(cudaStreamSynchronize(s));
+  if (ne > 0xFFFFFFFFull) throw Error(MG_EINVAL, "rgg: more than 2^32-1 arcs");
+  DevArray<unsigned long long> k0, k1;
+  k0.alloc(ne ? ne : 1);
+  k1.alloc(ne ? ne : 1);
+  MGB_LAUNCH(rgg_pairs_kernel<1>, grid_for(n, 256, 148 * 32), 256, 0, s, sm, n, r, G, start.ptr,
+             order.ptr, deg.ptr, koff.ptr, k0.ptr);
+  // rows come out grouped by source; sort to get ascending neighbour IDs
+  cub::DoubleBuffer<unsigned long long> db(k0.ptr, k1.ptr);
+  tb = 0;
+  cub::DeviceRadixSort::SortKeys(nullptr, tb, db, (int64_t)ne, 0, 64, s);
+  scr.need(tb);
+  cub::DeviceRadixSort::SortKeys(scr.p, tb, db, (int64_t)ne, 0, 64, s);
+  off.alloc(n + 1ull);
+  col.alloc(ne ? ne : 1);
+  // row offsets = exclusive degree prefix (u32), columns = low words
+  std::vector<unsigned long long> hoff(n + 1ull);
+  MGB_CUDA(cudaMemcpyAsync(hoff.data(), koff.ptr, 8ull * (n + 1), cudaMemcpyDeviceToHost, s));
+  MGB_CUDA(cudaStreamSynchronize(s));
+  std::vector<uint32_t> hoff32(hoff.begin(), hoff.end());
+  MGB_CUDA(cudaMemcpy(off.ptr, hoff32.data(), 4ull * (n + 1), cudaMemcpyHostToDevice));
+  MGB_LAUNCH(csr_from_sorted_pairs_kernel, 148 * 32, 256, 0, s, db.Current(), ne, col.ptr);
+  MGB_CUDA(cudaStreamSynchronize(s));
+  for (auto* a : {&cell, &idx, &cell2, &order, &start, &deg}) a->free_();
+  koff.free_();
+  k0.free_();
+  k1.free_();
+  cudaStreamDestroy(s);
+  *ne_out = ne;
+}
+
 }  // namespace mgb
 
 using namespace mgb;
+
+extern "C" int mg_plan_create_rgg_device(uint32_t n_vertices, uint64_t seed, const uint32_t* owner,
+                                         uint32_t n, const int* devices, mg_plan** out) {
+  return run_guarded([&] {
+    if (n == 0 || n > kMaxWorkers) throw Error(MG_EINVAL, "mg_plan_create_rgg_device: bad n");
+    if (n > 1 && !owner)
+      throw Error(MG_EINVAL, "mg_plan_create_rgg_device: owner map required for n > 1");
+    std::vector<uint32_t> own(n_vertices, 0);
+    if (owner) own.assign(owner, owner + n_vertices);
+    for (uint32_t o : own)
+      if (o >= n) throw Error(MG_EINVAL, "build_partition_plan: owner out of range");
+    DevArray<uint32_t> off, col, w;
+    uint64_t ne = 0;
+    device_rgg_csr(devices ? devices[0] : 0, n_vertices, seed, off, col, &ne);
+    *out = reinterpret_cast<mg_plan*>(
+        plan_from_device_csr(n_vertices, ne, off, col, w, own, n, devices, -1));
+  });
+}
 
 extern "C" int mg_plan_create_rmat_device(int scale, int ef, uint64_t seed, int with_w,
                                           uint32_t lo, uint32_t hi, uint64_t wseed,
