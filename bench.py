@@ -40,14 +40,15 @@ def peaks():
         return HBM_FALLBACK, "fallback"
 
 
-def ncu_traffic():
-    """dram bytes per pull-step launch pair from the committed ncu capture, if any"""
+def ncu_traffic(kind):
+    """dram bytes per launch of the dominant kernel from the committed ncu capture"""
     p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     try:
         with open(p) as f:
-            return json.load(f).get("dobfs_pull_bytes_per_launch")
+            d = json.load(f)
+        return d.get(f"dobfs_{kind}_bytes_per_launch"), d.get(f"dobfs_{kind}_launch")
     except Exception:
-        return None
+        return None, None
 
 
 class Clocks:
@@ -287,7 +288,7 @@ def run_ours(args, rank, world, local, workload):
             cpu = {"value": None, "unit": "GTEPS", "cores": 1, "kind": "reference",
                    "sample": f"unavailable: {ex}"}
     achieved = prof["bytes"] / (prof["ms"] * 1e-3) / 1e9 if prof["ms"] else None
-    traffic = ncu_traffic()
+    traffic, traffic_src = ncu_traffic(kind)
     line = {
         "metric": "DOBFS GTEPS (A_r / t) on RMAT",
         "value": round(value, 3),
@@ -326,7 +327,7 @@ def run_ours(args, rank, world, local, workload):
                      "achieved": round(achieved, 1) if achieved else None, "peak": hbm,
                      "peak_kind": hbm_kind, "unit": "GB/s",
                      "frac": round(achieved / hbm, 4) if achieved else None,
-                     "traffic": traffic,
+                     "traffic": traffic, "traffic_source": traffic_src,
                      "algorithmic_bytes_per_launch": prof["bytes"] / max(prof["launches"], 1),
                      "avg_launch_ms": prof["ms"] / max(prof["launches"], 1),
                      "share_of_step": round(prof["ms"] / prof["dev_ms"], 4) if prof["dev_ms"]
