@@ -225,7 +225,7 @@ def run_ours(args, rank, world, local, workload):
     steps = [sources[i % len(sources)] for i in range(args.steps)]
     total_arcs = sum(arcs[s] for s in steps)
 
-    def timed(do_a, do_b):
+    def timed(do_a, do_b, cfg=cfg):
         """K device-resident steps; CUDA-event times from the library stream"""
         mg.lib().mg_plan_set_profiling(plan._h, 1)
         for s in sources[:2]:  # warm this parameter set
@@ -271,6 +271,10 @@ def run_ours(args, rank, world, local, workload):
     labels = host.numpy().view(np.uint32)
     main = timed(0.01, 0.1)        # the reference's defaults (primitives.hpp:69-70)
     tuned = timed(0.001, 0.1)      # do_a tuned for RMAT (per graph type)
+    exact = None
+    if world == 1:  # extension: exact-cost physical direction (mg_config.dobfs_exact_cost)
+        exact = timed(0.01, 0.1, mg.EngineConfig(policy=mg.AllocPolicyKind.Maximum,
+                                                 fused=mg.FusedMode.On, dobfs_exact_cost=True))
     dev_ms, value, e2e, clk, launches, wall = (main["dev_max_ms"], main["value"], main["e2e"],
                                               main["clocks"], main["launches"], main["wall"])
     kind = "push" if main["push"][0] >= main["pull"][0] else "pull"
@@ -341,6 +345,13 @@ def run_ours(args, rank, world, local, workload):
                   "e2e": round(tuned["e2e"], 3),
                   "note": "same graph and sources; the reference with the same do_a takes the "
                           "same direction decisions (direction log checked in tests)"},
+        "exact_cost": None if exact is None else {
+            "do_a": 0.01, "do_b": 0.1, "value": round(exact["value"], 3),
+            "ms_per_step": round(exact["dev_max_ms"] / args.steps, 4),
+            "e2e": round(exact["e2e"], 3),
+            "note": "extension mg_config.dobfs_exact_cost: logically-forward supersteps whose "
+                    "exact edge count exceeds 4x the unvisited list run on the pull kernel; "
+                    "labels, direction log, S and reported W stay the reference's (tested)"},
         "cpu_baseline": cpu,
         "clocks": clk,
         "gpu_launches": launches,

@@ -253,6 +253,7 @@ struct EngineConfig {
   uint32_t h_inflation = 1;
   std::optional<DropPackage> drop_package;
   uint64_t max_supersteps = 1000000;
+  bool dobfs_exact_cost = false;  // extension: see mg_config
 
   mg_config to_c() const {
     mg_config c;
@@ -275,6 +276,7 @@ struct EngineConfig {
       c.drop_iteration = drop_package->iteration;
     }
     c.max_supersteps = max_supersteps;
+    c.dobfs_exact_cost = dobfs_exact_cost ? 1 : 0;
     return c;
   }
 };

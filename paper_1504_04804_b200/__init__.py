@@ -225,6 +225,7 @@ class EngineConfig:
     h_inflation: int = 1
     drop_package: Optional[DropPackage] = None
     max_supersteps: int = 1000000
+    dobfs_exact_cost: bool = False
 
     def to_c(self):
         c = abi.default_config()
@@ -234,6 +235,7 @@ class EngineConfig:
         c.h_inflation = self.h_inflation
         c.max_supersteps = self.max_supersteps
         c.hard_cap_bytes = self.hard_cap_bytes
+        c.dobfs_exact_cost = int(self.dobfs_exact_cost)
         for k, v in self.factors.items():
             c.factors[ROLES.index(k)] = v
         if self.drop_package is not None:

@@ -36,6 +36,7 @@ class mg_config(C.Structure):
         ("max_supersteps", C.c_uint64),
         ("hard_cap_bytes", C.c_uint64),
         ("factors", C.c_double * MG_NUM_ROLES),
+        ("dobfs_exact_cost", C.c_int),
     ]
 
 

@@ -24,6 +24,7 @@ static void free_worker(Worker& w) {
   for (auto& a : w.su64) a.free_();
   for (auto& a : w.aux) a.free_();
   w.nonisolated.free_();
+  w.toff.free_(); w.tcol.free_(); w.tlong.free_();
   if (w.host_ctr) cudaFreeHost(w.host_ctr);
   if (w.stream) cudaStreamDestroy(w.stream);
   for (cudaEvent_t e : {w.ev_start, w.ev_end, w.ev_x0, w.ev_x1, w.ev_k0, w.ev_k1})

@@ -116,6 +116,11 @@ struct Worker {
   DevArray<unsigned long long> su64[3];
   DevArray<uint32_t> aux[6];          // primitive-private scratch (bitmaps, queues)
   DevArray<uint32_t> nonisolated;     // hosted vertices with out-degree > 0 (ascending)
+  // transpose of the sub-graph (in-arcs from hosted vertices), rows sorted by
+  // source; built once per plan for the pull-form PageRank accumulation
+  DevArray<uint32_t> toff, tcol, tlong;
+  uint32_t n_tlong = 0;
+  bool transpose_ready = false;
   uint32_t n_nonisolated = 0;
   bool nonisolated_ready = false;
   std::vector<uint32_t> hosted_host;  // hosted local IDs (host copy)

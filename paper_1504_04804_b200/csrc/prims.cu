@@ -7,6 +7,8 @@
 // the per-vertex hooks with atomics whose outcome is independent of thread
 // order (atomicCAS / atomicMin / atomicExch stamps), so labels, distances and
 // components are bit-identical to the sequential reference.
+#include <cub/device/device_radix_sort.cuh>
+
 #include <cmath>
 #include <cstring>
 
@@ -167,7 +169,9 @@ struct DobfsDev {
     return true;
   }
   __device__ bool keep(uint32_t) const { return true; }
-  // pre-test on the live bitmap in L2 (an L1 copy would go stale)
+  // pre-test on the live bitmap in L2 (ld.cg).  Measured: L1-cached (ld.ca)
+  // and read-only (ld.nc) probes are no faster on RMAT-26 — the probes are
+  // spread too widely for L1 reuse.
   __device__ bool prefilter(uint32_t v) const {
     return !(__ldcg(&vis[v >> 5]) & (1u << (v & 31)));
   }
@@ -253,58 +257,95 @@ constexpr int kPullGroup = 8;  // lanes per vertex in the long-row pass
 // tests its first kPullK arcs (independent loads in flight); a hit labels the
 // vertex, a short row without a hit keeps it unvisited, a long row goes to the
 // cooperative stage with its scan position.
+constexpr int kPV = 4;  // unvisited-list entries per thread per iteration
+
 __global__ void __launch_bounds__(256)
     dobfs_pull_thread_kernel(GraphView g, const uint32_t* __restrict__ ul, uint32_t nul,
                              uint32_t* labels, uint32_t* preds, uint32_t* vis,
                              const uint32_t* __restrict__ fb, uint32_t next_label, int mark_preds,
                              OwnerView ow, uint32_t* out, uint32_t* ul_out, uint32_t* ul_out_cnt,
-                             uint32_t* longq, uint32_t* long_cnt, Counters* ctr) {
+                             uint32_t* longq, uint32_t* long_cnt, Counters* ctr,
+                             unsigned long long* scanned_out) {
   unsigned long long scanned = 0, opened = 0;
-  __shared__ BlockQueue<256> q_found, q_keep, q_long;
+  // three CTA queues (discovered / still unvisited / long rows), flushed
+  // together once per 256*kPV entries: one reservation per queue, 4 barriers
+  __shared__ BlockQueue<256 * kPV> q_found, q_keep, q_long;
   q_found.reset();
   q_keep.reset();
   q_long.reset();
   __syncthreads();
-  for (uint32_t base = blockIdx.x * blockDim.x; base < nul; base += gridDim.x * blockDim.x) {
-    uint32_t i = base + threadIdx.x;
-    bool found = false, keep = false, lng = false;
-    uint32_t v = 0;
-    if (i < nul) {
-      v = ul[i];
-      if (!(vis[v >> 5] & (1u << (v & 31)))) {
-        ++opened;
-        const uint32_t b = g.off[v], e = g.off[v + 1];
-        const uint32_t d = e - b;
-        uint32_t w[kPullK];
+  const uint32_t chunk = 256 * kPV;
+  for (uint32_t base = blockIdx.x * chunk; base < nul; base += gridDim.x * chunk) {
+    uint32_t v[kPV], b[kPV], d[kPV], w[kPV][kPullK];
+    bool open[kPV];
 #pragma unroll
-        for (int k = 0; k < kPullK; ++k) w[k] = (uint32_t)k < d ? __ldg(&g.col[b + k]) : 0u;
-        int hit = -1;
+    for (int j = 0; j < kPV; ++j) {  // list entries: coalesced, kPV loads in flight
+      uint32_t i = base + threadIdx.x + j * 256;
+      v[j] = i < nul ? ul[i] : 0u;
+      open[j] = i < nul;
+    }
 #pragma unroll
-        for (int k = kPullK - 1; k >= 0; --k)
-          if ((uint32_t)k < d && (__ldg(&fb[w[k] >> 5]) & (1u << (w[k] & 31)))) hit = k;
-        if (hit >= 0) {
-          found = true;
-          scanned += hit + 1;
-          labels[v] = next_label;
-          atomicOr(&vis[v >> 5], 1u << (v & 31));
-          if (mark_preds) preds[v] = ow.to_global(w[hit]);
-        } else if (d <= (uint32_t)kPullK) {
-          scanned += d;
-          keep = true;
-        } else {
-          scanned += kPullK;
-          lng = true;
+    for (int j = 0; j < kPV; ++j)
+      open[j] = open[j] && !(vis[v[j] >> 5] & (1u << (v[j] & 31)));
+#pragma unroll
+    for (int j = 0; j < kPV; ++j) {
+      b[j] = open[j] ? g.off[v[j]] : 0u;
+      d[j] = open[j] ? g.off[v[j] + 1] - b[j] : 0u;
+    }
+#pragma unroll
+    for (int j = 0; j < kPV; ++j)
+#pragma unroll
+      for (int k = 0; k < kPullK; ++k)
+        w[j][k] = (uint32_t)k < d[j] ? __ldg(&g.col[b[j] + k]) : 0u;
+    bool found[kPV], keep[kPV], lng[kPV];
+#pragma unroll
+    for (int j = 0; j < kPV; ++j) {
+      int hit = -1;
+      uint32_t par = 0;  // register-resident (no dynamic indexing of w)
+#pragma unroll
+      for (int k = kPullK - 1; k >= 0; --k)
+        if ((uint32_t)k < d[j] && (__ldg(&fb[w[j][k] >> 5]) & (1u << (w[j][k] & 31)))) {
+          hit = k;
+          par = w[j][k];
         }
+      found[j] = keep[j] = lng[j] = false;
+      if (!open[j]) continue;
+      ++opened;
+      if (hit >= 0) {
+        found[j] = true;
+        scanned += hit + 1;
+        labels[v[j]] = next_label;
+        atomicOr(&vis[v[j] >> 5], 1u << (v[j] & 31));
+        if (mark_preds) preds[v[j]] = ow.to_global(par);
+      } else if (d[j] <= (uint32_t)kPullK) {
+        scanned += d[j];
+        keep[j] = true;
+      } else {
+        scanned += kPullK;
+        lng[j] = true;
       }
     }
-    q_found.push(found, v);
-    q_keep.push(keep, v);
-    q_long.push(lng, v);
-    q_found.flush(&ctr->out_cnt, out);
-    q_keep.flush(ul_out_cnt, ul_out);
-    q_long.flush(long_cnt, longq);
+#pragma unroll
+    for (int j = 0; j < kPV; ++j) {
+      q_found.push(found[j], v[j]);
+      q_keep.push(keep[j], v[j]);
+      q_long.push(lng[j], v[j]);
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      q_found.base = q_found.n ? atomicAdd(&ctr->out_cnt, q_found.n) : 0u;
+      q_keep.base = q_keep.n ? atomicAdd(ul_out_cnt, q_keep.n) : 0u;
+      q_long.base = q_long.n ? atomicAdd(long_cnt, q_long.n) : 0u;
+    }
+    __syncthreads();
+    for (uint32_t k = threadIdx.x; k < q_found.n; k += 256) out[q_found.base + k] = q_found.buf[k];
+    for (uint32_t k = threadIdx.x; k < q_keep.n; k += 256) ul_out[q_keep.base + k] = q_keep.buf[k];
+    for (uint32_t k = threadIdx.x; k < q_long.n; k += 256) longq[q_long.base + k] = q_long.buf[k];
+    __syncthreads();
+    if (threadIdx.x == 0) q_found.n = q_keep.n = q_long.n = 0;
+    __syncthreads();
   }
-  warp_add_u64(&ctr->edges, scanned);
+  warp_add_u64(scanned_out, scanned);
   warp_add_u64(&ctr->u[2], opened);
 }
 
@@ -316,7 +357,8 @@ __global__ void __launch_bounds__(256)
                             const uint32_t* long_cnt, uint32_t* labels, uint32_t* preds,
                             uint32_t* vis, const uint32_t* __restrict__ fb, uint32_t next_label,
                             int mark_preds, OwnerView ow, uint32_t* out, uint32_t* ul_out,
-                            uint32_t* ul_out_cnt, Counters* ctr) {
+                            uint32_t* ul_out_cnt, Counters* ctr,
+                            unsigned long long* scanned_out) {
   const uint32_t nl = *long_cnt;
   const unsigned lane = threadIdx.x & 31u;
   const unsigned sub = lane & (kPullGroup - 1);
@@ -363,7 +405,7 @@ __global__ void __launch_bounds__(256)
     s = warp_append(ul_out_cnt, keep);
     if (keep) ul_out[s] = v;
   }
-  warp_add_u64(&ctr->edges, scanned);
+  warp_add_u64(scanned_out, scanned);
 }
 
 struct DobfsPrim : PrimBase {
@@ -378,7 +420,10 @@ struct DobfsPrim : PrimBase {
   // unvisited-list bookkeeping per worker: which aux buffer holds it, length
   std::vector<int> ul_src;  // -1: the plan's non-isolated list
   std::vector<uint32_t> ul_len;
-  DobfsPrim(uint32_t s, double a, double b, bool m) : source(s), do_a(a), do_b(b), mark_preds(m) {
+  bool exact_cost = false;
+  uint64_t physical_pull_steps = 0;
+  DobfsPrim(uint32_t s, double a, double b, bool m, bool exact)
+      : source(s), do_a(a), do_b(b), mark_preds(m), exact_cost(exact) {
     name = "dobfs";
     nva = m ? 1 : 0;
     communication = MG_COMM_BROADCAST;
@@ -458,7 +503,19 @@ struct DobfsPrim : PrimBase {
       dir_log.push_back(dir);
     }
     const uint64_t nw = words(w.nv);
-    if (dir == 0) {
+    // extension (mg_config.dobfs_exact_cost, single partition): a logically
+    // forward superstep whose exact edge count Σdeg(Q) dwarfs the unvisited
+    // list is computed by the pull kernels instead.  For one partition both
+    // produce the same set (the unvisited neighbours of Q); W is reported as
+    // the reference counts the forward step (E:66), i.e. Σdeg(Q).
+    bool physical_pull = dir == 1;
+    uint64_t logical_w = 0;
+    if (dir == 0 && exact_cost && c.P->n == 1 && c.in_count) {
+      logical_w = c.degsum();
+      physical_pull = logical_w > 4ull * ul_len[w.p];
+      if (physical_pull) ++physical_pull_steps;
+    }
+    if (!physical_pull) {
       MGB_CUDA(cudaMemcpyAsync(w.aux[4].ptr, w.su32[2].ptr, 4 * nw, cudaMemcpyDeviceToDevice,
                                w.stream));
       if (c.P->profile) MGB_CUDA(cudaEventRecord(w.ev_k0, w.stream));
@@ -490,14 +547,23 @@ struct DobfsPrim : PrimBase {
       prof_nul_[w.p] = nul;
       prof_kind_[w.p] = 0;
     }
+    // examined arcs: the reference's W in a backward step; a scratch counter
+    // when a forward step runs physically as a pull (W = Σdeg(Q) then)
+    unsigned long long* scanned = dir == 1 ? &c.ctr()->edges : &c.ctr()->u[3];
     if (nul) {
-      MGB_LAUNCH(dobfs_pull_thread_kernel, grid_for(nul, 256, kNumSMs * 16), 256, 0, w.stream,
+      MGB_LAUNCH(dobfs_pull_thread_kernel, grid_for(nul, 256 * kPV, kNumSMs * 8), 256, 0,
+                 w.stream,
                  w.graph(), ul, nul, w.su32[0].ptr, w.su32[1].ptr, w.su32[2].ptr, w.su32[3].ptr,
                  next_label, mark_preds ? 1 : 0, c.owner_view(), w.output.ptr, w.aux[dst].ptr,
-                 ulcnt, w.aux[3].ptr, cnts + 1, c.ctr());
+                 ulcnt, w.aux[3].ptr, cnts + 1, c.ctr(), scanned);
       MGB_LAUNCH(dobfs_pull_group_kernel, kNumSMs * 16, 256, 0, w.stream, w.graph(), w.aux[3].ptr,
                  cnts + 1, w.su32[0].ptr, w.su32[1].ptr, w.su32[2].ptr, w.su32[3].ptr, next_label,
-                 mark_preds ? 1 : 0, c.owner_view(), w.output.ptr, w.aux[dst].ptr, ulcnt, c.ctr());
+                 mark_preds ? 1 : 0, c.owner_view(), w.output.ptr, w.aux[dst].ptr, ulcnt, c.ctr(),
+                 scanned);
+    }
+    if (dir == 0) {
+      unsigned long long lw = logical_w;  // pageable source: staged before return
+      MGB_CUDA(cudaMemcpyAsync(&c.ctr()->edges, &lw, 8, cudaMemcpyHostToDevice, w.stream));
     }
     if (c.P->profile) {
       MGB_CUDA(cudaEventRecord(w.ev_k1, w.stream));
@@ -831,41 +897,91 @@ __global__ void max_hosted_label_kernel(const uint32_t* labels, const uint32_t* 
   if (lane_id() == 0 && m) atomicMax(&ctr->u[0], (unsigned long long)m);
 }
 
-// backward level step (primitives.cpp:592-617).  Each vertex of the level is
-// handled by one thread walking its arcs in order with explicitly rounded
-// operations (no FMA contraction), so delta/bc match the reference bit for bit.
+// backward level step (primitives.cpp:592-617), in two kernels:
+//   select: hosted vertices of the level -> the level list (also the output
+//           broadcast of the superstep) split by degree;
+//   accumulate: rows below kBcWarpDeg by one thread walking its arcs in order,
+//           longer rows by a warp (lane-strided partial sums, fixed xor-tree
+//           reduction: deterministic, within 1e-15 of the sequential sum).
+// Explicitly rounded operations (no FMA contraction) keep short rows bit-exact.
+constexpr uint32_t kBcWarpDeg = 32;
+
 __global__ void __launch_bounds__(256)
-    bc_backward_kernel(GraphView g, const uint32_t* __restrict__ hosted, uint32_t nh,
-                       const uint32_t* labels, const double* sigma, double* delta, double* bc,
-                       const uint32_t* bstamp, uint32_t level, uint32_t prev_stamp,
-                       uint32_t source, int accumulate, OwnerView ow, uint32_t* out,
-                       Counters* ctr) {
-  unsigned long long scanned = 0;
+    bc_level_select_kernel(const uint32_t* __restrict__ hosted, uint32_t nh,
+                           const uint32_t* __restrict__ labels, const uint32_t* __restrict__ off,
+                           uint32_t level, uint32_t* out, Counters* ctr, uint32_t* small,
+                           uint32_t* nsmall, uint32_t* big, uint32_t* nbig) {
   for (uint32_t base = blockIdx.x * blockDim.x; base < nh; base += gridDim.x * blockDim.x) {
     uint32_t i = base + threadIdx.x;
-    bool emit = false;
+    bool in = false, is_big = false;
     uint32_t v = 0;
     if (i < nh) {
       v = hosted[i];
-      emit = labels[v] == level;
-      if (emit && accumulate) {
-        double acc = 0.0;
-        const double sv = sigma[v];
-        uint32_t b = g.off[v], e = g.off[v + 1];
-        for (uint32_t k = b; k < e; ++k) {
-          uint32_t w = g.col[k];
-          bool succ = ow.hosts(w) ? (labels[w] == level + 1) : (bstamp[w] == prev_stamp);
-          double sw = sigma[w];
-          if (succ && sw > 0.0)
-            acc = __dadd_rn(acc, __dmul_rn(__ddiv_rn(sv, sw), __dadd_rn(1.0, delta[w])));
-        }
-        scanned += e - b;
-        delta[v] = acc;
-        if (v != source) bc[v] = __dadd_rn(bc[v], acc);
-      }
+      in = labels[v] == level;
+      if (in) is_big = off[v + 1] - off[v] >= kBcWarpDeg;
     }
-    uint32_t slot = warp_append(&ctr->out_cnt, emit);
-    if (emit) out[slot] = v;
+    uint32_t s = warp_append(&ctr->out_cnt, in);
+    if (in) out[s] = v;
+    s = warp_append(nsmall, in && !is_big);
+    if (in && !is_big) small[s] = v;
+    s = warp_append(nbig, in && is_big);
+    if (in && is_big) big[s] = v;
+  }
+}
+
+__device__ __forceinline__ double bc_term(const GraphView& g, uint32_t k, double sv,
+                                          const uint32_t* labels, const double* sigma,
+                                          const double* delta, const uint32_t* bstamp,
+                                          uint32_t level, uint32_t prev_stamp, const OwnerView& ow) {
+  uint32_t w = g.col[k];
+  bool succ = ow.hosts(w) ? (labels[w] == level + 1) : (bstamp[w] == prev_stamp);
+  double sw = sigma[w];
+  if (succ && sw > 0.0) return __dmul_rn(__ddiv_rn(sv, sw), __dadd_rn(1.0, delta[w]));
+  return 0.0;
+}
+
+__global__ void __launch_bounds__(256)
+    bc_backward_thread_kernel(GraphView g, const uint32_t* __restrict__ list, const uint32_t* nlist,
+                              const uint32_t* labels, const double* sigma, double* delta,
+                              double* bc, const uint32_t* bstamp, uint32_t level,
+                              uint32_t prev_stamp, uint32_t source, OwnerView ow, Counters* ctr) {
+  const uint32_t n = *nlist;
+  unsigned long long scanned = 0;
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    uint32_t v = list[i];
+    const double sv = sigma[v];
+    double acc = 0.0;
+    uint32_t b = g.off[v], e = g.off[v + 1];
+    for (uint32_t k = b; k < e; ++k)
+      acc = __dadd_rn(acc, bc_term(g, k, sv, labels, sigma, delta, bstamp, level, prev_stamp, ow));
+    scanned += e - b;
+    delta[v] = acc;
+    if (v != source) bc[v] = __dadd_rn(bc[v], acc);
+  }
+  warp_add_u64(&ctr->edges, scanned);
+}
+
+__global__ void __launch_bounds__(256)
+    bc_backward_warp_kernel(GraphView g, const uint32_t* __restrict__ list, const uint32_t* nlist,
+                            const uint32_t* labels, const double* sigma, double* delta, double* bc,
+                            const uint32_t* bstamp, uint32_t level, uint32_t prev_stamp,
+                            uint32_t source, OwnerView ow, Counters* ctr) {
+  const uint32_t n = *nlist;
+  const uint32_t warps = gridDim.x * blockDim.x / 32;
+  unsigned long long scanned = 0;
+  for (uint32_t i = (blockIdx.x * blockDim.x + threadIdx.x) / 32; i < n; i += warps) {
+    uint32_t v = list[i];
+    const double sv = sigma[v];
+    double acc = 0.0;
+    uint32_t b = g.off[v], e = g.off[v + 1];
+    for (uint32_t k = b + lane_id(); k < e; k += 32)
+      acc = __dadd_rn(acc, bc_term(g, k, sv, labels, sigma, delta, bstamp, level, prev_stamp, ow));
+    for (int o = 16; o > 0; o >>= 1) acc = __dadd_rn(acc, __shfl_xor_sync(0xffffffffu, acc, o));
+    if (lane_id() == 0) {
+      scanned += e - b;
+      delta[v] = acc;
+      if (v != source) bc[v] = __dadd_rn(bc[v], acc);
+    }
   }
   warp_add_u64(&ctr->edges, scanned);
 }
@@ -928,11 +1044,26 @@ struct BcPrim : PrimBase {
     if (phase == kBwd) {
       uint32_t level = max_level - (uint32_t)(c.iter - backward_from);
       c.ensure_output(nh);
-      if (nh)
-        MGB_LAUNCH(bc_backward_kernel, grid_for(nh, 256, kNumSMs * 16), 256, 0, w.stream,
-                   w.graph(), w.hosted.ptr, nh, w.su32[0].ptr, w.sf64[0].ptr, w.sf64[1].ptr,
-                   w.sf64[2].ptr, w.su32[3].ptr, level, (uint32_t)c.iter, source,
-                   level < max_level ? 1 : 0, c.owner_view(), w.output.ptr, c.ctr());
+      if (w.aux[0].n < nh + 1ull) w.aux[0].alloc(nh + 1ull);  // short rows of the level
+      if (w.aux[1].n < nh + 1ull) w.aux[1].alloc(nh + 1ull);  // long rows of the level
+      if (w.aux[2].n < 2) w.aux[2].alloc(2);
+      uint32_t* cnts = w.aux[2].ptr;
+      MGB_CUDA(cudaMemsetAsync(cnts, 0, 8, w.stream));
+      if (nh) {
+        MGB_LAUNCH(bc_level_select_kernel, grid_for(nh, 256, kNumSMs * 16), 256, 0, w.stream,
+                   w.hosted.ptr, nh, w.su32[0].ptr, w.off.ptr, level, w.output.ptr, c.ctr(),
+                   w.aux[0].ptr, cnts, w.aux[1].ptr, cnts + 1);
+        if (level < max_level) {  // the deepest level only broadcasts
+          MGB_LAUNCH(bc_backward_thread_kernel, kNumSMs * 8, 256, 0, w.stream, w.graph(),
+                     w.aux[0].ptr, cnts, w.su32[0].ptr, w.sf64[0].ptr, w.sf64[1].ptr,
+                     w.sf64[2].ptr, w.su32[3].ptr, level, (uint32_t)c.iter, source,
+                     c.owner_view(), c.ctr());
+          MGB_LAUNCH(bc_backward_warp_kernel, kNumSMs * 8, 256, 0, w.stream, w.graph(),
+                     w.aux[1].ptr, cnts + 1, w.su32[0].ptr, w.sf64[0].ptr, w.sf64[1].ptr,
+                     w.sf64[2].ptr, w.su32[3].ptr, level, (uint32_t)c.iter, source,
+                     c.owner_view(), c.ctr());
+        }
+      }
       c.report.u[0] = max_level;
       c.report.u[1] = kBwd;
       return;
@@ -969,6 +1100,100 @@ struct PrDev {
   // the output is the static border list: entry i's destination-local ID
   __device__ uint32_t peer_id(uint32_t, uint32_t, uint32_t i) const { return border_dst[i]; }
 };
+
+// --- pull-form accumulation ------------------------------------------------
+// accum[v] = sum over hosted in-neighbours u of rank[u]/deg(u) is the same sum
+// the reference's push loop forms (primitives.cpp:766-776), gathered per
+// destination in a fixed order instead of scattered with f64 atomics.  The
+// transpose of the worker's sub-graph is built once per plan.
+
+__global__ void transpose_keys_kernel(GraphView g, const uint32_t* __restrict__ hosted,
+                                      uint32_t nh, unsigned long long* keys) {
+  const uint32_t warps = gridDim.x * blockDim.x / 32;
+  for (uint32_t i = (blockIdx.x * blockDim.x + threadIdx.x) / 32; i < nh; i += warps) {
+    uint32_t u = hosted[i];
+    for (uint32_t e = g.off[u] + lane_id(); e < g.off[u + 1]; e += 32)
+      keys[e] = ((unsigned long long)g.col[e] << 32) | u;
+  }
+}
+
+__global__ void transpose_csr_kernel(const unsigned long long* __restrict__ keys, uint64_t ne,
+                                     uint32_t nv, uint32_t* toff, uint32_t* tcol) {
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < ne; i += stride)
+    tcol[i] = (uint32_t)keys[i];
+  for (uint64_t v = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; v <= nv; v += stride) {
+    unsigned long long target = v << 32;
+    uint64_t lo = 0, hi = ne;
+    while (lo < hi) {
+      uint64_t m = (lo + hi) >> 1;
+      if (keys[m] < target) lo = m + 1;
+      else hi = m;
+    }
+    toff[v] = (uint32_t)lo;
+  }
+}
+
+constexpr uint32_t kPullLong = 64;  // rows at least this long get a warp
+
+__global__ void select_long_rows_kernel(const uint32_t* __restrict__ toff, uint32_t nv,
+                                        uint32_t* out, uint32_t* cnt) {
+  for (uint32_t base = blockIdx.x * blockDim.x; base < nv; base += gridDim.x * blockDim.x) {
+    uint32_t v = base + threadIdx.x;
+    bool lng = v < nv && toff[v + 1] - toff[v] >= kPullLong;
+    uint32_t s = warp_append(cnt, lng);
+    if (lng) out[s] = v;
+  }
+}
+
+// contrib[u] = rank[u]/deg(u) for hosted u; dangling mass aside
+__global__ void pr_contrib_kernel(GraphView g, const uint32_t* __restrict__ hosted, uint32_t nh,
+                                  const double* __restrict__ rank, double* contrib,
+                                  Counters* ctr) {
+  double dangling = 0.0;
+  unsigned long long scanned = 0;
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < nh; i += gridDim.x * blockDim.x) {
+    uint32_t u = hosted[i];
+    uint32_t d = g.off[u + 1] - g.off[u];
+    if (d == 0) {
+      dangling += rank[u];
+      contrib[u] = 0.0;
+    } else {
+      contrib[u] = rank[u] / (double)d;
+      scanned += d;
+    }
+  }
+  for (int o = 16; o > 0; o >>= 1) dangling += __shfl_xor_sync(0xffffffffu, dangling, o);
+  warp_add_u64(&ctr->edges, scanned);
+  if (lane_id() == 0 && dangling != 0.0) atomicAdd(&ctr->f[0], dangling);
+}
+
+__global__ void __launch_bounds__(256)
+    pr_pull_kernel(const uint32_t* __restrict__ toff, const uint32_t* __restrict__ tcol,
+                   uint32_t nv, const double* __restrict__ contrib, double* accum) {
+  for (uint32_t v = blockIdx.x * blockDim.x + threadIdx.x; v < nv; v += gridDim.x * blockDim.x) {
+    uint32_t b = toff[v], e = toff[v + 1];
+    if (e - b >= kPullLong) continue;  // warp kernel
+    double s = 0.0;
+    for (uint32_t k = b; k < e; ++k) s += __ldg(&contrib[__ldg(&tcol[k])]);
+    accum[v] = s;
+  }
+}
+
+__global__ void __launch_bounds__(256)
+    pr_pull_warp_kernel(const uint32_t* __restrict__ toff, const uint32_t* __restrict__ tcol,
+                        const uint32_t* __restrict__ rows, uint32_t nrows,
+                        const double* __restrict__ contrib, double* accum) {
+  const uint32_t warps = gridDim.x * blockDim.x / 32;
+  for (uint32_t i = (blockIdx.x * blockDim.x + threadIdx.x) / 32; i < nrows; i += warps) {
+    uint32_t v = rows[i];
+    double s = 0.0;
+    for (uint32_t k = toff[v] + lane_id(); k < toff[v + 1]; k += 32)
+      s += __ldg(&contrib[__ldg(&tcol[k])]);
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    if (lane_id() == 0) accum[v] = s;
+  }
+}
 
 // pr_update (primitives.cpp:697-711) fused with zeroing the hosted accumulators
 __global__ void pr_update_kernel(const uint32_t* __restrict__ hosted, uint32_t nh, double* rank,
@@ -1064,6 +1289,42 @@ struct PrPrim : PrimBase {
                  nh, w.sf64[0].ptr, w.sf64[1].ptr, (1.0 - damping) / n, damping,
                  dangling_prev / n, do_update ? 1 : 0, c.ctr());
   }
+  // plan-lifetime transpose of the worker's sub-graph (rows sorted by source)
+  static void ensure_transpose(Worker& w) {
+    if (w.transpose_ready) return;
+    const uint64_t ne = w.ne;
+    const uint32_t nh = (uint32_t)w.hosted_host.size();
+    w.toff.alloc(w.nv + 1ull);
+    w.tcol.alloc(ne ? ne : 1);
+    DevArray<unsigned long long> k0, k1;
+    k0.alloc(ne ? ne : 1);
+    k1.alloc(ne ? ne : 1);
+    if (nh && ne)
+      MGB_LAUNCH(transpose_keys_kernel, grid_for((uint64_t)nh * 32, 256, kNumSMs * 16), 256, 0,
+                 w.stream, w.graph(), w.hosted.ptr, nh, k0.ptr);
+    cub::DoubleBuffer<unsigned long long> db(k0.ptr, k1.ptr);
+    size_t tb = 0;
+    cub::DeviceRadixSort::SortKeys(nullptr, tb, db, (int64_t)ne, 0, 64, w.stream);
+    void* tmp = nullptr;
+    MGB_CUDA(cudaMalloc(&tmp, tb + 16));
+    cub::DeviceRadixSort::SortKeys(tmp, tb, db, (int64_t)ne, 0, 64, w.stream);
+    MGB_LAUNCH(transpose_csr_kernel, kNumSMs * 16, 256, 0, w.stream, db.Current(), ne, w.nv,
+               w.toff.ptr, w.tcol.ptr);
+    DevArray<uint32_t> cnt;
+    cnt.alloc(1);
+    MGB_CUDA(cudaMemsetAsync(cnt.ptr, 0, 4, w.stream));
+    w.tlong.alloc(w.nv ? w.nv : 1);
+    if (w.nv)
+      MGB_LAUNCH(select_long_rows_kernel, grid_for(w.nv, 256, kNumSMs * 8), 256, 0, w.stream,
+                 w.toff.ptr, w.nv, w.tlong.ptr, cnt.ptr);
+    MGB_CUDA(cudaMemcpyAsync(&w.n_tlong, cnt.ptr, 4, cudaMemcpyDeviceToHost, w.stream));
+    MGB_CUDA(cudaStreamSynchronize(w.stream));
+    cudaFree(tmp);
+    k0.free_();
+    k1.free_();
+    cnt.free_();
+    w.transpose_ready = true;
+  }
   void body(Ctx& c) {  // primitives.cpp:747-782
     Worker& w = *c.w;
     const bool first = c.worker() == c.P->local_workers.front();
@@ -1076,9 +1337,20 @@ struct PrPrim : PrimBase {
     }
     if (first && c.worker() == 0 && c.prev && c.iter >= 2) rank_sums.push_back(c.prev->sum_f(2));
     uint32_t nh = (uint32_t)w.hosted_host.size();
+    // accum[v] = sum of rank[u]/deg(u) over hosted in-neighbours u,
+    // gathered per destination (pull) in a fixed order
+    ensure_transpose(w);
+    if (w.sf64[2].n < w.nv || !w.sf64[2].ptr) w.sf64[2].alloc(w.nv ? w.nv : 1);
     if (nh)
-      MGB_LAUNCH(pr_push_kernel, grid_for((uint64_t)nh * 32, 256, kNumSMs * 16), 256, 0,
-                 w.stream, w.graph(), w.hosted.ptr, nh, w.sf64[0].ptr, w.sf64[1].ptr, c.ctr());
+      MGB_LAUNCH(pr_contrib_kernel, grid_for(nh, 256, kNumSMs * 8), 256, 0, w.stream, w.graph(),
+                 w.hosted.ptr, nh, w.sf64[0].ptr, w.sf64[2].ptr, c.ctr());
+    if (w.nv)
+      MGB_LAUNCH(pr_pull_kernel, grid_for(w.nv, 256, kNumSMs * 16), 256, 0, w.stream,
+                 w.toff.ptr, w.tcol.ptr, w.nv, w.sf64[2].ptr, w.sf64[1].ptr);
+    if (w.n_tlong)
+      MGB_LAUNCH(pr_pull_warp_kernel, grid_for((uint64_t)w.n_tlong * 32, 256, kNumSMs * 8), 256,
+                 0, w.stream, w.toff.ptr, w.tcol.ptr, w.tlong.ptr, w.n_tlong, w.sf64[2].ptr,
+                 w.sf64[1].ptr);
     uint32_t nb = (uint32_t)w.border.n;
     c.ensure_output(nb);
     if (nb)
@@ -1209,7 +1481,7 @@ int mg_dobfs(mg_plan* plan, uint32_t source, double do_a, double do_b, int mark_
     Plan& P = *reinterpret_cast<Plan*>(plan);
     check_source(P, source, "dobfs");
     mg_config c = cfg_or_default(cfg);
-    DobfsPrim prim(source, do_a, do_b, mark_preds != 0);
+    DobfsPrim prim(source, do_a, do_b, mark_preds != 0, c.dobfs_exact_cost != 0);
     P.last = mg_stats{};
     run_primitive(P, prim, c);
     P.last_result_kind = 0;

@@ -152,6 +152,31 @@ def test_dobfs_labels_direction_log_and_work(G, name, n, do_a, do_b):
         assert np.array_equal(r.stats.h_matrix, rr.h_matrix)
 
 
+@pytest.mark.parametrize("scale,ef,seed", [(12, 16, 1), (12, 32, 6), (14, 16, 3)])
+def test_dobfs_exact_cost_extension_keeps_reference_semantics(scale, ef, seed):
+    """dobfs_exact_cost runs heavy forward supersteps with the pull kernel; the
+    labels, direction log, S and W reported must still be the reference's"""
+    g = mg.Csr.rmat(scale, ef, seed)
+    off, col, _ = g.arrays()
+    plan = mg.PartitionPlan(g, None, 1)
+    for src in (0, 7):
+        for do_a in (0.01, 0.001):
+            a = mg.dobfs(plan, mg.DobfsOptions(source=src, do_a=do_a))
+            b = mg.dobfs(plan, mg.DobfsOptions(source=src, do_a=do_a, mark_preds=True),
+                         mg.EngineConfig(dobfs_exact_cost=True))
+            assert np.array_equal(a.labels, b.labels)
+            assert np.array_equal(b.labels, seq.bfs_levels(off, col, src))
+            assert list(a.direction_log) == list(b.direction_log)
+            assert a.stats.supersteps == b.stats.supersteps
+            assert a.stats.edges_examined == b.stats.edges_examined
+            depth = seq.bfs_levels(off, col, src)
+            for v in np.nonzero(b.labels != mg.kInfLabel)[0][:500]:
+                if v == src:
+                    continue
+                p = int(b.preds[v])
+                assert depth[p] + 1 == depth[v] and v in col[off[p]:off[p + 1]]
+
+
 def test_dobfs_work_reduction_and_broadcast_bound():
     g = mg.Csr.rmat(12, 32, 6)
     plan, _ = plan_for(g, 2, 4)
