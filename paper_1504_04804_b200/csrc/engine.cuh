@@ -209,6 +209,7 @@ struct Ctx {
   uint64_t iter = 0;
   const GlobalView* prev = nullptr;
   bool fused = false;
+  bool want_deg = true;     // exact advance bounds tracked (policy != max)
   uint32_t in_count = 0;    // input frontier length (host-known)
   uint64_t in_degsum = 0;   // sum of its out-degrees (host-known)
   WorkerReport report;      // host-side f/u fields set by hooks
@@ -324,6 +325,18 @@ void build_send_tables(Plan& P);
 void prepare_worker(Plan& P, Worker& w, const mg_config& cfg);
 void collect_buffer_stats(Plan& P);
 
+// the primitive's device functor set: one type (dev()), or a choice of two
+// made per run (SSSP's u32 / u64 distances: dev32() / dev64())
+template <class Prim, class Fn>
+auto with_dev(Prim& prim, Ctx& c, Fn&& fn) -> decltype(prim.dev(c), void()) {
+  fn(prim.dev(c));
+}
+template <class Prim, class Fn>
+auto with_dev(Prim& prim, Ctx& c, Fn&& fn) -> decltype(prim.dev32(c), void()) {
+  if (prim.narrow) fn(prim.dev32(c));
+  else fn(prim.dev64(c));
+}
+
 // ---------------------------------------------------------------------------
 // the enactor
 
@@ -373,6 +386,7 @@ void run_primitive(Plan& P, Prim& prim, const mg_config& cfg) {
     ctx[p].w = &w;
     ctx[p].run = &rs;
     ctx[p].fused = fused;
+    ctx[p].want_deg = want_deg;
   }
   if (P.shm) fabric_sync(P);  // collective: map peers' (possibly regrown) arenas
   build_send_tables(P);
@@ -398,7 +412,9 @@ void run_primitive(Plan& P, Prim& prim, const mg_config& cfg) {
     DeviceGuard dg(w.dev);
     MGB_CUDA(cudaEventRecord(w.ev_start, w.stream));
     MGB_CUDA(cudaMemsetAsync(w.ctr.ptr, 0, sizeof(Counters), w.stream));
-    MGB_CUDA(cudaMemsetAsync(w.merge_stamp.ptr, 0, sizeof(uint32_t) * w.nv, w.stream));
+    // the merge stamp is only read by the merge kernel (n > 1)
+    if (n > 1)
+      MGB_CUDA(cudaMemsetAsync(w.merge_stamp.ptr, 0, sizeof(uint32_t) * w.nv, w.stream));
     prim.init(ctx[p]);
     // advance bound of superstep 0
     if (rs.next_count[p])
@@ -454,12 +470,13 @@ void run_primitive(Plan& P, Prim& prim, const mg_config& cfg) {
           cfg.drop_dst < 64)
         drop = 1ull << cfg.drop_dst;
       if (n > 1) MGB_CUDA(cudaEventRecord(w.ev_x0, w.stream));
-      auto dev = prim.dev(c);
-      MGB_LAUNCH(split_pack_kernel<decltype(dev)>, grid_for(w.output.cap, 256, kNumSMs * 8),
-                 256, 0, w.stream, dev, c.owner_view(), w.graph(), w.output.ptr, w.ctr.ptr,
-                 w.next_input.ptr, w.send_table.ptr + parity * n, n,
-                 step_comm[p] == MG_COMM_BROADCAST ? 1 : 0, drop, prim.nva, prim.nvv,
-                 want_deg ? 1 : 0);
+      with_dev(prim, c, [&](auto dev) {
+        MGB_LAUNCH(split_pack_kernel<decltype(dev)>, grid_for(w.output.cap, 256, kNumSMs * 8),
+                   256, 0, w.stream, dev, c.owner_view(), w.graph(), w.output.ptr, w.ctr.ptr,
+                   w.next_input.ptr, w.send_table.ptr + parity * n, n,
+                   step_comm[p] == MG_COMM_BROADCAST ? 1 : 0, drop, prim.nva, prim.nvv,
+                   want_deg ? 1 : 0);
+      });
       if (n > 1) {
         MGB_LAUNCH(publish_kernel, 1, 64, 0, w.stream, w.ctr.ptr, w.send_cnt_ptr.ptr + parity * n,
                    n, p);
@@ -481,15 +498,16 @@ void run_primitive(Plan& P, Prim& prim, const mg_config& cfg) {
       if (n > 1) {
         for (uint32_t s : P.local_workers)
           if (s != p) MGB_CUDA(cudaStreamWaitEvent(w.stream, rs.packed[s], 0));
-        auto dev = prim.dev(c);
         uint64_t maxcap = 0;
         for (uint32_t s = 0; s < n; ++s)
           if (s != p && w.slot_cap[s] > maxcap) maxcap = w.slot_cap[s];
         dim3 grid(grid_for(maxcap, 256, kNumSMs * 2), n);
-        MGB_LAUNCH(merge_kernel<decltype(dev)>, grid, 256, 0, w.stream, dev, w.recv_table.ptr + parity * n,
-                   w.inbox_cnt.ptr + parity * kMaxWorkers, p, (uint32_t)(iter + 1),
-                   (uint32_t)iter, w.merge_stamp.ptr, w.next_input.ptr, w.ctr.ptr, w.graph(),
-                   prim.nva, prim.nvv, 1, want_deg ? 1 : 0);
+        with_dev(prim, c, [&](auto dev) {
+          MGB_LAUNCH(merge_kernel<decltype(dev)>, grid, 256, 0, w.stream, dev,
+                     w.recv_table.ptr + parity * n, w.inbox_cnt.ptr + parity * kMaxWorkers, p,
+                     (uint32_t)(iter + 1), (uint32_t)iter, w.merge_stamp.ptr, w.next_input.ptr,
+                     w.ctr.ptr, w.graph(), prim.nva, prim.nvv, 1, want_deg ? 1 : 0);
+        });
       }
       prim.after_merge(c);
       MGB_CUDA(cudaMemcpyAsync(w.host_ctr, w.ctr.ptr, sizeof(Counters), cudaMemcpyDeviceToHost,

@@ -173,6 +173,7 @@ Plan* plan_from_device_csr(uint32_t nv, uint64_t ne, DevArray<uint32_t>& goff,
     P->nv = nv;
     P->ne = ne;
     P->weighted = gw.ptr != nullptr;
+    if (P->weighted) P->max_weight = device_max_u32(gw.ptr, ne);
     P->owner_host = owner;
     P->devices.resize(n);
     for (uint32_t p = 0; p < n; ++p) {

@@ -154,48 +154,49 @@ __global__ void __launch_bounds__(kExpBlock)
     const uint32_t lo = tile_lo[tile];
     const uint32_t hi = tile + 1 < ntiles ? tile_lo[tile + 1] : n_in - 1;
     const uint32_t R = hi - lo + 1;
-    const bool staged = R <= (uint32_t)kStage;
-    __syncthreads();  // previous tile done with the stage
-    if (staged) {
-      for (uint32_t j = threadIdx.x; j < R; j += kExpBlock) {
-        s_pref[j] = lb_pref(prefix, block_off, lo + j);
-        s_row[j] = rowstart[lo + j];
-        s_src[j] = in[lo + j];
-      }
-      if (threadIdx.x == 0)
-        s_pref[R] = (hi + 1 < n_in) ? lb_pref(prefix, block_off, hi + 1) : total;
+    // The tile's vertex range is staged in chunks of at most kStage vertices, so
+    // a tile of many low-degree rows (R up to kTile) still locates every arc in
+    // shared memory; hub-heavy tiles need one chunk.
+    for (uint32_t c0 = 0; c0 < R; c0 += kStage) {
+    const uint32_t cR = R - c0 < (uint32_t)kStage ? R - c0 : (uint32_t)kStage;
+    const uint32_t clo = lo + c0;
+    __syncthreads();  // previous chunk done with the stage
+    for (uint32_t j = threadIdx.x; j < cR; j += kExpBlock) {
+      s_pref[j] = lb_pref(prefix, block_off, clo + j);
+      s_row[j] = rowstart[clo + j];
+      s_src[j] = in[clo + j];
     }
+    if (threadIdx.x == 0)
+      s_pref[cR] = (clo + cR < n_in) ? lb_pref(prefix, block_off, clo + cR) : total;
     __syncthreads();
-    auto pref = [&](uint32_t j) -> unsigned long long {  // j relative to lo
-      return staged ? s_pref[j]
-                    : ((lo + j < n_in) ? lb_pref(prefix, block_off, lo + j) : total);
-    };
-    // warp w owns arcs [t0 + w*kWarpArcs, +kWarpArcs), processed in kBatches
-    // batches of 32*kItems; lane l takes arcs l, l+32, ... of each batch
-    const unsigned long long w0 = t0 + (unsigned long long)warp * kWarpArcs + lane;
-    uint32_t j = 0;
-    if (w0 < t1) {
-      uint32_t a = 0, b = R - 1;  // last j with pref(j) <= w0
-      while (a < b) {
-        uint32_t m = (a + b + 1) >> 1;
-        if (pref(m) <= w0) a = m;
-        else b = m - 1;
+    // arcs of this chunk inside the tile
+    const unsigned long long a0 = s_pref[0] > t0 ? s_pref[0] : t0;
+    const unsigned long long a1 = s_pref[cR] < t1 ? s_pref[cR] : t1;
+    // batches of 32*kItems arcs round-robin over the warps; lane l takes arcs
+    // l, l+32, ... of its batch (coalesced col_indices)
+    for (unsigned long long e0 = a0 + (unsigned long long)warp * 32 * kItems + lane; e0 - lane < a1;
+         e0 += (unsigned long long)(kExpBlock / 32) * 32 * kItems) {
+      uint32_t j;
+      {
+        uint32_t a = 0, b = cR - 1;  // last j with s_pref[j] <= e0 (smem search)
+        const unsigned long long key = e0 < a1 ? e0 : a1 - 1;
+        while (a < b) {
+          uint32_t m = (a + b + 1) >> 1;
+          if (s_pref[m] <= key) a = m;
+          else b = m - 1;
+        }
+        j = a;
       }
-      j = a;
-    }
-    unsigned long long jnext = w0 < t1 ? pref(j + 1) : 0;
-    for (int batch = 0; batch < kBatches; ++batch) {
-      const unsigned long long e0 = w0 + (unsigned long long)batch * 32 * kItems;
+      unsigned long long jnext = s_pref[j + 1];
       uint32_t eid[kItems], src[kItems], nb[kItems];
 #pragma unroll
-      for (int k = 0; k < kItems; ++k) {  // locate
+      for (int k = 0; k < kItems; ++k) {  // locate: a short walk in shared memory
         const unsigned long long e = e0 + 32ull * k;
         eid[k] = 0xFFFFFFFFu;
-        if (e < t1) {
-          while (e >= jnext) jnext = pref(++j + 1);
-          const unsigned long long base = pref(j);
-          eid[k] = (staged ? s_row[j] : rowstart[lo + j]) + (uint32_t)(e - base);
-          src[k] = staged ? s_src[j] : in[lo + j];
+        if (e < a1) {
+          while (e >= jnext) jnext = s_pref[++j + 1];
+          eid[k] = s_row[j] + (uint32_t)(e - s_pref[j]);
+          src[k] = s_src[j];
         }
       }
 #pragma unroll
@@ -214,6 +215,7 @@ __global__ void __launch_bounds__(kExpBlock)
         q.push(a, nb[k]);
       }
       q.flush(out_cnt, out, false);
+    }
     }
   }
   q.flush(out_cnt, out, true);

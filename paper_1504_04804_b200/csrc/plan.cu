@@ -7,6 +7,25 @@
 
 namespace mgb {
 
+__global__ void max_u32_kernel(const uint32_t* __restrict__ a, uint64_t n, uint32_t* out) {
+  uint32_t m = 0;
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
+       i += (uint64_t)gridDim.x * blockDim.x)
+    m = a[i] > m ? a[i] : m;
+  m = __reduce_max_sync(0xffffffffu, m);
+  if ((threadIdx.x & 31) == 0 && m) atomicMax(out, m);
+}
+
+uint32_t device_max_u32(const uint32_t* a, uint64_t n) {
+  DevArray<uint32_t> o;
+  o.alloc(1);
+  MGB_CUDA(cudaMemset(o.ptr, 0, 4));
+  if (n) MGB_LAUNCH(max_u32_kernel, kNumSMs * 8, 256, 0, 0, a, n, o.ptr);
+  uint32_t h = 0;
+  MGB_CUDA(cudaMemcpy(&h, o.ptr, 4, cudaMemcpyDeviceToHost));
+  return h;
+}
+
 std::atomic<uint64_t> g_launches{0};
 
 Worker& worker(Plan& P, uint32_t p) { return *P.workers[p]; }
@@ -24,6 +43,8 @@ static void free_worker(Worker& w) {
   for (auto& a : w.su64) a.free_();
   for (auto& a : w.aux) a.free_();
   w.nonisolated.free_();
+  w.pull_rec.free_();
+  for (auto& a : w.ul_buf) a.free_();
   w.toff.free_(); w.tcol.free_(); w.tlong.free_();
   if (w.host_ctr) cudaFreeHost(w.host_ctr);
   if (w.stream) cudaStreamDestroy(w.stream);
@@ -128,6 +149,8 @@ Plan* plan_from_host(const HostPlan& H, const int* devices, std::shared_ptr<Host
     P->nv = H.nv;
     P->ne = H.ne;
     P->weighted = g ? g->weighted() : false;
+    if (P->weighted)
+      for (uint32_t x : g->w) P->max_weight = x > P->max_weight ? x : P->max_weight;
     P->owner_host = H.owner;
     P->host_graph = g;
     P->devices.resize(H.n);
@@ -251,18 +274,26 @@ void build_send_tables(Plan& P) {
         table[par * n + q] = d.slots[par][p];
         cnt[par * n + q] = d.inbox_cnt.ptr + par * kMaxWorkers + p;
       }
+    std::vector<SlotView> recv(2 * n);
+    for (int par = 0; par < 2; ++par)
+      for (uint32_t s = 0; s < n; ++s) recv[par * n + s] = w.slots[par][s];
+    // the tables change only when an arena is (re)mapped: skip the three
+    // synchronous uploads when the device copies are already current
+    std::vector<uint8_t> sig(sizeof(SlotView) * 4 * n + sizeof(uint32_t*) * 2 * n);
+    std::memcpy(sig.data(), table.data(), sizeof(SlotView) * 2 * n);
+    std::memcpy(sig.data() + sizeof(SlotView) * 2 * n, recv.data(), sizeof(SlotView) * 2 * n);
+    std::memcpy(sig.data() + sizeof(SlotView) * 4 * n, cnt.data(), sizeof(uint32_t*) * 2 * n);
+    if (sig == w.table_sig && w.send_table.ptr) continue;
     if (!w.send_table.ptr || w.send_table.n != 2 * n) w.send_table.alloc(2 * n);
     if (!w.send_cnt_ptr.ptr || w.send_cnt_ptr.n != 2 * n) w.send_cnt_ptr.alloc(2 * n);
     MGB_CUDA(cudaMemcpy(w.send_table.ptr, table.data(), sizeof(SlotView) * 2 * n,
                         cudaMemcpyHostToDevice));
     MGB_CUDA(cudaMemcpy(w.send_cnt_ptr.ptr, cnt.data(), sizeof(uint32_t*) * 2 * n,
                         cudaMemcpyHostToDevice));
-    std::vector<SlotView> recv(2 * n);
-    for (int par = 0; par < 2; ++par)
-      for (uint32_t s = 0; s < n; ++s) recv[par * n + s] = w.slots[par][s];
     if (!w.recv_table.ptr || w.recv_table.n != 2 * n) w.recv_table.alloc(2 * n);
     MGB_CUDA(cudaMemcpy(w.recv_table.ptr, recv.data(), sizeof(SlotView) * 2 * n,
                         cudaMemcpyHostToDevice));
+    w.table_sig = std::move(sig);
   }
 }
 

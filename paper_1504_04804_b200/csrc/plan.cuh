@@ -108,6 +108,7 @@ struct Worker {
   DevArray<SlotView> send_table;   // [2][n]
   DevArray<uint32_t*> send_cnt_ptr;  // [2][n] -> &inbox_cnt[parity][p] at peer
   DevArray<SlotView> recv_table;     // [2][n] device copy of `slots` (merge kernel)
+  std::vector<uint8_t> table_sig;    // host image of the three tables last uploaded
 
   // primitive state arrays (|V_i| entries each), reused across runs; results
   // of the last run stay here until the next run (mg_plan_fetch)
@@ -116,6 +117,8 @@ struct Worker {
   DevArray<unsigned long long> su64[3];
   DevArray<uint32_t> aux[6];          // primitive-private scratch (bitmaps, queues)
   DevArray<uint32_t> nonisolated;     // hosted vertices with out-degree > 0 (ascending)
+  DevArray<uint4> pull_rec;           // DOBFS pull records {v, deg, arc0, arc1} per nonisolated
+  DevArray<uint32_t> ul_buf[3];       // DOBFS unvisited lists (ping-pong) + long-row queue
   // transpose of the sub-graph (in-arcs from hosted vertices), rows sorted by
   // source; built once per plan for the pull-form PageRank accumulation
   DevArray<uint32_t> toff, tcol, tlong;
@@ -139,6 +142,7 @@ struct Plan {
   uint32_t nv = 0;
   uint64_t ne = 0;
   bool weighted = false;
+  uint32_t max_weight = 0;  // largest edge weight (SSSP picks its distance width from it)
   std::vector<int> devices;
   std::vector<std::unique_ptr<Worker>> workers;  // only local workers are populated
   std::vector<uint32_t> local_workers;           // partition ids driven by this process
@@ -183,6 +187,7 @@ struct WorkerReport;
 void fabric_sync(Plan& P);
 
 Worker& worker(Plan& P, uint32_t p);
+uint32_t device_max_u32(const uint32_t* a, uint64_t n);
 void init_worker_runtime(Worker& w);
 void plan_free(Plan* P);
 

@@ -250,162 +250,237 @@ __global__ void select_nonisolated_kernel(const uint32_t* __restrict__ hosted, u
   }
 }
 
-constexpr int kPullK = 4;      // arcs each thread tests before handing off
+// Pull records (plan lifetime, one per non-isolated hosted vertex, ascending):
+// {v, deg(v), col[off[v]], col[off[v]+1]} — 16 bytes, the first two arcs of the
+// row stored next to the vertex (0xFFFFFFFF past the end of a short row).  In
+// R-MAT rows the lowest-ID neighbours (hubs) come first, so most unvisited
+// vertices find a frontier parent within the first two arcs; the pull step
+// then reads one coalesced 16-byte record per vertex instead of an offset pair
+// plus a random 32-byte col_indices sector.  Unvisited lists hold record
+// positions; the first pull of a run walks all records without a list.
+constexpr int kPullK = 2;      // arcs held in the record
 constexpr int kPullGroup = 8;  // lanes per vertex in the long-row pass
+constexpr int kPV = 8;         // records per thread per iteration (loads in flight)
 
-// pull step, stage 1 (primitives.cpp:230-251): one thread per unvisited vertex
-// tests its first kPullK arcs (independent loads in flight); a hit labels the
-// vertex, a short row without a hit keeps it unvisited, a long row goes to the
-// cooperative stage with its scan position.
-constexpr int kPV = 4;  // unvisited-list entries per thread per iteration
+__global__ void pull_records_kernel(GraphView g, const uint32_t* __restrict__ ni, uint32_t n,
+                                    uint4* rec) {
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    uint32_t v = ni[i];
+    uint32_t b = g.off[v], d = g.off[v + 1] - b;
+    rec[i] = make_uint4(v, d, d > 0 ? g.col[b] : kInfLabel, d > 1 ? g.col[b + 1] : kInfLabel);
+  }
+}
 
+__device__ __forceinline__ bool bit_set(const uint32_t* bits, uint32_t v) {
+  return (__ldg(&bits[v >> 5]) >> (v & 31)) & 1u;
+}
+
+// pull step, stage 1 (primitives.cpp:230-251): one thread per unvisited record
+// tests the record's two arcs against the frontier bitmap; a hit labels the
+// vertex, a short row without a hit stays unvisited, a longer row goes to the
+// cooperative stage.  CTA queues (one global atomic per queue per 256*kPV
+// records).  With emit_found == 0 (single partition) the discovered vertices
+// are only counted: the next superstep rebuilds the frontier from the visited
+// bitmap when it needs a list (a pull never does).
 __global__ void __launch_bounds__(256)
-    dobfs_pull_thread_kernel(GraphView g, const uint32_t* __restrict__ ul, uint32_t nul,
-                             uint32_t* labels, uint32_t* preds, uint32_t* vis,
+    dobfs_pull_thread_kernel(const uint4* __restrict__ rec, const uint32_t* __restrict__ ul,
+                             uint32_t nul, uint32_t* labels, uint32_t* preds, uint32_t* vis,
                              const uint32_t* __restrict__ fb, uint32_t next_label, int mark_preds,
-                             OwnerView ow, uint32_t* out, uint32_t* ul_out, uint32_t* ul_out_cnt,
-                             uint32_t* longq, uint32_t* long_cnt, Counters* ctr,
-                             unsigned long long* scanned_out) {
+                             OwnerView ow, int emit_found, uint32_t* out, uint32_t* ul_out,
+                             uint32_t* ul_out_cnt, uint32_t* longq, uint32_t* long_cnt,
+                             Counters* ctr, unsigned long long* scanned_out) {
   unsigned long long scanned = 0, opened = 0;
-  // three CTA queues (discovered / still unvisited / long rows), flushed
-  // together once per 256*kPV entries: one reservation per queue, 4 barriers
+  uint32_t found_n = 0;
   __shared__ BlockQueue<256 * kPV> q_found, q_keep, q_long;
+  __shared__ uint32_t s_found;
   q_found.reset();
   q_keep.reset();
   q_long.reset();
+  if (threadIdx.x == 0) s_found = 0;
   __syncthreads();
   const uint32_t chunk = 256 * kPV;
   for (uint32_t base = blockIdx.x * chunk; base < nul; base += gridDim.x * chunk) {
-    uint32_t v[kPV], b[kPV], d[kPV], w[kPV][kPullK];
-    bool open[kPV];
-#pragma unroll
-    for (int j = 0; j < kPV; ++j) {  // list entries: coalesced, kPV loads in flight
-      uint32_t i = base + threadIdx.x + j * 256;
-      v[j] = i < nul ? ul[i] : 0u;
-      open[j] = i < nul;
-    }
-#pragma unroll
-    for (int j = 0; j < kPV; ++j)
-      open[j] = open[j] && !(vis[v[j] >> 5] & (1u << (v[j] & 31)));
+    uint32_t pos[kPV];
+    uint4 r[kPV];
 #pragma unroll
     for (int j = 0; j < kPV; ++j) {
-      b[j] = open[j] ? g.off[v[j]] : 0u;
-      d[j] = open[j] ? g.off[v[j] + 1] - b[j] : 0u;
+      uint32_t i = base + threadIdx.x + j * 256;
+      pos[j] = i < nul ? (ul ? __ldg(&ul[i]) : i) : kInfLabel;
     }
 #pragma unroll
-    for (int j = 0; j < kPV; ++j)
+    for (int j = 0; j < kPV; ++j)  // coalesced 16-byte records, kPV in flight
+      r[j] = pos[j] != kInfLabel ? __ldg(&rec[pos[j]]) : make_uint4(0, 0, kInfLabel, kInfLabel);
+    bool open[kPV], h0[kPV], h1[kPV];
 #pragma unroll
-      for (int k = 0; k < kPullK; ++k)
-        w[j][k] = (uint32_t)k < d[j] ? __ldg(&g.col[b[j] + k]) : 0u;
+    for (int j = 0; j < kPV; ++j) {
+      open[j] = pos[j] != kInfLabel && !((__ldcg(&vis[r[j].x >> 5]) >> (r[j].x & 31)) & 1u);
+      h0[j] = open[j] && bit_set(fb, r[j].z);
+      h1[j] = open[j] && r[j].y > 1 && bit_set(fb, r[j].w);
+    }
     bool found[kPV], keep[kPV], lng[kPV];
 #pragma unroll
     for (int j = 0; j < kPV; ++j) {
-      int hit = -1;
-      uint32_t par = 0;  // register-resident (no dynamic indexing of w)
-#pragma unroll
-      for (int k = kPullK - 1; k >= 0; --k)
-        if ((uint32_t)k < d[j] && (__ldg(&fb[w[j][k] >> 5]) & (1u << (w[j][k] & 31)))) {
-          hit = k;
-          par = w[j][k];
-        }
-      found[j] = keep[j] = lng[j] = false;
+      const uint32_t v = r[j].x, d = r[j].y;
+      found[j] = open[j] && (h0[j] || h1[j]);
+      keep[j] = open[j] && !found[j] && d <= (uint32_t)kPullK;
+      lng[j] = open[j] && !found[j] && d > (uint32_t)kPullK;
       if (!open[j]) continue;
       ++opened;
-      if (hit >= 0) {
-        found[j] = true;
-        scanned += hit + 1;
-        labels[v[j]] = next_label;
-        atomicOr(&vis[v[j] >> 5], 1u << (v[j] & 31));
-        if (mark_preds) preds[v[j]] = ow.to_global(par);
-      } else if (d[j] <= (uint32_t)kPullK) {
-        scanned += d[j];
-        keep[j] = true;
+      if (found[j]) {
+        scanned += h0[j] ? 1 : 2;
+        labels[v] = next_label;
+        atomicOr(&vis[v >> 5], 1u << (v & 31));
+        if (mark_preds) preds[v] = ow.to_global(h0[j] ? r[j].z : r[j].w);
+        ++found_n;
       } else {
-        scanned += kPullK;
-        lng[j] = true;
+        scanned += d < (uint32_t)kPullK ? d : (uint32_t)kPullK;
       }
     }
 #pragma unroll
     for (int j = 0; j < kPV; ++j) {
-      q_found.push(found[j], v[j]);
-      q_keep.push(keep[j], v[j]);
-      q_long.push(lng[j], v[j]);
+      if (emit_found) q_found.push(found[j], r[j].x);
+      q_keep.push(keep[j], pos[j]);
+      q_long.push(lng[j], pos[j]);
     }
     __syncthreads();
     if (threadIdx.x == 0) {
-      q_found.base = q_found.n ? atomicAdd(&ctr->out_cnt, q_found.n) : 0u;
+      if (emit_found) q_found.base = q_found.n ? atomicAdd(&ctr->out_cnt, q_found.n) : 0u;
       q_keep.base = q_keep.n ? atomicAdd(ul_out_cnt, q_keep.n) : 0u;
       q_long.base = q_long.n ? atomicAdd(long_cnt, q_long.n) : 0u;
     }
     __syncthreads();
-    for (uint32_t k = threadIdx.x; k < q_found.n; k += 256) out[q_found.base + k] = q_found.buf[k];
+    if (emit_found)
+      for (uint32_t k = threadIdx.x; k < q_found.n; k += 256) out[q_found.base + k] = q_found.buf[k];
     for (uint32_t k = threadIdx.x; k < q_keep.n; k += 256) ul_out[q_keep.base + k] = q_keep.buf[k];
     for (uint32_t k = threadIdx.x; k < q_long.n; k += 256) longq[q_long.base + k] = q_long.buf[k];
     __syncthreads();
-    if (threadIdx.x == 0) q_found.n = q_keep.n = q_long.n = 0;
+    if (threadIdx.x == 0) {
+      if (emit_found) q_found.n = 0;
+      q_keep.n = q_long.n = 0;
+    }
     __syncthreads();
+  }
+  if (!emit_found) {
+    unsigned m = __reduce_add_sync(0xffffffffu, found_n);
+    if (lane_id() == 0 && m) atomicAdd(&s_found, m);
+    __syncthreads();
+    if (threadIdx.x == 0 && s_found) atomicAdd(&ctr->out_cnt, s_found);
   }
   warp_add_u64(scanned_out, scanned);
   warp_add_u64(&ctr->u[2], opened);
 }
 
-// pull step, stage 2: long rows, 8 lanes per vertex from arc kPullK on; each
-// round tests one 32-byte sector of col_indices and the first hit in arc
-// order wins, so W equals the reference's sequential count
+// pull step, stage 2: rows longer than the record, 8 lanes per vertex from arc
+// kPullK on; each round tests one 32-byte sector of col_indices and the first
+// hit in arc order wins, so W equals the reference's sequential count.  Queue
+// appends are CTA-aggregated like stage 1.
+constexpr int kGroupIters = 4;  // vertices per group between CTA flushes
+
 __global__ void __launch_bounds__(256)
-    dobfs_pull_group_kernel(GraphView g, const uint32_t* __restrict__ longq,
-                            const uint32_t* long_cnt, uint32_t* labels, uint32_t* preds,
-                            uint32_t* vis, const uint32_t* __restrict__ fb, uint32_t next_label,
-                            int mark_preds, OwnerView ow, uint32_t* out, uint32_t* ul_out,
+    dobfs_pull_group_kernel(GraphView g, const uint4* __restrict__ rec,
+                            const uint32_t* __restrict__ longq, const uint32_t* long_cnt,
+                            uint32_t* labels, uint32_t* preds, uint32_t* vis,
+                            const uint32_t* __restrict__ fb, uint32_t next_label, int mark_preds,
+                            OwnerView ow, int emit_found, uint32_t* out, uint32_t* ul_out,
                             uint32_t* ul_out_cnt, Counters* ctr,
                             unsigned long long* scanned_out) {
+  __shared__ BlockQueue<256 / kPullGroup * kGroupIters> q_found, q_keep;
+  __shared__ uint32_t s_found;
   const uint32_t nl = *long_cnt;
   const unsigned lane = threadIdx.x & 31u;
   const unsigned sub = lane & (kPullGroup - 1);
   const unsigned gbase = lane & ~(kPullGroup - 1);
   const unsigned gmask = ((1u << kPullGroup) - 1u) << gbase;
   unsigned long long scanned = 0;
-  const uint32_t groups = (gridDim.x * blockDim.x) / kPullGroup;
-  const uint32_t gid = (blockIdx.x * blockDim.x + threadIdx.x) / kPullGroup;
-  const uint32_t rounds = (nl + groups - 1) / groups;
-  for (uint32_t r = 0; r < rounds; ++r) {
-    uint32_t i = r * groups + gid;
-    bool found = false, keep = false;
-    uint32_t v = 0;
-    if (i < nl) {
-      v = longq[i];
-      const uint32_t b = g.off[v] + kPullK, e = g.off[v + 1];
-      keep = true;
-      for (uint32_t k = b; k < e; k += kPullGroup) {
-        uint32_t idx = k + sub;
-        uint32_t w = idx < e ? __ldg(&g.col[idx]) : 0u;
-        bool hit = idx < e && (__ldg(&fb[w >> 5]) & (1u << (w & 31)));
-        unsigned m = __ballot_sync(gmask, hit) & gmask;
-        if (m) {
-          unsigned first = __ffs(m) - 1 - gbase;
-          if (sub == 0) {
-            scanned += k - b + first + 1;
-            found = true;
-            keep = false;
+  uint32_t found_n = 0;
+  q_found.reset();
+  q_keep.reset();
+  if (threadIdx.x == 0) s_found = 0;
+  __syncthreads();
+  const uint32_t gpb = 256 / kPullGroup;  // groups per CTA
+  const uint32_t per_cta = gpb * kGroupIters;
+  for (uint32_t cbase = blockIdx.x * per_cta; cbase < nl; cbase += gridDim.x * per_cta) {
+    for (int it = 0; it < kGroupIters; ++it) {
+      const uint32_t i = cbase + it * gpb + threadIdx.x / kPullGroup;
+      bool found = false, keep = false;
+      uint32_t v = 0, pos = 0;
+      if (i < nl) {
+        pos = longq[i];
+        const uint4 r = rec[pos];
+        v = r.x;
+        const uint32_t row = g.off[v];
+        const uint32_t b = row + kPullK, e = row + r.y;
+        keep = true;
+        for (uint32_t k = b; k < e; k += kPullGroup) {
+          uint32_t idx = k + sub;
+          uint32_t w = idx < e ? __ldg(&g.col[idx]) : 0u;
+          bool hit = idx < e && bit_set(fb, w);
+          unsigned m = __ballot_sync(gmask, hit) & gmask;
+          if (m) {
+            unsigned first = __ffs(m) - 1 - gbase;
             uint32_t pw = __shfl_sync(gmask, w, gbase + first);
-            labels[v] = next_label;
-            atomicOr(&vis[v >> 5], 1u << (v & 31));
-            if (mark_preds) preds[v] = ow.to_global(pw);
-          } else {
-            __shfl_sync(gmask, w, gbase + first);
+            if (sub == 0) {
+              scanned += k - b + first + 1;
+              found = true;
+              keep = false;
+              labels[v] = next_label;
+              atomicOr(&vis[v >> 5], 1u << (v & 31));
+              if (mark_preds) preds[v] = ow.to_global(pw);
+              ++found_n;
+            }
+            break;
           }
-          break;
+          if (sub == 0) scanned += (e - k < (uint32_t)kPullGroup) ? (e - k) : kPullGroup;
         }
-        if (sub == 0) scanned += (e - k < (uint32_t)kPullGroup) ? (e - k) : kPullGroup;
+        if (sub != 0) keep = false;
       }
-      if (sub != 0) keep = false;
+      if (emit_found) q_found.push(found, v);
+      q_keep.push(keep, pos);
     }
-    uint32_t s = warp_append(&ctr->out_cnt, found);
-    if (found) out[s] = v;
-    s = warp_append(ul_out_cnt, keep);
-    if (keep) ul_out[s] = v;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      q_found.base = q_found.n ? atomicAdd(&ctr->out_cnt, q_found.n) : 0u;
+      q_keep.base = q_keep.n ? atomicAdd(ul_out_cnt, q_keep.n) : 0u;
+    }
+    __syncthreads();
+    for (uint32_t k = threadIdx.x; k < q_found.n; k += 256) out[q_found.base + k] = q_found.buf[k];
+    for (uint32_t k = threadIdx.x; k < q_keep.n; k += 256) ul_out[q_keep.base + k] = q_keep.buf[k];
+    __syncthreads();
+    if (threadIdx.x == 0) q_found.n = q_keep.n = 0;
+    __syncthreads();
+  }
+  if (!emit_found) {
+    unsigned m = __reduce_add_sync(0xffffffffu, found_n);
+    if (lane_id() == 0 && m) atomicAdd(&s_found, m);
+    __syncthreads();
+    if (threadIdx.x == 0 && s_found) atomicAdd(&ctr->out_cnt, s_found);
   }
   warp_add_u64(scanned_out, scanned);
+}
+
+// frontier list = vis & ~prev (the vertices discovered in the previous
+// superstep), rebuilt for a push step that follows a list-free pull step:
+// per round 256 words, a CTA scan of their popcounts, one atomic per round
+__global__ void __launch_bounds__(256)
+    bitmap_diff_list_kernel(const uint32_t* __restrict__ vis, const uint32_t* __restrict__ prev,
+                            uint32_t nw, uint32_t* out, uint32_t* cnt) {
+  using Scan = cub::BlockScan<uint32_t, 256>;
+  __shared__ typename Scan::TempStorage tmp;
+  __shared__ uint32_t s_base;
+  for (uint32_t base = blockIdx.x * 256; base < nw; base += gridDim.x * 256) {
+    const uint32_t i = base + threadIdx.x;
+    uint32_t d = i < nw ? (__ldg(&vis[i]) & ~__ldg(&prev[i])) : 0u;
+    uint32_t excl, total;
+    Scan(tmp).ExclusiveSum((uint32_t)__popc(d), excl, total);
+    if (threadIdx.x == 0) s_base = total ? atomicAdd(cnt, total) : 0u;
+    __syncthreads();
+    uint32_t o = s_base + excl;
+    while (d) {
+      out[o++] = i * 32 + (__ffs(d) - 1);
+      d &= d - 1;
+    }
+    __syncthreads();
+  }
 }
 
 struct DobfsPrim : PrimBase {
@@ -443,23 +518,31 @@ struct DobfsPrim : PrimBase {
     MGB_CUDA(cudaMemcpyAsync(&k, cnt.ptr, 4, cudaMemcpyDeviceToHost, w.stream));
     MGB_CUDA(cudaStreamSynchronize(w.stream));
     cnt.free_();
-    // ascending order keeps the pull step's offset loads coalesced
+    // ascending order keeps the pull step's record reads coalesced
     std::vector<uint32_t> h(k);
     MGB_CUDA(cudaMemcpy(h.data(), w.nonisolated.ptr, 4ull * k, cudaMemcpyDeviceToHost));
     std::sort(h.begin(), h.end());
     MGB_CUDA(cudaMemcpy(w.nonisolated.ptr, h.data(), 4ull * k, cudaMemcpyHostToDevice));
     w.n_nonisolated = k;
+    w.pull_rec.alloc(k ? k : 1);
+    if (k)
+      MGB_LAUNCH(pull_records_kernel, grid_for(k, 256, kNumSMs * 16), 256, 0, w.stream, w.graph(),
+                 w.nonisolated.ptr, k, w.pull_rec.ptr);
+    MGB_CUDA(cudaStreamSynchronize(w.stream));
     w.nonisolated_ready = true;
-    for (int i = 0; i < 3; ++i) w.aux[i].alloc(i < 2 ? (k ? k : 1) : 4);  // UL ping-pong, counters
   }
   void init(Ctx& c) {  // primitives.cpp:185-195
     Worker& w = *c.w;
     ensure_nonisolated(w);  // plan-lifetime precomputation, outside the timed region on reuse
+    const uint64_t k = w.n_nonisolated ? w.n_nonisolated : 1;
+    // unvisited lists (ping-pong) and the long-row queue: plan-lifetime buffers
+    for (int i = 0; i < 3; ++i)
+      if (w.ul_buf[i].n < k + 1 || !w.ul_buf[i].ptr) w.ul_buf[i].alloc(k + 1);
     fill(w.su32[0], w.nv, 0xFF, w.stream);        // labels
     fill(w.su32[2], words(w.nv), 0, w.stream);    // visited bitmap
     fill(w.aux[4], words(w.nv), 0, w.stream);     // visited as of the previous superstep
     if (w.su32[3].n < words(w.nv) || !w.su32[3].ptr) w.su32[3].alloc(words(w.nv));  // frontier
-    if (w.aux[3].n < w.n_nonisolated + 1 || !w.aux[3].ptr) w.aux[3].alloc(w.n_nonisolated + 1);
+    if (w.aux[2].n < 4 || !w.aux[2].ptr) w.aux[2].alloc(4);
     if (mark_preds) fill(w.su32[1], w.nv, 0xFF, w.stream);
     MGB_LAUNCH(set_one_kernel<uint32_t>, 1, 1, 0, w.stream, w.su32[0].ptr, source, 0u);
     uint32_t sw = 1u << (source & 31);
@@ -468,9 +551,11 @@ struct DobfsPrim : PrimBase {
     if (ul_src.empty()) {
       ul_src.assign(c.P->n, -1);
       ul_len.assign(c.P->n, 0);
+      list_free.assign(c.P->n, false);
     }
     ul_src[w.p] = -1;
     ul_len[w.p] = w.n_nonisolated;
+    list_free[w.p] = false;
   }
   static void set_bit_host(Worker& w, uint32_t v, uint32_t bit) {
     MGB_LAUNCH(or_word_kernel, 1, 1, 0, w.stream, w.su32[2].ptr + (v >> 5), bit);
@@ -503,6 +588,19 @@ struct DobfsPrim : PrimBase {
       dir_log.push_back(dir);
     }
     const uint64_t nw = words(w.nv);
+    if (list_free[w.p]) {
+      // the previous (pull) superstep only counted its discoveries: rebuild the
+      // input frontier list from the visited bitmap (vis & ~vis_prev); a pull
+      // step needs no list, only the bitmap
+      list_free[w.p] = false;
+      if (dir == 0) {  // this superstep advances (or sizes) from the list
+        uint32_t* cnt = w.aux[2].ptr + 2;
+        MGB_CUDA(cudaMemsetAsync(cnt, 0, 4, w.stream));
+        w.input.ensure(c.in_count, w.stream);
+        MGB_LAUNCH(bitmap_diff_list_kernel, grid_for(nw, 256, kNumSMs * 8), 256, 0, w.stream,
+                   w.su32[2].ptr, w.aux[4].ptr, (uint32_t)nw, w.input.ptr, cnt);
+      }
+    }
     // extension (mg_config.dobfs_exact_cost, single partition): a logically
     // forward superstep whose exact edge count Σdeg(Q) dwarfs the unvisited
     // list is computed by the pull kernels instead.  For one partition both
@@ -534,33 +632,37 @@ struct DobfsPrim : PrimBase {
     MGB_LAUNCH(frontier_diff_kernel, grid_for(nw, 256, kNumSMs * 8), 256, 0, w.stream,
                w.su32[2].ptr, w.aux[4].ptr, w.su32[3].ptr, (uint32_t)nw);
     const int src = ul_src[w.p];
-    const uint32_t* ul = src < 0 ? w.nonisolated.ptr : w.aux[src].ptr;
+    const uint32_t* ul = src < 0 ? nullptr : w.ul_buf[src].ptr;  // null: every record
     const int dst = src == 0 ? 1 : 0;
     const uint32_t nul = ul_len[w.p];
     uint32_t* ulcnt = &c.ctr()->misc;  // reported with the superstep's counters
     uint32_t* cnts = w.aux[2].ptr;     // [1] long-row queue length
     MGB_CUDA(cudaMemsetAsync(cnts, 0, 8, w.stream));
-    c.ensure_output(nul);
+    // one partition under the max policy: discoveries are counted, not listed
+    // (the next superstep rebuilds a list from the bitmap only if it pushes)
+    const bool emit = c.P->n > 1 || c.want_deg;
+    if (emit) c.ensure_output(nul);
     const uint32_t next_label = (uint32_t)c.iter + 1;
     if (c.P->profile) {
       MGB_CUDA(cudaEventRecord(w.ev_k0, w.stream));
       prof_nul_[w.p] = nul;
-      prof_kind_[w.p] = 0;
+      prof_kind_[w.p] = dir == 1 ? 0 : 2;  // 2: forward superstep run as a pull
     }
     // examined arcs: the reference's W in a backward step; a scratch counter
     // when a forward step runs physically as a pull (W = Σdeg(Q) then)
     unsigned long long* scanned = dir == 1 ? &c.ctr()->edges : &c.ctr()->u[3];
     if (nul) {
       MGB_LAUNCH(dobfs_pull_thread_kernel, grid_for(nul, 256 * kPV, kNumSMs * 8), 256, 0,
-                 w.stream,
-                 w.graph(), ul, nul, w.su32[0].ptr, w.su32[1].ptr, w.su32[2].ptr, w.su32[3].ptr,
-                 next_label, mark_preds ? 1 : 0, c.owner_view(), w.output.ptr, w.aux[dst].ptr,
-                 ulcnt, w.aux[3].ptr, cnts + 1, c.ctr(), scanned);
-      MGB_LAUNCH(dobfs_pull_group_kernel, kNumSMs * 16, 256, 0, w.stream, w.graph(), w.aux[3].ptr,
-                 cnts + 1, w.su32[0].ptr, w.su32[1].ptr, w.su32[2].ptr, w.su32[3].ptr, next_label,
-                 mark_preds ? 1 : 0, c.owner_view(), w.output.ptr, w.aux[dst].ptr, ulcnt, c.ctr(),
+                 w.stream, w.pull_rec.ptr, ul, nul, w.su32[0].ptr, w.su32[1].ptr, w.su32[2].ptr,
+                 w.su32[3].ptr, next_label, mark_preds ? 1 : 0, c.owner_view(), emit ? 1 : 0,
+                 w.output.ptr, w.ul_buf[dst].ptr, ulcnt, w.ul_buf[2].ptr, cnts + 1, c.ctr(),
                  scanned);
+      MGB_LAUNCH(dobfs_pull_group_kernel, kNumSMs * 8, 256, 0, w.stream, w.graph(),
+                 w.pull_rec.ptr, w.ul_buf[2].ptr, cnts + 1, w.su32[0].ptr, w.su32[1].ptr,
+                 w.su32[2].ptr, w.su32[3].ptr, next_label, mark_preds ? 1 : 0, c.owner_view(),
+                 emit ? 1 : 0, w.output.ptr, w.ul_buf[dst].ptr, ulcnt, c.ctr(), scanned);
     }
+    list_free[w.p] = !emit;
     if (dir == 0) {
       unsigned long long lw = logical_w;  // pageable source: staged before return
       MGB_CUDA(cudaMemcpyAsync(&c.ctr()->edges, &lw, 8, cudaMemcpyHostToDevice, w.stream));
@@ -593,7 +695,10 @@ struct DobfsPrim : PrimBase {
       c.P->prof2_launches += 1;
       return;
     }
-    double bytes = 4.0 * prof_nul_[w.p] + 8.0 * (double)h.u[2] + 4.0 * (double)h.edges +
+    // arcs the pull kernels examined: W of a backward superstep; in a forward
+    // superstep run as a pull W is the logical push count, the scan sits in u[3]
+    const double examined = prof_kind_[w.p] == 0 ? (double)h.edges : (double)h.u[3];
+    double bytes = 4.0 * prof_nul_[w.p] + 8.0 * (double)h.u[2] + 4.0 * examined +
                    8.0 * (double)h.out_cnt + 4.0 * (double)h.misc;
     c.P->prof_ms += ms;
     c.P->prof_bytes += bytes;
@@ -602,6 +707,7 @@ struct DobfsPrim : PrimBase {
   std::vector<int> prof_kind_ = std::vector<int>(kMaxWorkers, 0);
   void finalize(Ctx& c, const GlobalView&) { collect_profile(c); }
   std::vector<bool> pending_ul_ = std::vector<bool>(kMaxWorkers, false);
+  std::vector<bool> list_free;  // per worker: last pull step counted, did not list
   std::vector<bool> prof_pending_ = std::vector<bool>(kMaxWorkers, false);
   std::vector<uint32_t> prof_nul_ = std::vector<uint32_t>(kMaxWorkers, 0);
 };
@@ -609,10 +715,17 @@ struct DobfsPrim : PrimBase {
 // ===========================================================================
 // SSSP (primitives.cpp:307-397)
 
+// Distances are kept in T = u32 when every finite distance fits (max edge
+// weight x |V| < 2^32 - 1: RMAT-24 with w <= 64 needs 1.07e9), else u64 like
+// the reference.  The u32 array is half the size (67 MB at |V| = 2^24, inside
+// the 126 MB L2), so the random relaxation atomics hit L2; results are widened
+// to u64 (u32 inf -> u64 inf) when the run finishes.
+template <class T>
 struct SsspDev {
-  unsigned long long* dists;
-  const unsigned long long* fdist;
-  unsigned long long* last_sent;
+  static constexpr T kInf = (T)~(T)0;
+  T* dists;
+  const T* fdist;
+  T* last_sent;
   uint32_t* preds;
   uint32_t* seen;
   const uint32_t* w;
@@ -621,9 +734,9 @@ struct SsspDev {
   int mark_preds;
   // relax from the superstep-frozen source distance (primitives.cpp:340-348)
   __device__ bool visit(uint32_t u, uint32_t v, uint32_t e) const {
-    unsigned long long nd = fdist[u] + w[e];
-    if (nd >= dists[v]) return false;
-    unsigned long long old = atomicMin(&dists[v], nd);
+    T nd = fdist[u] + (T)w[e];
+    if (nd >= __ldcg(&dists[v])) return false;
+    T old = atomicMin(&dists[v], nd);
     if (nd < old) {
       if (mark_preds) preds[v] = ow.to_global(u);
       return true;
@@ -631,10 +744,10 @@ struct SsspDev {
     return false;
   }
   __device__ bool keep(uint32_t v) const { return atomicExch(&seen[v], iter + 1) != iter + 1; }
-  __device__ bool prefilter(uint32_t v) const { return true; }
+  __device__ bool prefilter(uint32_t) const { return true; }
   __device__ bool combine(uint32_t v, const uint32_t* va, const double* vv, uint32_t) const {
-    unsigned long long nd = (unsigned long long)vv[0];
-    unsigned long long old = atomicMin(&dists[v], nd);
+    T nd = (T)vv[0];
+    T old = atomicMin(&dists[v], nd);
     if (nd < old) {
       if (mark_preds) preds[v] = va[0];
       return ow.hosts(v);
@@ -656,17 +769,27 @@ struct SsspDev {
   __device__ uint32_t peer_id(uint32_t v, uint32_t, uint32_t) const { return v; }
 };
 
-__global__ void snapshot_kernel(const uint32_t* __restrict__ in, uint32_t n,
-                                const unsigned long long* dists, unsigned long long* fdist) {
+template <class T>
+__global__ void snapshot_kernel(const uint32_t* __restrict__ in, uint32_t n, const T* dists,
+                                T* fdist) {
   for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
     uint32_t u = in[i];
     fdist[u] = dists[u];
   }
 }
 
+__global__ void widen_dist_kernel(const uint32_t* __restrict__ d32, uint32_t n,
+                                  unsigned long long* d64) {
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    uint32_t d = d32[i];
+    d64[i] = d == kInfLabel ? ~0ull : (unsigned long long)d;
+  }
+}
+
 struct SsspPrim : PrimBase {
   uint32_t source;
   bool mark_preds;
+  bool narrow = false;  // u32 distances (decided per run from the plan's max weight)
   SsspPrim(uint32_t s, bool m) : source(s), mark_preds(m) {
     name = "sssp";
     nva = m ? 1 : 0;
@@ -675,26 +798,54 @@ struct SsspPrim : PrimBase {
   }
   void init(Ctx& c) {  // primitives.cpp:323-332
     Worker& w = *c.w;
-    fill(w.su64[0], w.nv, 0xFF, w.stream);  // dists
-    fill(w.su64[1], w.nv, 0xFF, w.stream);  // frontier_dist
-    fill(w.su64[2], w.nv, 0xFF, w.stream);  // last_sent
+    narrow = (uint64_t)c.P->max_weight * ((uint64_t)c.P->nv + 1) < 0xFFFFFFFFull;
+    if (narrow) {
+      fill(w.su32[0], w.nv, 0xFF, w.stream);  // dists
+      fill(w.su32[3], w.nv, 0xFF, w.stream);  // frontier_dist
+      fill(w.aux[5], w.nv, 0xFF, w.stream);   // last_sent
+      MGB_LAUNCH(set_one_kernel<uint32_t>, 1, 1, 0, w.stream, w.su32[0].ptr, source, 0u);
+    } else {
+      fill(w.su64[0], w.nv, 0xFF, w.stream);  // dists
+      fill(w.su64[1], w.nv, 0xFF, w.stream);  // frontier_dist
+      fill(w.su64[2], w.nv, 0xFF, w.stream);  // last_sent
+      MGB_LAUNCH(set_one_kernel<unsigned long long>, 1, 1, 0, w.stream, w.su64[0].ptr, source,
+                 0ull);
+    }
     fill(w.su32[2], w.nv, 0, w.stream);     // seen
     if (mark_preds) fill(w.su32[1], w.nv, 0xFF, w.stream);
-    MGB_LAUNCH(set_one_kernel<unsigned long long>, 1, 1, 0, w.stream, w.su64[0].ptr, source,
-               0ull);
     if (c.P->owner_host[source] == w.p) c.push_initial({source});
   }
-  SsspDev dev(Ctx& c) {
+  SsspDev<uint32_t> dev32(Ctx& c) {
+    Worker& w = *c.w;
+    return {w.su32[0].ptr, w.su32[3].ptr, w.aux[5].ptr, w.su32[1].ptr, w.su32[2].ptr,
+            w.w.ptr, c.owner_view(), (uint32_t)c.iter, mark_preds ? 1 : 0};
+  }
+  SsspDev<unsigned long long> dev64(Ctx& c) {
     Worker& w = *c.w;
     return {w.su64[0].ptr, w.su64[1].ptr, w.su64[2].ptr, w.su32[1].ptr, w.su32[2].ptr,
             w.w.ptr, c.owner_view(), (uint32_t)c.iter, mark_preds ? 1 : 0};
   }
   void body(Ctx& c) {
     Worker& w = *c.w;
-    if (c.in_count)
-      MGB_LAUNCH(snapshot_kernel, grid_for(c.in_count, 256), 256, 0, w.stream, w.input.ptr,
-                 c.in_count, w.su64[0].ptr, w.su64[1].ptr);
-    c.pipeline(dev(c), w.nv);
+    if (narrow) {
+      if (c.in_count)
+        MGB_LAUNCH(snapshot_kernel<uint32_t>, grid_for(c.in_count, 256), 256, 0, w.stream,
+                   w.input.ptr, c.in_count, w.su32[0].ptr, w.su32[3].ptr);
+      c.pipeline(dev32(c), w.nv);
+    } else {
+      if (c.in_count)
+        MGB_LAUNCH(snapshot_kernel<unsigned long long>, grid_for(c.in_count, 256), 256, 0,
+                   w.stream, w.input.ptr, c.in_count, w.su64[0].ptr, w.su64[1].ptr);
+      c.pipeline(dev64(c), w.nv);
+    }
+  }
+  void finalize(Ctx& c, const GlobalView&) {
+    Worker& w = *c.w;
+    if (!narrow) return;
+    if (w.su64[0].n < w.nv || !w.su64[0].ptr) w.su64[0].alloc(w.nv ? w.nv : 1);
+    if (w.nv)
+      MGB_LAUNCH(widen_dist_kernel, grid_for(w.nv, 256, kNumSMs * 8), 256, 0, w.stream,
+                 w.su32[0].ptr, w.nv, w.su64[0].ptr);
   }
 };
 
