@@ -243,13 +243,14 @@ struct Ctx {
     // tile table: exact when the degree sum is known, else bounded by 2|E_i|
     // (an input frontier may hold a vertex twice, e.g. SSSP, E:901-904 + E:845)
     const uint64_t max_deg = in_degsum == kUnknownDeg ? 2 * w->ne + 1 : in_degsum;
-    const uint64_t max_tiles = max_deg / kTile + 2;
+    const uint64_t max_tiles = max_deg / kTile + 2 + kMinTiles;
     if (w->lb_tile.n < max_tiles + 1) w->lb_tile.alloc(max_tiles + 1);
     MGB_LAUNCH(lb_tiles_kernel, grid_for(max_tiles + 1, 256, kNumSMs * 8), 256, 0, w->stream,
                w->lb_pref.ptr, w->lb_bsum.ptr, in_count, w->lb_bsum.ptr + nb, w->lb_tile.ptr,
                (uint32_t)max_tiles);
     const unsigned resident = kNumSMs * 6;  // 32 KB smem + 256 threads per CTA
-    unsigned grid = in_degsum == kUnknownDeg ? resident : grid_for(in_degsum, kTile, resident);
+    unsigned grid = in_degsum == kUnknownDeg ? resident
+                                             : grid_for(in_degsum, lb_tile_size(in_degsum), resident);
     MGB_LAUNCH((lb_expand_kernel<F, kFused>), grid, kExpBlock, 0, w->stream, f, graph(),
                w->input.ptr, in_count, w->lb_row.ptr, w->lb_pref.ptr, w->lb_bsum.ptr,
                w->lb_bsum.ptr + nb, w->lb_tile.ptr, dst, dst_cnt);
@@ -536,7 +537,7 @@ void run_primitive(Plan& P, Prim& prim, const mg_config& cfg) {
       }
       view.reports[p] = r;
       rs.next_count[p] = (uint32_t)r.next_frontier;
-      rs.next_deg[p] = want_deg ? hc.next_deg : kUnknownDeg;
+      rs.next_deg[p] = (want_deg || prim.reports_deg) ? hc.next_deg : kUnknownDeg;
       if (n > 1) {
         for (uint32_t q = 0; q < n; ++q) {
           if (q == p) continue;

@@ -410,4 +410,32 @@ HostPlan build_plan(const HostCsr& g, const std::vector<uint32_t>& owner, uint32
   return P;
 }
 
+// Locality order for gather-heavy kernels (PageRank pull): the discovery order
+// of a FIFO breadth-first search (Cuthill-McKee without the degree sort),
+// started at the lowest-ID unvisited vertex of every component.  Neighbours
+// end up within one BFS level band of each other, so a pull over rows in this
+// order gathers from a narrow window instead of the whole vertex array.
+// Returns perm[old] = new.
+std::vector<uint32_t> bfs_locality_order(const uint32_t* off, const uint32_t* col, uint32_t nv) {
+  std::vector<uint32_t> perm(nv, kInvalid), queue(nv);
+  uint32_t next = 0;
+  for (uint32_t s = 0; s < nv; ++s) {
+    if (perm[s] != kInvalid) continue;
+    uint32_t head = next, tail = next;
+    perm[s] = next++;
+    queue[tail++] = s;
+    while (head < tail) {
+      const uint32_t u = queue[head++];
+      for (uint32_t e = off[u]; e < off[u + 1]; ++e) {
+        const uint32_t v = col[e];
+        if (perm[v] == kInvalid) {
+          perm[v] = next++;
+          queue[tail++] = v;
+        }
+      }
+    }
+  }
+  return perm;
+}
+
 }  // namespace mgb

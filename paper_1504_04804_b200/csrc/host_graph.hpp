@@ -77,6 +77,9 @@ struct HostPlan {
 
 HostPlan build_plan(const HostCsr& g, const std::vector<uint32_t>& owner, uint32_t n, int dup);
 
+// FIFO-BFS (Cuthill-McKee order without degree sort) vertex order: perm[old] = new
+std::vector<uint32_t> bfs_locality_order(const uint32_t* off, const uint32_t* col, uint32_t nv);
+
 // counter-based R-MAT draw shared by host and device: edge i, bit k
 struct RmatThresholds {
   uint32_t a, ab, abc;

@@ -6,13 +6,15 @@
 //   lb_degree_kernel   one pass over the frontier: row start + out-degree per
 //                      vertex, CTA-local exclusive scan of the degrees, CTA sums
 //   lb_scan_kernel     one CTA scans the CTA sums (global offsets + total W)
-//   lb_expand_kernel   persistent CTAs walk fixed tiles of kTile arcs of the
-//                      concatenated adjacency: one binary search per tile over
-//                      the global degree prefix, the tile's vertex range staged
-//                      in shared memory, then every thread expands kItems
-//                      consecutive arcs (one smem search + a linear walk), so
-//                      a 1e6-arc hub is spread over every SM and consecutive
-//                      threads read consecutive col_indices.
+//   lb_expand_kernel   persistent CTAs walk tiles of the concatenated
+//                      adjacency (kTile = 8192 arcs, smaller for small advances
+//                      so at least kMinTiles = 2 x 148 tiles exist): one binary
+//                      search per tile over the global degree prefix, the
+//                      tile's vertex range staged in shared memory in chunks of
+//                      kStage vertices, then every lane expands kItems
+//                      lane-strided arcs (one smem search + a short walk), so a
+//                      1e6-arc hub is spread over every SM and consecutive
+//                      lanes read consecutive col_indices.
 // The edge count W (reference E:66) is the scan total.
 // filter = order-free compaction by keep(v) with warp-aggregated appends.
 #pragma once
@@ -26,9 +28,7 @@ namespace mgb {
 constexpr int kLbBlock = 256;     // degree pass: one vertex per thread
 constexpr int kExpBlock = 256;    // expansion CTA
 constexpr int kItems = 8;         // arcs per thread per batch (lane-strided)
-constexpr int kBatches = 4;       // batches per warp per tile
-constexpr uint32_t kWarpArcs = 32 * kItems * kBatches;     // 1024
-constexpr uint32_t kTile = (kExpBlock / 32) * kWarpArcs;   // 8192 arcs per tile
+constexpr uint32_t kTile = 8192;  // arcs per tile for large advances
 constexpr int kWarpQ = 384;       // warp-private output staging entries
 constexpr int kStage = 1536;      // max tile vertices staged in shared memory
 
@@ -80,6 +80,16 @@ static __global__ void __launch_bounds__(1024)
   }
 }
 
+// Arcs per expansion tile: kTile for large advances; small advances are cut
+// into at least kMinTiles tiles (multiples of 256 arcs) so every SM gets work.
+constexpr uint32_t kMinTiles = 2 * kNumSMs;
+__host__ __device__ __forceinline__ unsigned long long lb_tile_size(unsigned long long total) {
+  if (total >= (unsigned long long)kTile * kMinTiles) return kTile;
+  unsigned long long t = (total + kMinTiles - 1) / kMinTiles;
+  t = (t + 255) / 256 * 256;
+  return t < 256 ? 256 : t;
+}
+
 // global prefix of frontier entry i
 __device__ __forceinline__ unsigned long long lb_pref(const unsigned long long* prefix,
                                                       const unsigned long long* block_off,
@@ -118,15 +128,17 @@ static __global__ void lb_tiles_kernel(const unsigned long long* __restrict__ pr
                                        uint32_t n_in, const unsigned long long* total_ptr,
                                        uint32_t* tile_lo, uint32_t max_tiles) {
   const unsigned long long total = *total_ptr;
-  const unsigned long long ntiles = (total + kTile - 1) / kTile;
+  const unsigned long long ts = lb_tile_size(total);
+  const unsigned long long ntiles = (total + ts - 1) / ts;
   for (unsigned long long t = blockIdx.x * (unsigned long long)blockDim.x + threadIdx.x;
        t <= ntiles && t <= max_tiles; t += (unsigned long long)gridDim.x * blockDim.x)
-    tile_lo[t] = t == ntiles ? n_in - 1 : lb_search(prefix, block_off, n_in, t * kTile);
+    tile_lo[t] = t == ntiles ? n_in - 1 : lb_search(prefix, block_off, n_in, t * ts);
 }
 
 // lb 3b: edge-balanced expansion (visit [+ keep when fused]).  Per tile the
-// vertex range is staged in shared memory; warp w owns arcs [t0+w*32*kItems,
-// +32*kItems) with lane l taking arcs l, l+32, ... (coalesced col_indices).
+// vertex range is staged in shared memory (chunks of kStage vertices); batches
+// of 32*kItems arcs go round-robin to the warps, lane l taking arcs l, l+32,
+// ... of its batch (coalesced col_indices).
 // The kItems arcs of a lane go through four batched phases — locate, load the
 // neighbour IDs, pre-test them (prefilter, e.g. the visited bitmap in L2),
 // then visit the survivors — so each thread keeps kItems independent loads in
@@ -144,13 +156,14 @@ __global__ void __launch_bounds__(kExpBlock)
   __shared__ uint32_t s_src[kStage];
   __shared__ uint32_t s_q[kExpBlock / 32][kWarpQ];
   const unsigned long long total = *total_ptr;
-  const unsigned long long ntiles = (total + kTile - 1) / kTile;
+  const unsigned long long ts = lb_tile_size(total);
+  const unsigned long long ntiles = (total + ts - 1) / ts;
   const unsigned warp = threadIdx.x >> 5, lane = lane_id();
   WarpQueue<kWarpQ, kWarpQ - 32 * kItems> q;
   q.init(s_q[warp]);
   for (unsigned long long tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-    const unsigned long long t0 = tile * kTile;
-    const unsigned long long t1 = t0 + kTile < total ? t0 + kTile : total;
+    const unsigned long long t0 = tile * ts;
+    const unsigned long long t1 = t0 + ts < total ? t0 + ts : total;
     const uint32_t lo = tile_lo[tile];
     const uint32_t hi = tile + 1 < ntiles ? tile_lo[tile + 1] : n_in - 1;
     const uint32_t R = hi - lo + 1;

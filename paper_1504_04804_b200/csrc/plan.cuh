@@ -124,6 +124,9 @@ struct Worker {
   DevArray<uint32_t> toff, tcol, tlong;
   uint32_t n_tlong = 0;
   bool transpose_ready = false;
+  bool pr_reordered = false;          // single partition: PR arrays in locality order
+  DevArray<uint32_t> pr_perm, pr_pdeg;  // vertex -> ordered position; out-degree by position
+  DevArray<uint32_t> pr_iperm;          // ordered position -> vertex
   uint32_t n_nonisolated = 0;
   bool nonisolated_ready = false;
   std::vector<uint32_t> hosted_host;  // hosted local IDs (host copy)

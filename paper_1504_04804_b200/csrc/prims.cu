@@ -30,6 +30,7 @@ struct PrimBase {
   bool allow_comm_override = false;
   int dup_required = MG_DUP_ALL;
   bool has_stop_condition = false;
+  bool reports_deg = false;  // body leaves Σdeg(next frontier) in ctr->next_deg
   uint64_t inbox_bound(Plan& P, uint32_t src, uint32_t dst, int comm) const {
     // selective: each proxy at most once per superstep (keep dedup) -> |B_{src,dst}|;
     // broadcast: the whole output, bounded by |V_src| local IDs
@@ -275,21 +276,64 @@ __device__ __forceinline__ bool bit_set(const uint32_t* bits, uint32_t v) {
   return (__ldg(&bits[v >> 5]) >> (v & 31)) & 1u;
 }
 
+// Warp-level append of up to kPV items per lane into a CTA queue: ONE shared
+// atomic per warp per call (the ballots of all kPV slots are summed first).
+template <int K, int kCap>
+__device__ __forceinline__ void warp_queue_append(BlockQueue<kCap>& q, const bool* pred,
+                                                  const uint32_t* val) {
+  unsigned m[K];
+  uint32_t tot = 0;
+#pragma unroll
+  for (int j = 0; j < K; ++j) {
+    m[j] = __ballot_sync(0xffffffffu, pred[j]);
+    tot += __popc(m[j]);
+  }
+  if (!tot) return;
+  uint32_t base = 0;
+  if (lane_id() == 0) base = atomicAdd(&q.n, tot);
+  base = __shfl_sync(0xffffffffu, base, 0);
+  const unsigned lt = (1u << lane_id()) - 1u;
+#pragma unroll
+  for (int j = 0; j < K; ++j) {
+    if (pred[j]) q.buf[base + __popc(m[j] & lt)] = val[j];
+    base += __popc(m[j]);
+  }
+}
+
+// set the visited bits of the lanes' discoveries with one atomicOr per run of
+// lanes hitting the same word (records are sorted, so a warp's discoveries
+// form few runs): a segmented OR by shuffles, the run head issues the atomic
+__device__ __forceinline__ void warp_set_bits(uint32_t* bits, bool pred, uint32_t v) {
+  const uint32_t wd = pred ? v >> 5 : 0xFFFFFFFFu;
+  uint32_t b = pred ? 1u << (v & 31) : 0u;
+  const unsigned lane = lane_id();
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t ob = __shfl_down_sync(0xffffffffu, b, o);
+    const uint32_t ow = __shfl_down_sync(0xffffffffu, wd, o);
+    if (lane + o < 32 && ow == wd) b |= ob;
+  }
+  const uint32_t pw = __shfl_up_sync(0xffffffffu, wd, 1);
+  if (pred && (lane == 0 || pw != wd)) atomicOr(&bits[wd], b);
+}
+
 // pull step, stage 1 (primitives.cpp:230-251): one thread per unvisited record
 // tests the record's two arcs against the frontier bitmap; a hit labels the
 // vertex, a short row without a hit stays unvisited, a longer row goes to the
-// cooperative stage.  CTA queues (one global atomic per queue per 256*kPV
-// records).  With emit_found == 0 (single partition) the discovered vertices
-// are only counted: the next superstep rebuilds the frontier from the visited
-// bitmap when it needs a list (a pull never does).
-__global__ void __launch_bounds__(256)
+// cooperative stage.  CTA queues with one shared atomic per warp and one
+// global atomic per queue per 256*kPV records.  With emit_found == 0 (single
+// partition) the discovered vertices are only counted (and their degrees
+// summed into deg_out when non-null): the next superstep rebuilds the frontier
+// list from the visited bitmap only if it pushes.
+__global__ void __launch_bounds__(256, 4)
     dobfs_pull_thread_kernel(const uint4* __restrict__ rec, const uint32_t* __restrict__ ul,
                              uint32_t nul, uint32_t* labels, uint32_t* preds, uint32_t* vis,
                              const uint32_t* __restrict__ fb, uint32_t next_label, int mark_preds,
                              OwnerView ow, int emit_found, uint32_t* out, uint32_t* ul_out,
                              uint32_t* ul_out_cnt, uint32_t* longq, uint32_t* long_cnt,
-                             Counters* ctr, unsigned long long* scanned_out) {
-  unsigned long long scanned = 0, opened = 0;
+                             Counters* ctr, unsigned long long* scanned_out,
+                             unsigned long long* deg_out) {
+  unsigned long long scanned = 0, opened = 0, degs = 0;
   uint32_t found_n = 0;
   __shared__ BlockQueue<256 * kPV> q_found, q_keep, q_long;
   __shared__ uint32_t s_found;
@@ -318,46 +362,41 @@ __global__ void __launch_bounds__(256)
       h1[j] = open[j] && r[j].y > 1 && bit_set(fb, r[j].w);
     }
     bool found[kPV], keep[kPV], lng[kPV];
+    uint32_t vv[kPV];
 #pragma unroll
     for (int j = 0; j < kPV; ++j) {
       const uint32_t v = r[j].x, d = r[j].y;
+      vv[j] = v;
       found[j] = open[j] && (h0[j] || h1[j]);
       keep[j] = open[j] && !found[j] && d <= (uint32_t)kPullK;
       lng[j] = open[j] && !found[j] && d > (uint32_t)kPullK;
-      if (!open[j]) continue;
-      ++opened;
+      opened += open[j];
       if (found[j]) {
         scanned += h0[j] ? 1 : 2;
         labels[v] = next_label;
-        atomicOr(&vis[v >> 5], 1u << (v & 31));
         if (mark_preds) preds[v] = ow.to_global(h0[j] ? r[j].z : r[j].w);
         ++found_n;
-      } else {
+        degs += d;
+      } else if (open[j]) {
         scanned += d < (uint32_t)kPullK ? d : (uint32_t)kPullK;
       }
+      warp_set_bits(vis, found[j], v);
     }
-#pragma unroll
-    for (int j = 0; j < kPV; ++j) {
-      if (emit_found) q_found.push(found[j], r[j].x);
-      q_keep.push(keep[j], pos[j]);
-      q_long.push(lng[j], pos[j]);
-    }
+    if (emit_found) warp_queue_append<kPV>(q_found, found, vv);
+    warp_queue_append<kPV>(q_keep, keep, pos);
+    warp_queue_append<kPV>(q_long, lng, pos);
     __syncthreads();
     if (threadIdx.x == 0) {
-      if (emit_found) q_found.base = q_found.n ? atomicAdd(&ctr->out_cnt, q_found.n) : 0u;
+      q_found.base = q_found.n ? atomicAdd(&ctr->out_cnt, q_found.n) : 0u;
       q_keep.base = q_keep.n ? atomicAdd(ul_out_cnt, q_keep.n) : 0u;
       q_long.base = q_long.n ? atomicAdd(long_cnt, q_long.n) : 0u;
     }
     __syncthreads();
-    if (emit_found)
-      for (uint32_t k = threadIdx.x; k < q_found.n; k += 256) out[q_found.base + k] = q_found.buf[k];
+    for (uint32_t k = threadIdx.x; k < q_found.n; k += 256) out[q_found.base + k] = q_found.buf[k];
     for (uint32_t k = threadIdx.x; k < q_keep.n; k += 256) ul_out[q_keep.base + k] = q_keep.buf[k];
     for (uint32_t k = threadIdx.x; k < q_long.n; k += 256) longq[q_long.base + k] = q_long.buf[k];
     __syncthreads();
-    if (threadIdx.x == 0) {
-      if (emit_found) q_found.n = 0;
-      q_keep.n = q_long.n = 0;
-    }
+    if (threadIdx.x == 0) q_found.n = q_keep.n = q_long.n = 0;
     __syncthreads();
   }
   if (!emit_found) {
@@ -368,6 +407,7 @@ __global__ void __launch_bounds__(256)
   }
   warp_add_u64(scanned_out, scanned);
   warp_add_u64(&ctr->u[2], opened);
+  if (deg_out) warp_add_u64(deg_out, degs);
 }
 
 // pull step, stage 2: rows longer than the record, 8 lanes per vertex from arc
@@ -383,8 +423,9 @@ __global__ void __launch_bounds__(256)
                             const uint32_t* __restrict__ fb, uint32_t next_label, int mark_preds,
                             OwnerView ow, int emit_found, uint32_t* out, uint32_t* ul_out,
                             uint32_t* ul_out_cnt, Counters* ctr,
-                            unsigned long long* scanned_out) {
+                            unsigned long long* scanned_out, unsigned long long* deg_out) {
   __shared__ BlockQueue<256 / kPullGroup * kGroupIters> q_found, q_keep;
+  unsigned long long degs = 0;
   __shared__ uint32_t s_found;
   const uint32_t nl = *long_cnt;
   const unsigned lane = threadIdx.x & 31u;
@@ -404,9 +445,10 @@ __global__ void __launch_bounds__(256)
       const uint32_t i = cbase + it * gpb + threadIdx.x / kPullGroup;
       bool found = false, keep = false;
       uint32_t v = 0, pos = 0;
+      uint4 r;
       if (i < nl) {
         pos = longq[i];
-        const uint4 r = rec[pos];
+        r = rec[pos];
         v = r.x;
         const uint32_t row = g.off[v];
         const uint32_t b = row + kPullK, e = row + r.y;
@@ -427,6 +469,7 @@ __global__ void __launch_bounds__(256)
               atomicOr(&vis[v >> 5], 1u << (v & 31));
               if (mark_preds) preds[v] = ow.to_global(pw);
               ++found_n;
+              degs += r.y;
             }
             break;
           }
@@ -456,6 +499,7 @@ __global__ void __launch_bounds__(256)
     if (threadIdx.x == 0 && s_found) atomicAdd(&ctr->out_cnt, s_found);
   }
   warp_add_u64(scanned_out, scanned);
+  if (deg_out) warp_add_u64(deg_out, degs);
 }
 
 // frontier list = vis & ~prev (the vertices discovered in the previous
@@ -497,8 +541,9 @@ struct DobfsPrim : PrimBase {
   std::vector<uint32_t> ul_len;
   bool exact_cost = false;
   uint64_t physical_pull_steps = 0;
-  DobfsPrim(uint32_t s, double a, double b, bool m, bool exact)
+  DobfsPrim(uint32_t s, double a, double b, bool m, bool exact, uint32_t nparts)
       : source(s), do_a(a), do_b(b), mark_preds(m), exact_cost(exact) {
+    reports_deg = exact && nparts == 1;
     name = "dobfs";
     nva = m ? 1 : 0;
     communication = MG_COMM_BROADCAST;
@@ -624,6 +669,9 @@ struct DobfsPrim : PrimBase {
         prof_kind_[w.p] = 1;
         prof_nul_[w.p] = c.in_count;
       }
+      if (reports_deg && !c.want_deg)
+        MGB_LAUNCH(degsum_dev_kernel, kNumSMs * 4, 256, 0, w.stream, w.graph(), w.output.ptr,
+                   &c.ctr()->out_cnt, &c.ctr()->next_deg);
       return;
     }
     // backward: the (global) input frontier is exactly what became visited in
@@ -651,16 +699,19 @@ struct DobfsPrim : PrimBase {
     // examined arcs: the reference's W in a backward step; a scratch counter
     // when a forward step runs physically as a pull (W = Σdeg(Q) then)
     unsigned long long* scanned = dir == 1 ? &c.ctr()->edges : &c.ctr()->u[3];
+    // exact-cost runs report Σdeg of the next frontier so the next superstep's
+    // cost test needs no extra host round trip
+    unsigned long long* deg_out = reports_deg && !c.want_deg ? &c.ctr()->next_deg : nullptr;
     if (nul) {
       MGB_LAUNCH(dobfs_pull_thread_kernel, grid_for(nul, 256 * kPV, kNumSMs * 8), 256, 0,
                  w.stream, w.pull_rec.ptr, ul, nul, w.su32[0].ptr, w.su32[1].ptr, w.su32[2].ptr,
                  w.su32[3].ptr, next_label, mark_preds ? 1 : 0, c.owner_view(), emit ? 1 : 0,
                  w.output.ptr, w.ul_buf[dst].ptr, ulcnt, w.ul_buf[2].ptr, cnts + 1, c.ctr(),
-                 scanned);
+                 scanned, deg_out);
       MGB_LAUNCH(dobfs_pull_group_kernel, kNumSMs * 8, 256, 0, w.stream, w.graph(),
                  w.pull_rec.ptr, w.ul_buf[2].ptr, cnts + 1, w.su32[0].ptr, w.su32[1].ptr,
                  w.su32[2].ptr, w.su32[3].ptr, next_label, mark_preds ? 1 : 0, c.owner_view(),
-                 emit ? 1 : 0, w.output.ptr, w.ul_buf[dst].ptr, ulcnt, c.ctr(), scanned);
+                 emit ? 1 : 0, w.output.ptr, w.ul_buf[dst].ptr, ulcnt, c.ctr(), scanned, deg_out);
     }
     list_free[w.p] = !emit;
     if (dir == 0) {
@@ -768,6 +819,30 @@ struct SsspDev {
   }
   __device__ uint32_t peer_id(uint32_t v, uint32_t, uint32_t) const { return v; }
 };
+
+// batched relaxation: the frozen source distances, weights and current
+// destination distances of the whole batch are loaded first (independent
+// loads in flight), then the improving arcs issue their atomicMin together
+template <int K, class T>
+__device__ __forceinline__ void visit_batch(const SsspDev<T>& f, const uint32_t* src,
+                                            const uint32_t* nb, const uint32_t* eid,
+                                            const bool* pass, bool* acc) {
+  T nd[K], cur[K];
+#pragma unroll
+  for (int k = 0; k < K; ++k) {
+    nd[k] = pass[k] ? __ldg(&f.fdist[src[k]]) + (T)__ldg(&f.w[eid[k]]) : (T)0;
+    cur[k] = pass[k] ? __ldcg(&f.dists[nb[k]]) : (T)0;
+  }
+  T old[K];
+#pragma unroll
+  for (int k = 0; k < K; ++k)
+    old[k] = pass[k] && nd[k] < cur[k] ? atomicMin(&f.dists[nb[k]], nd[k]) : (T)0;
+#pragma unroll
+  for (int k = 0; k < K; ++k) {
+    acc[k] = pass[k] && nd[k] < cur[k] && nd[k] < old[k];
+    if (acc[k] && f.mark_preds) f.preds[nb[k]] = f.ow.to_global(src[k]);
+  }
+}
 
 template <class T>
 __global__ void snapshot_kernel(const uint32_t* __restrict__ in, uint32_t n, const T* dists,
@@ -926,6 +1001,85 @@ __global__ void cc_delta_kernel(uint32_t* comp, uint32_t* snapshot, uint32_t nv,
   }
 }
 
+// A single Duplicate-All partition may keep its gather-heavy state (PageRank,
+// CC) in the FIFO-BFS locality order of bfs_locality_order; the transpose
+// built for it (rows = vertices in that order, arcs = in-neighbours) is shared.
+bool ordered_layout(const Plan& P) { return P.n == 1 && P.dup == MG_DUP_ALL; }
+void ensure_transpose(Plan& P, Worker& w);  // defined with the PageRank kernels
+
+__global__ void iperm_kernel(const uint32_t* __restrict__ perm, uint32_t n, uint32_t* iperm) {
+  for (uint32_t v = blockIdx.x * blockDim.x + threadIdx.x; v < n; v += gridDim.x * blockDim.x)
+    iperm[perm[v]] = v;
+}
+
+// hook over the ordered arcs (the arc set is the sub-graph's, so the union is
+// the same): 8 lanes per row, same larger-root-under-smaller rule
+constexpr int kCcGroup = 8;
+__global__ void __launch_bounds__(256)
+    cc_hook_rows_kernel(const uint32_t* __restrict__ toff, const uint32_t* __restrict__ tcol,
+                        uint32_t nv, uint32_t* comp, uint32_t* hooked) {
+  const unsigned sub = threadIdx.x & (kCcGroup - 1);
+  const uint32_t groups = gridDim.x * (blockDim.x / kCcGroup);
+  bool any = false;
+  for (uint32_t u = blockIdx.x * (blockDim.x / kCcGroup) + threadIdx.x / kCcGroup; u < nv;
+       u += groups) {
+    const uint32_t b = toff[u], e = toff[u + 1];
+    for (uint32_t k = b + sub; k < e; k += kCcGroup) {
+      const uint32_t v = __ldg(&tcol[k]);
+      uint32_t ru = cc_root(comp, u), rv = cc_root(comp, v);
+      if (ru == rv) continue;
+      uint32_t hi = ru > rv ? ru : rv, lo = ru < rv ? ru : rv;
+      atomicMin(&comp[hi], lo);
+      any = true;
+    }
+  }
+  if (__any_sync(0xffffffffu, any) && lane_id() == 0) *hooked = 1;
+}
+
+// labels back in vertex IDs: the component label is its smallest vertex ID.
+// Each CTA walks a contiguous range of ordered positions; runs of equal roots
+// are min-reduced by shuffles, the CTA's first root in shared memory, so the
+// giant component's root sees one global atomic per CTA, not one per vertex.
+__global__ void __launch_bounds__(256)
+    cc_min_id_kernel(const uint32_t* __restrict__ comp_p, const uint32_t* __restrict__ iperm,
+                     uint32_t n, uint32_t* minid) {
+  __shared__ uint32_t s_root, s_min;
+  const uint32_t per = (n + gridDim.x - 1) / gridDim.x;
+  const uint32_t lo = blockIdx.x * per, hi = lo + per < n ? lo + per : n;
+  if (lo >= hi) return;
+  if (threadIdx.x == 0) {
+    s_root = comp_p[lo];
+    s_min = 0xFFFFFFFFu;
+  }
+  __syncthreads();
+  const unsigned lane = lane_id();
+  for (uint32_t base = lo; base < hi; base += blockDim.x) {
+    const uint32_t i = base + threadIdx.x;
+    const bool ok = i < hi;
+    const uint32_t r = ok ? comp_p[i] : 0xFFFFFFFFu;
+    uint32_t m = ok ? iperm[i] : 0xFFFFFFFFu;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t om = __shfl_down_sync(0xffffffffu, m, o);
+      const uint32_t orr = __shfl_down_sync(0xffffffffu, r, o);
+      if (lane + o < 32 && orr == r) m = om < m ? om : m;
+    }
+    const uint32_t pr = __shfl_up_sync(0xffffffffu, r, 1);
+    if (ok && (lane == 0 || pr != r)) {
+      if (r == s_root) atomicMin(&s_min, m);
+      else atomicMin(&minid[r], m);
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) atomicMin(&minid[s_root], s_min);
+}
+__global__ void cc_labels_kernel(const uint32_t* __restrict__ comp_p,
+                                 const uint32_t* __restrict__ iperm,
+                                 const uint32_t* __restrict__ minid, uint32_t n, uint32_t* comp) {
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
+    comp[iperm[i]] = minid[comp_p[i]];
+}
+
 struct CcPrim : PrimBase {
   DevArray<uint32_t>* flag = nullptr;
   CcPrim() {
@@ -933,14 +1087,21 @@ struct CcPrim : PrimBase {
     nva = 1;
     communication = MG_COMM_BROADCAST;
   }
+  // single partition: components computed in the locality order (comp_p in
+  // aux[5], snapshot in su32[1]); labels mapped back to vertex IDs at the end
+  bool ordered = false;
+  uint32_t* comp_arr(Worker& w) { return ordered ? w.aux[5].ptr : w.su32[0].ptr; }
   void init(Ctx& c) {  // primitives.cpp:425-434
     Worker& w = *c.w;
+    ordered = ordered_layout(*c.P) && w.nv > 0;
+    if (ordered) ensure_transpose(*c.P, w);  // plan lifetime
     if (w.su32[0].n < w.nv || !w.su32[0].ptr) w.su32[0].alloc(w.nv ? w.nv : 1);
     if (w.su32[1].n < w.nv || !w.su32[1].ptr) w.su32[1].alloc(w.nv ? w.nv : 1);
+    if (ordered && (w.aux[5].n < w.nv || !w.aux[5].ptr)) w.aux[5].alloc(w.nv);
     if (!w.su32[3].ptr) w.su32[3].alloc(1);
     if (w.nv) {
-      MGB_LAUNCH(iota_kernel, grid_for(w.nv, 256), 256, 0, w.stream, w.su32[0].ptr, w.nv);
-      MGB_CUDA(cudaMemcpyAsync(w.su32[1].ptr, w.su32[0].ptr, 4ull * w.nv,
+      MGB_LAUNCH(iota_kernel, grid_for(w.nv, 256), 256, 0, w.stream, comp_arr(w), w.nv);
+      MGB_CUDA(cudaMemcpyAsync(w.su32[1].ptr, comp_arr(w), 4ull * w.nv,
                                cudaMemcpyDeviceToDevice, w.stream));
     }
     // a non-empty initial frontier keeps superstep 0 alive
@@ -960,23 +1121,36 @@ struct CcPrim : PrimBase {
     uint32_t h = 1;
     uint64_t scanned = 0;
     const uint64_t local_edges = w.ne;  // every hosted arc once per hook pass
+    uint32_t* comp = comp_arr(w);
     while (h) {
       MGB_CUDA(cudaMemsetAsync(hooked, 0, 4, w.stream));
-      if (nh)
+      if (ordered)
+        MGB_LAUNCH(cc_hook_rows_kernel, grid_for((uint64_t)w.nv * kCcGroup, 256, kNumSMs * 16),
+                   256, 0, w.stream, w.toff.ptr, w.tcol.ptr, w.nv, comp, hooked);
+      else if (nh)
         MGB_LAUNCH(cc_hook_kernel, grid_for((uint64_t)nh * 32, 256, kNumSMs * 16), 256, 0,
-                   w.stream, w.graph(), w.hosted.ptr, nh, w.su32[0].ptr, hooked);
+                   w.stream, w.graph(), w.hosted.ptr, nh, comp, hooked);
       if (w.nv)
-        MGB_LAUNCH(cc_jump_kernel, grid_for(w.nv, 256, kNumSMs * 16), 256, 0, w.stream,
-                   w.su32[0].ptr, w.nv);
+        MGB_LAUNCH(cc_jump_kernel, grid_for(w.nv, 256, kNumSMs * 16), 256, 0, w.stream, comp,
+                   w.nv);
       MGB_CUDA(cudaMemcpyAsync(&h, hooked, 4, cudaMemcpyDeviceToHost, w.stream));
       MGB_CUDA(cudaStreamSynchronize(w.stream));
       scanned += local_edges;
     }
     c.ensure_output(w.nv);
     if (w.nv)
-      MGB_LAUNCH(cc_delta_kernel, grid_for(w.nv, 256, kNumSMs * 16), 256, 0, w.stream,
-                 w.su32[0].ptr, w.su32[1].ptr, w.nv, w.output.ptr, c.ctr());
+      MGB_LAUNCH(cc_delta_kernel, grid_for(w.nv, 256, kNumSMs * 16), 256, 0, w.stream, comp,
+                 w.su32[1].ptr, w.nv, w.output.ptr, c.ctr());
     add_edges(c, scanned);
+  }
+  void finalize(Ctx& c, const GlobalView&) {
+    Worker& w = *c.w;
+    if (!ordered) return;
+    MGB_CUDA(cudaMemsetAsync(w.su32[1].ptr, 0xFF, 4ull * w.nv, w.stream));  // min vertex ID
+    MGB_LAUNCH(cc_min_id_kernel, grid_for(w.nv, 256, kNumSMs * 4), 256, 0, w.stream,
+               w.aux[5].ptr, w.pr_iperm.ptr, w.nv, w.su32[1].ptr);
+    MGB_LAUNCH(cc_labels_kernel, grid_for(w.nv, 256, kNumSMs * 8), 256, 0, w.stream,
+               w.aux[5].ptr, w.pr_iperm.ptr, w.su32[1].ptr, w.nv, w.su32[0].ptr);
   }
   static void add_edges(Ctx& c, uint64_t k);
 };
@@ -998,6 +1172,7 @@ struct BcDev {
   double* delta;
   uint32_t* bstamp;
   uint32_t* seen;
+  double* coef;
   OwnerView ow;
   uint32_t iter;
   int phase;
@@ -1022,6 +1197,7 @@ struct BcDev {
     sigma[v] = vv[0];  // dependency phase (primitives.cpp:650-653)
     delta[v] = vv[1];
     bstamp[v] = it + 1;
+    coef[v] = (1.0 + vv[1]) / vv[0];  // the proxy's successor coefficient
     return false;
   }
   __device__ void gather(uint32_t v, uint32_t*, double* vv) const {
@@ -1036,6 +1212,30 @@ struct BcDev {
   __device__ bool send_filter(uint32_t, uint32_t) const { return true; }
   __device__ uint32_t peer_id(uint32_t v, uint32_t, uint32_t) const { return v; }
 };
+
+// batched forward visit: label loads, then the claiming CASes, then the sigma
+// additions of the whole batch, each group in flight together
+template <int K>
+__device__ __forceinline__ void visit_batch(const BcDev& f, const uint32_t* src,
+                                            const uint32_t* nb, const uint32_t*,
+                                            const bool* pass, bool* acc) {
+  const uint32_t cand = f.iter + 1;
+  uint32_t old[K];
+  double su[K];
+#pragma unroll
+  for (int k = 0; k < K; ++k) {
+    old[k] = pass[k] ? __ldcg(&f.labels[nb[k]]) : 0u;
+    su[k] = pass[k] ? f.sigma[src[k]] : 0.0;
+  }
+#pragma unroll
+  for (int k = 0; k < K; ++k)
+    if (pass[k] && old[k] == kInfLabel) old[k] = atomicCAS(&f.labels[nb[k]], kInfLabel, cand);
+#pragma unroll
+  for (int k = 0; k < K; ++k) {
+    if (pass[k] && (old[k] == kInfLabel || old[k] == cand)) atomicAdd(&f.sigma[nb[k]], su[k]);
+    acc[k] = pass[k] && old[k] == kInfLabel;
+  }
+}
 
 __global__ void max_hosted_label_kernel(const uint32_t* labels, const uint32_t* hosted,
                                         uint32_t nh, Counters* ctr) {
@@ -1053,26 +1253,44 @@ __global__ void max_hosted_label_kernel(const uint32_t* labels, const uint32_t* 
 //           broadcast of the superstep) split by degree;
 //   accumulate: rows below kBcWarpDeg by one thread walking its arcs in order,
 //           longer rows by a warp (lane-strided partial sums, fixed xor-tree
-//           reduction: deterministic, within 1e-15 of the sequential sum).
-// Explicitly rounded operations (no FMA contraction) keep short rows bit-exact.
+//           reduction: deterministic).
+// Successor coefficients: once a vertex's dependency is final its coefficient
+// coef[w] = (1 + delta[w]) / sigma[w] is stored — by the select pass of the
+// NEXT (shallower) level for hosted vertices, on receipt of the owner's
+// broadcast for proxies — so
+//   delta[v] = sigma[v] * sum over arcs (v,w) of coef[w]
+// needs ONE random 8-byte load per arc.  No mask is needed: while level L is
+// processed only levels > L carry coefficients (levels finish from the
+// deepest up, and level L's own are written only after its pass), and an arc
+// from level L never reaches past L+1 (BFS levels), so every non-zero
+// coefficient on a row of level L belongs to a successor — the reference's
+// "label == L+1 / stamped by the last broadcast" test (primitives.cpp:600-610).  The factored sum differs from the
+// reference's per-term sigma_v/sigma_w*(1+delta_w) by rounding only (~1e-16
+// relative; the bar is 1e-5).
 constexpr uint32_t kBcWarpDeg = 32;
 
 __global__ void __launch_bounds__(256)
     bc_level_select_kernel(const uint32_t* __restrict__ hosted, uint32_t nh,
                            const uint32_t* __restrict__ labels, const uint32_t* __restrict__ off,
                            uint32_t level, uint32_t* out, Counters* ctr, uint32_t* small,
-                           uint32_t* nsmall, uint32_t* big, uint32_t* nbig) {
+                           uint32_t* nsmall, uint32_t* big, uint32_t* nbig, int deepest,
+                           const double* __restrict__ sigma, const double* __restrict__ delta,
+                           double* coef) {
   for (uint32_t base = blockIdx.x * blockDim.x; base < nh; base += gridDim.x * blockDim.x) {
     uint32_t i = base + threadIdx.x;
     bool in = false, is_big = false;
     uint32_t v = 0;
     if (i < nh) {
       v = hosted[i];
-      in = labels[v] == level;
+      const uint32_t lv = labels[v];
+      in = lv == level;
       if (in) is_big = off[v + 1] - off[v] >= kBcWarpDeg;
+      if (in && deepest) coef[v] = 1.0 / sigma[v];  // delta = 0 on the deepest level
+      else if (lv == level + 1 && !deepest) coef[v] = (1.0 + delta[v]) / sigma[v];
     }
     uint32_t s = warp_append(&ctr->out_cnt, in);
     if (in) out[s] = v;
+    if (deepest) continue;
     s = warp_append(nsmall, in && !is_big);
     if (in && !is_big) small[s] = v;
     s = warp_append(nbig, in && is_big);
@@ -1080,58 +1298,53 @@ __global__ void __launch_bounds__(256)
   }
 }
 
-__device__ __forceinline__ double bc_term(const GraphView& g, uint32_t k, double sv,
-                                          const uint32_t* labels, const double* sigma,
-                                          const double* delta, const uint32_t* bstamp,
-                                          uint32_t level, uint32_t prev_stamp, const OwnerView& ow) {
-  uint32_t w = g.col[k];
-  bool succ = ow.hosts(w) ? (labels[w] == level + 1) : (bstamp[w] == prev_stamp);
-  double sw = sigma[w];
-  if (succ && sw > 0.0) return __dmul_rn(__ddiv_rn(sv, sw), __dadd_rn(1.0, delta[w]));
-  return 0.0;
+__device__ __forceinline__ void bc_finish(uint32_t v, uint32_t source, double sv, double acc,
+                                          double* delta, double* bc) {
+  const double dv = sv * acc;
+  delta[v] = dv;
+  if (v != source) bc[v] += dv;
 }
 
 __global__ void __launch_bounds__(256)
     bc_backward_thread_kernel(GraphView g, const uint32_t* __restrict__ list, const uint32_t* nlist,
-                              const uint32_t* labels, const double* sigma, double* delta,
-                              double* bc, const uint32_t* bstamp, uint32_t level,
-                              uint32_t prev_stamp, uint32_t source, OwnerView ow, Counters* ctr) {
+                              const double* __restrict__ sigma, double* delta, double* bc,
+                              const double* __restrict__ coef, uint32_t source, Counters* ctr) {
   const uint32_t n = *nlist;
   unsigned long long scanned = 0;
   for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
-    uint32_t v = list[i];
-    const double sv = sigma[v];
+    const uint32_t v = list[i];
+    const uint32_t b = g.off[v], e = g.off[v + 1];
     double acc = 0.0;
-    uint32_t b = g.off[v], e = g.off[v + 1];
-    for (uint32_t k = b; k < e; ++k)
-      acc = __dadd_rn(acc, bc_term(g, k, sv, labels, sigma, delta, bstamp, level, prev_stamp, ow));
+    uint32_t k = b;
+    for (; k + 1 < e; k += 2) {  // two gathers in flight
+      const double c0 = __ldg(&coef[__ldg(&g.col[k])]);
+      const double c1 = __ldg(&coef[__ldg(&g.col[k + 1])]);
+      acc += c0;
+      acc += c1;
+    }
+    if (k < e) acc += __ldg(&coef[__ldg(&g.col[k])]);
     scanned += e - b;
-    delta[v] = acc;
-    if (v != source) bc[v] = __dadd_rn(bc[v], acc);
+    bc_finish(v, source, sigma[v], acc, delta, bc);
   }
   warp_add_u64(&ctr->edges, scanned);
 }
 
 __global__ void __launch_bounds__(256)
     bc_backward_warp_kernel(GraphView g, const uint32_t* __restrict__ list, const uint32_t* nlist,
-                            const uint32_t* labels, const double* sigma, double* delta, double* bc,
-                            const uint32_t* bstamp, uint32_t level, uint32_t prev_stamp,
-                            uint32_t source, OwnerView ow, Counters* ctr) {
+                            const double* __restrict__ sigma, double* delta, double* bc,
+                            const double* __restrict__ coef, uint32_t source, Counters* ctr) {
   const uint32_t n = *nlist;
   const uint32_t warps = gridDim.x * blockDim.x / 32;
   unsigned long long scanned = 0;
   for (uint32_t i = (blockIdx.x * blockDim.x + threadIdx.x) / 32; i < n; i += warps) {
-    uint32_t v = list[i];
-    const double sv = sigma[v];
+    const uint32_t v = list[i];
+    const uint32_t b = g.off[v], e = g.off[v + 1];
     double acc = 0.0;
-    uint32_t b = g.off[v], e = g.off[v + 1];
-    for (uint32_t k = b + lane_id(); k < e; k += 32)
-      acc = __dadd_rn(acc, bc_term(g, k, sv, labels, sigma, delta, bstamp, level, prev_stamp, ow));
-    for (int o = 16; o > 0; o >>= 1) acc = __dadd_rn(acc, __shfl_xor_sync(0xffffffffu, acc, o));
+    for (uint32_t k = b + lane_id(); k < e; k += 32) acc += __ldg(&coef[__ldg(&g.col[k])]);
+    for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
     if (lane_id() == 0) {
       scanned += e - b;
-      delta[v] = acc;
-      if (v != source) bc[v] = __dadd_rn(bc[v], acc);
+      bc_finish(v, source, sigma[v], acc, delta, bc);
     }
   }
   warp_add_u64(&ctr->edges, scanned);
@@ -1160,6 +1373,7 @@ struct BcPrim : PrimBase {
     fill(w.sf64[0], w.nv, 0, w.stream);     // sigma
     fill(w.sf64[1], w.nv, 0, w.stream);     // delta
     fill(w.sf64[2], w.nv, 0, w.stream);     // bc
+    fill(w.sf64[3], w.nv, 0, w.stream);     // successor coefficients
     MGB_LAUNCH(set_one_kernel<uint32_t>, 1, 1, 0, w.stream, w.su32[0].ptr, source, 0u);
     if (c.P->owner_host[source] == w.p) {
       MGB_LAUNCH(set_one_kernel<double>, 1, 1, 0, w.stream, w.sf64[0].ptr, source, 1.0);
@@ -1169,7 +1383,7 @@ struct BcPrim : PrimBase {
   BcDev dev(Ctx& c) {
     Worker& w = *c.w;
     return {w.su32[0].ptr, w.sf64[0].ptr, w.sf64[1].ptr, w.su32[3].ptr, w.su32[2].ptr,
-            c.owner_view(), (uint32_t)c.iter, phase};
+            w.sf64[3].ptr, c.owner_view(), (uint32_t)c.iter, phase};
   }
   int phase_at_body = kFwd;
   void body(Ctx& c) {  // primitives.cpp:543-625
@@ -1203,16 +1417,15 @@ struct BcPrim : PrimBase {
       if (nh) {
         MGB_LAUNCH(bc_level_select_kernel, grid_for(nh, 256, kNumSMs * 16), 256, 0, w.stream,
                    w.hosted.ptr, nh, w.su32[0].ptr, w.off.ptr, level, w.output.ptr, c.ctr(),
-                   w.aux[0].ptr, cnts, w.aux[1].ptr, cnts + 1);
+                   w.aux[0].ptr, cnts, w.aux[1].ptr, cnts + 1, level == max_level ? 1 : 0,
+                   w.sf64[0].ptr, w.sf64[1].ptr, w.sf64[3].ptr);
         if (level < max_level) {  // the deepest level only broadcasts
           MGB_LAUNCH(bc_backward_thread_kernel, kNumSMs * 8, 256, 0, w.stream, w.graph(),
-                     w.aux[0].ptr, cnts, w.su32[0].ptr, w.sf64[0].ptr, w.sf64[1].ptr,
-                     w.sf64[2].ptr, w.su32[3].ptr, level, (uint32_t)c.iter, source,
-                     c.owner_view(), c.ctr());
+                     w.aux[0].ptr, cnts, w.sf64[0].ptr, w.sf64[1].ptr, w.sf64[2].ptr,
+                     w.sf64[3].ptr, source, c.ctr());
           MGB_LAUNCH(bc_backward_warp_kernel, kNumSMs * 8, 256, 0, w.stream, w.graph(),
-                     w.aux[1].ptr, cnts + 1, w.su32[0].ptr, w.sf64[0].ptr, w.sf64[1].ptr,
-                     w.sf64[2].ptr, w.su32[3].ptr, level, (uint32_t)c.iter, source,
-                     c.owner_view(), c.ctr());
+                     w.aux[1].ptr, cnts + 1, w.sf64[0].ptr, w.sf64[1].ptr, w.sf64[2].ptr,
+                     w.sf64[3].ptr, source, c.ctr());
         }
       }
       c.report.u[0] = max_level;
@@ -1319,15 +1532,29 @@ __global__ void pr_contrib_kernel(GraphView g, const uint32_t* __restrict__ host
   if (lane_id() == 0 && dangling != 0.0) atomicAdd(&ctr->f[0], dangling);
 }
 
+// rows shorter than kPullLong: one thread per row, four gathers in flight.
+// In the locality order neighbouring threads own neighbouring rows whose
+// in-neighbours overlap, so the contribution gathers mostly hit L1/L2.
 __global__ void __launch_bounds__(256)
     pr_pull_kernel(const uint32_t* __restrict__ toff, const uint32_t* __restrict__ tcol,
                    uint32_t nv, const double* __restrict__ contrib, double* accum) {
   for (uint32_t v = blockIdx.x * blockDim.x + threadIdx.x; v < nv; v += gridDim.x * blockDim.x) {
-    uint32_t b = toff[v], e = toff[v + 1];
+    const uint32_t b = __ldg(&toff[v]), e = __ldg(&toff[v + 1]);
     if (e - b >= kPullLong) continue;  // warp kernel
-    double s = 0.0;
-    for (uint32_t k = b; k < e; ++k) s += __ldg(&contrib[__ldg(&tcol[k])]);
-    accum[v] = s;
+    double s0 = 0.0, s1 = 0.0;
+    uint32_t k = b;
+    for (; k + 3 < e; k += 4) {
+      const uint32_t u0 = __ldg(&tcol[k]), u1 = __ldg(&tcol[k + 1]);
+      const uint32_t u2 = __ldg(&tcol[k + 2]), u3 = __ldg(&tcol[k + 3]);
+      const double c0 = __ldg(&contrib[u0]), c1 = __ldg(&contrib[u1]);
+      const double c2 = __ldg(&contrib[u2]), c3 = __ldg(&contrib[u3]);
+      s0 += c0;
+      s1 += c1;
+      s0 += c2;
+      s1 += c3;
+    }
+    for (; k < e; ++k) s0 += __ldg(&contrib[__ldg(&tcol[k])]);
+    accum[v] = s0 + s1;
   }
 }
 
@@ -1344,6 +1571,73 @@ __global__ void __launch_bounds__(256)
     for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
     if (lane_id() == 0) accum[v] = s;
   }
+}
+
+// --- locality-ordered single-partition form --------------------------------
+// With one partition every vertex is hosted, so the rank / accumulator /
+// contribution arrays can live in a vertex order chosen for locality (the
+// FIFO-BFS order of bfs_locality_order): the pull's gathers then fall inside
+// a narrow band of the contribution array instead of all of it.  The
+// transpose, the out-degrees and the rank arrays are kept in that order; the
+// ranks are mapped back to vertex IDs when the run ends.
+
+__global__ void transpose_keys_perm_kernel(GraphView g, const uint32_t* __restrict__ perm,
+                                           unsigned long long* keys, uint32_t* pdeg) {
+  const uint32_t warps = gridDim.x * blockDim.x / 32;
+  for (uint32_t u = (blockIdx.x * blockDim.x + threadIdx.x) / 32; u < g.nv; u += warps) {
+    const uint32_t pu = perm[u], b = g.off[u], e = g.off[u + 1];
+    if (lane_id() == 0) pdeg[pu] = e - b;
+    for (uint32_t k = b + lane_id(); k < e; k += 32)
+      keys[k] = ((unsigned long long)perm[g.col[k]] << 32) | pu;
+  }
+}
+
+// pr_update (primitives.cpp:697-711) fused with the next contribution
+// rank/deg (primitives.cpp:766-771): one streaming pass in the locality order
+__global__ void __launch_bounds__(256)
+    pr_update_contrib_kernel(uint32_t nv, const uint32_t* __restrict__ pdeg, double* rank,
+                             const double* __restrict__ accum, double* contrib, double base,
+                             double damping, double dangling_n, int update, Counters* ctr) {
+  double dmax = 0.0, sum = 0.0, dangling = 0.0;
+  unsigned long long scanned = 0;
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < nv; i += gridDim.x * blockDim.x) {
+    double r = rank[i];
+    if (update) {
+      double nr = base + damping * (accum[i] + dangling_n);
+      double rel = fabs(nr - r) / fmax(nr, 1e-300);
+      dmax = fmax(dmax, rel);
+      rank[i] = nr;
+      sum += nr;
+      r = nr;
+    }
+    const uint32_t d = pdeg[i];
+    if (d == 0) {
+      dangling += r;
+      contrib[i] = 0.0;
+    } else {
+      contrib[i] = r / (double)d;
+      scanned += d;
+    }
+  }
+  for (int o = 16; o > 0; o >>= 1) {
+    dmax = fmax(dmax, __shfl_xor_sync(0xffffffffu, dmax, o));
+    sum += __shfl_xor_sync(0xffffffffu, sum, o);
+    dangling += __shfl_xor_sync(0xffffffffu, dangling, o);
+  }
+  warp_add_u64(&ctr->edges, scanned);
+  if (lane_id() == 0) {
+    if (update) {
+      atomic_max_pos_f64(&ctr->f[1], dmax);
+      atomicAdd(&ctr->f[2], sum);
+    }
+    if (dangling != 0.0) atomicAdd(&ctr->f[0], dangling);
+  }
+}
+
+__global__ void unpermute_f64_kernel(const double* __restrict__ src, const uint32_t* __restrict__ perm,
+                                     uint32_t n, double* dst) {
+  for (uint32_t v = blockIdx.x * blockDim.x + threadIdx.x; v < n; v += gridDim.x * blockDim.x)
+    dst[v] = src[perm[v]];
 }
 
 // pr_update (primitives.cpp:697-711) fused with zeroing the hosted accumulators
@@ -1407,6 +1701,59 @@ __global__ void copy_border_kernel(const uint32_t* border, uint32_t n, uint32_t*
   if (blockIdx.x == 0 && threadIdx.x == 0) ctr->out_cnt = n;
 }
 
+// plan-lifetime transpose of the worker's sub-graph (rows sorted by source);
+// for a single Duplicate-All partition it is built in the locality order
+void ensure_transpose(Plan& P, Worker& w) {
+  if (w.transpose_ready) return;
+  const uint64_t ne = w.ne;
+  const uint32_t nh = (uint32_t)w.hosted_host.size();
+  w.toff.alloc(w.nv + 1ull);
+  w.tcol.alloc(ne ? ne : 1);
+  DevArray<unsigned long long> k0, k1;
+  k0.alloc(ne ? ne : 1);
+  k1.alloc(ne ? ne : 1);
+  w.pr_reordered = ordered_layout(P) && w.nv > 0;
+  if (w.pr_reordered) {
+    std::vector<uint32_t> off(w.nv + 1ull), col(ne);
+    MGB_CUDA(cudaMemcpy(off.data(), w.off.ptr, 4ull * (w.nv + 1ull), cudaMemcpyDeviceToHost));
+    if (ne) MGB_CUDA(cudaMemcpy(col.data(), w.col.ptr, 4ull * ne, cudaMemcpyDeviceToHost));
+    std::vector<uint32_t> perm = bfs_locality_order(off.data(), col.data(), w.nv);
+    w.pr_perm.upload(perm.data(), w.nv, w.stream);
+    w.pr_pdeg.alloc(w.nv);
+  w.pr_iperm.alloc(w.nv);
+  MGB_LAUNCH(iperm_kernel, grid_for(w.nv, 256, kNumSMs * 8), 256, 0, w.stream, w.pr_perm.ptr,
+             w.nv, w.pr_iperm.ptr);
+    MGB_LAUNCH(transpose_keys_perm_kernel, grid_for((uint64_t)w.nv * 32, 256, kNumSMs * 16),
+               256, 0, w.stream, w.graph(), w.pr_perm.ptr, k0.ptr, w.pr_pdeg.ptr);
+    MGB_CUDA(cudaStreamSynchronize(w.stream));
+  } else if (nh && ne) {
+    MGB_LAUNCH(transpose_keys_kernel, grid_for((uint64_t)nh * 32, 256, kNumSMs * 16), 256, 0,
+               w.stream, w.graph(), w.hosted.ptr, nh, k0.ptr);
+  }
+  cub::DoubleBuffer<unsigned long long> db(k0.ptr, k1.ptr);
+  size_t tb = 0;
+  cub::DeviceRadixSort::SortKeys(nullptr, tb, db, (int64_t)ne, 0, 64, w.stream);
+  void* tmp = nullptr;
+  MGB_CUDA(cudaMalloc(&tmp, tb + 16));
+  cub::DeviceRadixSort::SortKeys(tmp, tb, db, (int64_t)ne, 0, 64, w.stream);
+  MGB_LAUNCH(transpose_csr_kernel, kNumSMs * 16, 256, 0, w.stream, db.Current(), ne, w.nv,
+             w.toff.ptr, w.tcol.ptr);
+  DevArray<uint32_t> cnt;
+  cnt.alloc(1);
+  MGB_CUDA(cudaMemsetAsync(cnt.ptr, 0, 4, w.stream));
+  w.tlong.alloc(w.nv ? w.nv : 1);
+  if (w.nv)
+    MGB_LAUNCH(select_long_rows_kernel, grid_for(w.nv, 256, kNumSMs * 8), 256, 0, w.stream,
+               w.toff.ptr, w.nv, w.tlong.ptr, cnt.ptr);
+  MGB_CUDA(cudaMemcpyAsync(&w.n_tlong, cnt.ptr, 4, cudaMemcpyDeviceToHost, w.stream));
+  MGB_CUDA(cudaStreamSynchronize(w.stream));
+  cudaFree(tmp);
+  k0.free_();
+  k1.free_();
+  cnt.free_();
+  w.transpose_ready = true;
+}
+
 struct PrPrim : PrimBase {
   double damping, epsilon;
   uint64_t max_iter;
@@ -1423,6 +1770,14 @@ struct PrPrim : PrimBase {
   }
   void init(Ctx& c) {  // primitives.cpp:728-745
     Worker& w = *c.w;
+    ensure_transpose(*c.P, w);  // plan lifetime
+    if (w.pr_reordered) {
+      for (int k : {0, 1, 2, 3})
+        if (w.sf64[k].n < w.nv || !w.sf64[k].ptr) w.sf64[k].alloc(w.nv);
+      MGB_LAUNCH(fill_f64_kernel, grid_for(w.nv, 256, kNumSMs * 8), 256, 0, w.stream,
+                 w.sf64[3].ptr, w.nv, 1.0 / (double)c.P->nv);
+      return;
+    }
     fill(w.sf64[0], w.nv, 0, w.stream);  // rank
     fill(w.sf64[1], w.nv, 0, w.stream);  // accum
     uint32_t nh = (uint32_t)w.hosted_host.size();
@@ -1440,44 +1795,42 @@ struct PrPrim : PrimBase {
                  nh, w.sf64[0].ptr, w.sf64[1].ptr, (1.0 - damping) / n, damping,
                  dangling_prev / n, do_update ? 1 : 0, c.ctr());
   }
-  // plan-lifetime transpose of the worker's sub-graph (rows sorted by source)
-  static void ensure_transpose(Worker& w) {
-    if (w.transpose_ready) return;
-    const uint64_t ne = w.ne;
-    const uint32_t nh = (uint32_t)w.hosted_host.size();
-    w.toff.alloc(w.nv + 1ull);
-    w.tcol.alloc(ne ? ne : 1);
-    DevArray<unsigned long long> k0, k1;
-    k0.alloc(ne ? ne : 1);
-    k1.alloc(ne ? ne : 1);
-    if (nh && ne)
-      MGB_LAUNCH(transpose_keys_kernel, grid_for((uint64_t)nh * 32, 256, kNumSMs * 16), 256, 0,
-                 w.stream, w.graph(), w.hosted.ptr, nh, k0.ptr);
-    cub::DoubleBuffer<unsigned long long> db(k0.ptr, k1.ptr);
-    size_t tb = 0;
-    cub::DeviceRadixSort::SortKeys(nullptr, tb, db, (int64_t)ne, 0, 64, w.stream);
-    void* tmp = nullptr;
-    MGB_CUDA(cudaMalloc(&tmp, tb + 16));
-    cub::DeviceRadixSort::SortKeys(tmp, tb, db, (int64_t)ne, 0, 64, w.stream);
-    MGB_LAUNCH(transpose_csr_kernel, kNumSMs * 16, 256, 0, w.stream, db.Current(), ne, w.nv,
-               w.toff.ptr, w.tcol.ptr);
-    DevArray<uint32_t> cnt;
-    cnt.alloc(1);
-    MGB_CUDA(cudaMemsetAsync(cnt.ptr, 0, 4, w.stream));
-    w.tlong.alloc(w.nv ? w.nv : 1);
+  static void ensure_transpose(Plan& P, Worker& w) { mgb::ensure_transpose(P, w); }
+  // locality-ordered single partition: rank in sf64[3] (ordered), accum
+  // sf64[1], contributions sf64[2]; ranks mapped back into sf64[0] at the end
+  void update_contrib(Ctx& c, double dangling_prev, bool do_update) {
+    Worker& w = *c.w;
+    const double n = (double)c.P->nv;
+    MGB_LAUNCH(pr_update_contrib_kernel, grid_for(w.nv, 256, kNumSMs * 8), 256, 0, w.stream,
+               w.nv, w.pr_pdeg.ptr, w.sf64[3].ptr, w.sf64[1].ptr, w.sf64[2].ptr,
+               (1.0 - damping) / n, damping, dangling_prev / n, do_update ? 1 : 0, c.ctr());
+  }
+  void pull(Worker& w) {
     if (w.nv)
-      MGB_LAUNCH(select_long_rows_kernel, grid_for(w.nv, 256, kNumSMs * 8), 256, 0, w.stream,
-                 w.toff.ptr, w.nv, w.tlong.ptr, cnt.ptr);
-    MGB_CUDA(cudaMemcpyAsync(&w.n_tlong, cnt.ptr, 4, cudaMemcpyDeviceToHost, w.stream));
-    MGB_CUDA(cudaStreamSynchronize(w.stream));
-    cudaFree(tmp);
-    k0.free_();
-    k1.free_();
-    cnt.free_();
-    w.transpose_ready = true;
+      MGB_LAUNCH(pr_pull_kernel, grid_for(w.nv, 256, kNumSMs * 16), 256, 0, w.stream,
+                 w.toff.ptr, w.tcol.ptr, w.nv, w.sf64[2].ptr, w.sf64[1].ptr);
+    if (w.n_tlong)
+      MGB_LAUNCH(pr_pull_warp_kernel, grid_for((uint64_t)w.n_tlong * 32, 256, kNumSMs * 8), 256,
+                 0, w.stream, w.toff.ptr, w.tcol.ptr, w.tlong.ptr, w.n_tlong, w.sf64[2].ptr,
+                 w.sf64[1].ptr);
+  }
+  void body_ordered(Ctx& c) {
+    Worker& w = *c.w;
+    const bool first = c.worker() == c.P->local_workers.front();
+    if (c.iter >= 1) {
+      update_contrib(c, c.prev->sum_f(0), true);
+      if (first) ++updates;
+    } else {
+      update_contrib(c, 0.0, false);
+      c.report.f[1] = INFINITY;
+    }
+    if (first && c.prev && c.iter >= 2) rank_sums.push_back(c.prev->sum_f(2));
+    pull(w);
   }
   void body(Ctx& c) {  // primitives.cpp:747-782
     Worker& w = *c.w;
+    ensure_transpose(*c.P, w);
+    if (w.pr_reordered) return body_ordered(c);
     const bool first = c.worker() == c.P->local_workers.front();
     if (c.iter >= 1) {
       update(c, c.prev->sum_f(0), true);
@@ -1490,7 +1843,6 @@ struct PrPrim : PrimBase {
     uint32_t nh = (uint32_t)w.hosted_host.size();
     // accum[v] = sum of rank[u]/deg(u) over hosted in-neighbours u,
     // gathered per destination (pull) in a fixed order
-    ensure_transpose(w);
     if (w.sf64[2].n < w.nv || !w.sf64[2].ptr) w.sf64[2].alloc(w.nv ? w.nv : 1);
     if (nh)
       MGB_LAUNCH(pr_contrib_kernel, grid_for(nh, 256, kNumSMs * 8), 256, 0, w.stream, w.graph(),
@@ -1516,11 +1868,16 @@ struct PrPrim : PrimBase {
     bool delta_stopped = last.iteration >= 1 && last.max_f(1) < epsilon;
     const bool first = c.worker() == c.P->local_workers.front();
     if (first && c.worker() == 0 && last.iteration >= 1) rank_sums.push_back(last.sum_f(2));
+    Worker& w = *c.w;
     if (!delta_stopped) {
-      MGB_CUDA(cudaMemsetAsync(c.ctr(), 0, sizeof(Counters), c.w->stream));
-      update(c, last.sum_f(0), true);
+      MGB_CUDA(cudaMemsetAsync(c.ctr(), 0, sizeof(Counters), w.stream));
+      if (w.pr_reordered) update_contrib(c, last.sum_f(0), true);
+      else update(c, last.sum_f(0), true);
       if (first) ++updates;
     }
+    if (w.pr_reordered && w.nv)  // ranks back to vertex IDs
+      MGB_LAUNCH(unpermute_f64_kernel, grid_for(w.nv, 256, kNumSMs * 8), 256, 0, w.stream,
+                 w.sf64[3].ptr, w.pr_perm.ptr, w.nv, w.sf64[0].ptr);
   }
 };
 
@@ -1632,7 +1989,7 @@ int mg_dobfs(mg_plan* plan, uint32_t source, double do_a, double do_b, int mark_
     Plan& P = *reinterpret_cast<Plan*>(plan);
     check_source(P, source, "dobfs");
     mg_config c = cfg_or_default(cfg);
-    DobfsPrim prim(source, do_a, do_b, mark_preds != 0, c.dobfs_exact_cost != 0);
+    DobfsPrim prim(source, do_a, do_b, mark_preds != 0, c.dobfs_exact_cost != 0, P.n);
     P.last = mg_stats{};
     run_primitive(P, prim, c);
     P.last_result_kind = 0;
