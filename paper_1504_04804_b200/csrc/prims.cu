@@ -213,9 +213,16 @@ __device__ __forceinline__ void visit_batch(const DobfsDev& f, const uint32_t* s
   }
 }
 
-// fb = vis & ~prev (the level just discovered); prev = vis
+// fb = vis & ~prev (the level just discovered); prev = vis.  Thread 0 also
+// resets the pull step's queue counters and stores the superstep's logical W
+// (forward superstep run as a pull), saving two tiny copies per pull step.
 __global__ void frontier_diff_kernel(const uint32_t* __restrict__ vis, uint32_t* prev,
-                                     uint32_t* __restrict__ fb, uint32_t nw) {
+                                     uint32_t* __restrict__ fb, uint32_t nw, uint32_t* zero2,
+                                     unsigned long long* w_dst, unsigned long long w_val) {
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    zero2[0] = zero2[1] = 0u;
+    if (w_dst) *w_dst = w_val;
+  }
   const uint4* v4 = reinterpret_cast<const uint4*>(vis);
   uint4* p4 = reinterpret_cast<uint4*>(prev);
   uint4* f4 = reinterpret_cast<uint4*>(fb);
@@ -677,15 +684,15 @@ struct DobfsPrim : PrimBase {
     // backward: the (global) input frontier is exactly what became visited in
     // the previous superstep, so its bitmap is vis & ~vis_prev — one streaming
     // pass over |V|/32 words instead of an atomic per frontier vertex
+    uint32_t* cnts = w.aux[2].ptr;     // [1] long-row queue length (zeroed below)
     MGB_LAUNCH(frontier_diff_kernel, grid_for(nw, 256, kNumSMs * 8), 256, 0, w.stream,
-               w.su32[2].ptr, w.aux[4].ptr, w.su32[3].ptr, (uint32_t)nw);
+               w.su32[2].ptr, w.aux[4].ptr, w.su32[3].ptr, (uint32_t)nw, cnts,
+               dir == 0 ? &c.ctr()->edges : nullptr, (unsigned long long)logical_w);
     const int src = ul_src[w.p];
     const uint32_t* ul = src < 0 ? nullptr : w.ul_buf[src].ptr;  // null: every record
     const int dst = src == 0 ? 1 : 0;
     const uint32_t nul = ul_len[w.p];
     uint32_t* ulcnt = &c.ctr()->misc;  // reported with the superstep's counters
-    uint32_t* cnts = w.aux[2].ptr;     // [1] long-row queue length
-    MGB_CUDA(cudaMemsetAsync(cnts, 0, 8, w.stream));
     // one partition under the max policy: discoveries are counted, not listed
     // (the next superstep rebuilds a list from the bitmap only if it pushes)
     const bool emit = c.P->n > 1 || c.want_deg;
@@ -714,10 +721,6 @@ struct DobfsPrim : PrimBase {
                  emit ? 1 : 0, w.output.ptr, w.ul_buf[dst].ptr, ulcnt, c.ctr(), scanned, deg_out);
     }
     list_free[w.p] = !emit;
-    if (dir == 0) {
-      unsigned long long lw = logical_w;  // pageable source: staged before return
-      MGB_CUDA(cudaMemcpyAsync(&c.ctr()->edges, &lw, 8, cudaMemcpyHostToDevice, w.stream));
-    }
     if (c.P->profile) {
       MGB_CUDA(cudaEventRecord(w.ev_k1, w.stream));
       prof_pending_[w.p] = true;
