@@ -197,6 +197,18 @@ static __global__ void degsum_dev_kernel(GraphView g, const uint32_t* __restrict
 
 constexpr uint64_t kUnknownDeg = ~0ull;
 
+// end of superstep: the counters go to the worker's mapped pinned page (one
+// small kernel instead of a D2H copy) and are cleared for the next superstep
+// (instead of a memset at its start)
+static __global__ void report_kernel(Counters* ctr, Counters* host) {
+  uint32_t* src = reinterpret_cast<uint32_t*>(ctr);
+  volatile uint32_t* dst = reinterpret_cast<volatile uint32_t*>(host);
+  for (uint32_t i = threadIdx.x; i < sizeof(Counters) / 4; i += blockDim.x) {
+    dst[i] = src[i];
+    src[i] = 0u;
+  }
+}
+
 // ---------------------------------------------------------------------------
 // per-(run, worker) context: the WorkerHandle of the reference (engine.hpp:478-582)
 
@@ -309,13 +321,25 @@ struct RunState {
   std::vector<cudaEvent_t> packed;  // per worker, recorded after publish
 };
 
+struct SmallList {
+  uint32_t n, v[8];
+};
+static __global__ void put_small_kernel(uint32_t* dst, SmallList l) {
+  if (threadIdx.x < l.n) dst[threadIdx.x] = l.v[threadIdx.x];
+}
+
 inline void Ctx::push_initial(const std::vector<uint32_t>& vs) {
   uint32_t& nc = run->next_count[w->p];
   w->next_input.ensure(nc + vs.size(), w->stream, nc);
-  if (!vs.empty())
+  if (vs.size() <= 8) {  // sources: by kernel argument, no host round trip
+    SmallList l{static_cast<uint32_t>(vs.size()), {}};
+    for (size_t i = 0; i < vs.size(); ++i) l.v[i] = vs[i];
+    if (!vs.empty()) MGB_LAUNCH(put_small_kernel, 1, 32, 0, w->stream, w->next_input.ptr + nc, l);
+  } else {
     MGB_CUDA(cudaMemcpyAsync(w->next_input.ptr + nc, vs.data(), vs.size() * 4,
                              cudaMemcpyHostToDevice, w->stream));
-  MGB_CUDA(cudaStreamSynchronize(w->stream));  // vs is a host temporary
+    MGB_CUDA(cudaStreamSynchronize(w->stream));  // vs is a host temporary
+  }
   nc += static_cast<uint32_t>(vs.size());
 }
 
@@ -417,16 +441,22 @@ void run_primitive(Plan& P, Prim& prim, const mg_config& cfg) {
     if (n > 1)
       MGB_CUDA(cudaMemsetAsync(w.merge_stamp.ptr, 0, sizeof(uint32_t) * w.nv, w.stream));
     prim.init(ctx[p]);
-    // advance bound of superstep 0
-    if (rs.next_count[p])
-      MGB_LAUNCH(degsum_kernel, grid_for(rs.next_count[p], 256, 1024), 256, 0, w.stream,
-                 w.graph(), w.next_input.ptr, rs.next_count[p], &w.ctr.ptr->next_deg);
-    MGB_CUDA(cudaMemcpyAsync(w.host_ctr, w.ctr.ptr, sizeof(Counters), cudaMemcpyDeviceToHost,
-                             w.stream));
+    // advance bound of superstep 0 (only tracked when the policy sizes buffers
+    // exactly; the max policy needs no host round trip before superstep 0)
+    if (want_deg) {
+      if (rs.next_count[p])
+        MGB_LAUNCH(degsum_kernel, grid_for(rs.next_count[p], 256, 1024), 256, 0, w.stream,
+                   w.graph(), w.next_input.ptr, rs.next_count[p], &w.ctr.ptr->next_deg);
+      MGB_LAUNCH(report_kernel, 1, 128, 0, w.stream, w.ctr.ptr, w.host_ctr_dev);
+    }
   }
   for (uint32_t p : P.local_workers) {
-    MGB_CUDA(cudaStreamSynchronize(P.workers[p]->stream));
-    rs.next_deg[p] = P.workers[p]->host_ctr->next_deg;
+    if (want_deg) {
+      MGB_CUDA(cudaStreamSynchronize(P.workers[p]->stream));
+      rs.next_deg[p] = P.workers[p]->host_ctr->next_deg;
+    } else {
+      rs.next_deg[p] = kUnknownDeg;
+    }
   }
 
   for (uint64_t iter = 0;; ++iter) {
@@ -445,7 +475,7 @@ void run_primitive(Plan& P, Prim& prim, const mg_config& cfg) {
       c.iter = iter;
       c.prev = prev;
       c.report = WorkerReport{};
-      MGB_CUDA(cudaMemsetAsync(w.ctr.ptr, 0, sizeof(Counters), w.stream));
+      // the counters were cleared by the previous report_kernel (or at run start)
       prim.body(c);
       step_comm[p] = prim.comm_selector(c, comm);
       if (n == 1) {
@@ -511,8 +541,7 @@ void run_primitive(Plan& P, Prim& prim, const mg_config& cfg) {
         });
       }
       prim.after_merge(c);
-      MGB_CUDA(cudaMemcpyAsync(w.host_ctr, w.ctr.ptr, sizeof(Counters), cudaMemcpyDeviceToHost,
-                               w.stream));
+      MGB_LAUNCH(report_kernel, 1, 128, 0, w.stream, w.ctr.ptr, w.host_ctr_dev);
     }
     // barrier + completion (E:940, E:784-820)
     GlobalView view;

@@ -84,8 +84,10 @@ void init_worker_runtime(Worker& w) {
   MGB_CUDA(cudaEventCreate(&w.ev_k0));
   MGB_CUDA(cudaEventCreate(&w.ev_k1));
   w.ctr.alloc(1);
-  MGB_CUDA(cudaMallocHost(&w.host_ctr, sizeof(Counters)));
+  MGB_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&w.host_ctr), sizeof(Counters),
+                         cudaHostAllocMapped | cudaHostAllocPortable));
   std::memset(w.host_ctr, 0, sizeof(Counters));
+  MGB_CUDA(cudaHostGetDevicePointer(reinterpret_cast<void**>(&w.host_ctr_dev), w.host_ctr, 0));
   w.inbox_cnt.alloc(2 * kMaxWorkers);
   MGB_CUDA(cudaMemset(w.inbox_cnt.ptr, 0, sizeof(uint32_t) * 2 * kMaxWorkers));
   w.merge_stamp.alloc(w.nv ? w.nv : 1);

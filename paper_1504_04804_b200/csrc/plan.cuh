@@ -134,7 +134,8 @@ struct Worker {
 
   // counters
   DevArray<Counters> ctr;
-  Counters* host_ctr = nullptr;  // pinned
+  Counters* host_ctr = nullptr;      // pinned, mapped
+  Counters* host_ctr_dev = nullptr;  // its device-side address (report_kernel writes it)
 
   GraphView graph() const { return {nv, ne, off.ptr, col.ptr, w.ptr}; }
 };

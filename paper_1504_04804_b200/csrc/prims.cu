@@ -660,7 +660,7 @@ struct DobfsPrim : PrimBase {
     // the reference counts the forward step (E:66), i.e. Σdeg(Q).
     bool physical_pull = dir == 1;
     uint64_t logical_w = 0;
-    if (dir == 0 && exact_cost && c.P->n == 1 && c.in_count) {
+    if (dir == 0 && exact_cost && c.P->n == 1 && c.in_count && c.iter > 0) {
       logical_w = c.degsum();
       physical_pull = logical_w > 4ull * ul_len[w.p];
       if (physical_pull) ++physical_pull_steps;
