@@ -42,10 +42,11 @@ def lib():
     """Load the in-tree CUDA library (built by build.py / __graft_entry__.build())."""
     global _lib
     if _lib is None:
-        if not os.path.exists(LIB_PATH):
-            raise RuntimeError(f"{LIB_PATH} is missing: run `python -m paper_1504_04804_b200.build`"
+        path = os.environ.get("MG_LIB_PATH", LIB_PATH)  # experiment variants (build.py)
+        if not os.path.exists(path):
+            raise RuntimeError(f"{path} is missing: run `python -m paper_1504_04804_b200.build`"
                                " (there is no CPU fallback)")
-        _lib = abi.bind(C.CDLL(LIB_PATH))
+        _lib = abi.bind(C.CDLL(path))
     return _lib
 
 

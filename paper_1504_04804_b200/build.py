@@ -14,12 +14,16 @@ from concurrent.futures import ThreadPoolExecutor
 HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
-OUT_DIR = os.path.join(HERE, "build")
-LIB = os.path.join(HERE, "libmgraph_b200.so")
+# MG_BUILD_VARIANT=<name> MG_NVCC_DEFS="-DX=1 ..." builds an experiment variant
+# into build_<name>/ and libmgraph_b200_<name>.so (loaded with MG_LIB_PATH)
+_VARIANT = os.environ.get("MG_BUILD_VARIANT", "")
+OUT_DIR = os.path.join(HERE, "build" + ("_" + _VARIANT if _VARIANT else ""))
+LIB = os.path.join(HERE, "libmgraph_b200" + ("_" + _VARIANT if _VARIANT else "") + ".so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVFLAGS = ARCH + ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xptxas=-v",
-                  "--expt-relaxed-constexpr", "-I" + CSRC, "-I" + os.path.join(ROOT, "include")]
+                  "--expt-relaxed-constexpr", "-I" + CSRC, "-I" + os.path.join(ROOT, "include")] + \
+    os.environ.get("MG_NVCC_DEFS", "").split()
 CXXFLAGS = ["-O3", "-std=c++17", "-fPIC", "-pthread", "-I" + CSRC,
             "-I" + os.path.join(ROOT, "include"), "-I/usr/local/cuda/include"]
 

@@ -18,6 +18,8 @@
 #pragma once
 
 #include <chrono>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <functional>
 #include <optional>
@@ -365,8 +367,22 @@ auto with_dev(Prim& prim, Ctx& c, Fn&& fn) -> decltype(prim.dev32(c), void()) {
 // ---------------------------------------------------------------------------
 // the enactor
 
+// MG_TRACE_HOST=1: host timestamps of the enactor's phases on stderr
+struct HostTrace {
+  bool on = getenv("MG_TRACE_HOST") != nullptr;
+  std::chrono::steady_clock::time_point t0 = std::chrono::steady_clock::now();
+  void operator()(const char* what, uint64_t i = 0) const {
+    if (!on) return;
+    double us = std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() - t0)
+                    .count();
+    fprintf(stderr, "[trace] %9.1f us  %s %llu\n", us, what, (unsigned long long)i);
+  }
+};
+
 template <class Prim>
 void run_primitive(Plan& P, Prim& prim, const mg_config& cfg) {
+  HostTrace trace;
+  trace("enter");
   const uint32_t n = P.n;
   if (prim.dup_required >= 0 && P.dup != prim.dup_required)
     throw Error(MG_EINVAL, std::string(prim.name) + ": requires --dup " +
@@ -413,8 +429,10 @@ void run_primitive(Plan& P, Prim& prim, const mg_config& cfg) {
     ctx[p].fused = fused;
     ctx[p].want_deg = want_deg;
   }
+  trace("workers prepared");
   if (P.shm) fabric_sync(P);  // collective: map peers' (possibly regrown) arenas
   build_send_tables(P);
+  trace("send tables");
   P.h_matrix.assign(n, std::vector<uint64_t>(n, 0));
   P.prof_ms = 0;
   P.prof_bytes = 0;
@@ -440,7 +458,9 @@ void run_primitive(Plan& P, Prim& prim, const mg_config& cfg) {
     // the merge stamp is only read by the merge kernel (n > 1)
     if (n > 1)
       MGB_CUDA(cudaMemsetAsync(w.merge_stamp.ptr, 0, sizeof(uint32_t) * w.nv, w.stream));
+    trace("ctr cleared");
     prim.init(ctx[p]);
+    trace("prim init");
     // advance bound of superstep 0 (only tracked when the policy sizes buffers
     // exactly; the max policy needs no host round trip before superstep 0)
     if (want_deg) {
@@ -476,7 +496,9 @@ void run_primitive(Plan& P, Prim& prim, const mg_config& cfg) {
       c.prev = prev;
       c.report = WorkerReport{};
       // the counters were cleared by the previous report_kernel (or at run start)
+      trace("superstep", iter);
       prim.body(c);
+      trace("body issued", iter);
       step_comm[p] = prim.comm_selector(c, comm);
       if (n == 1) {
         // single partition: every output vertex is local (E:901-904), so the
@@ -552,7 +574,9 @@ void run_primitive(Plan& P, Prim& prim, const mg_config& cfg) {
     uint64_t it_edges = 0, it_comb = 0;
     for (uint32_t p : P.local_workers) {
       Worker& w = *P.workers[p];
+      trace("sync", iter);
       MGB_CUDA(cudaStreamSynchronize(w.stream));
+      trace("synced", iter);
       const Counters& hc = *w.host_ctr;
       if (hc.overflow) throw Error(MG_EWORKER, "inbox overflow on worker " + std::to_string(p));
       WorkerReport r = ctx[p].report;
@@ -631,6 +655,7 @@ void run_primitive(Plan& P, Prim& prim, const mg_config& cfg) {
       }
     }
     rs.views.push_back(std::move(view));
+    trace("report done", iter);
     if (stop) break;
   }
   for (uint32_t p : P.local_workers) {

@@ -214,7 +214,7 @@ __global__ void __launch_bounds__(kExpBlock)
       }
 #pragma unroll
       for (int k = 0; k < kItems; ++k)  // neighbour IDs: independent, coalesced loads
-        nb[k] = eid[k] != 0xFFFFFFFFu ? __ldg(&g.col[eid[k]]) : 0u;
+        nb[k] = eid[k] != 0xFFFFFFFFu ? ld_stream(&g.col[eid[k]]) : 0u;
       bool pass[kItems];
 #pragma unroll
       for (int k = 0; k < kItems; ++k)  // pre-tests: independent loads

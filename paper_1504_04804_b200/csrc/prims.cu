@@ -269,6 +269,7 @@ __global__ void select_nonisolated_kernel(const uint32_t* __restrict__ hosted, u
 constexpr int kPullK = 2;      // arcs held in the record
 constexpr int kPullGroup = 8;  // lanes per vertex in the long-row pass
 constexpr int kPV = 8;         // records per thread per iteration (loads in flight)
+constexpr uint32_t kPullQ = 3072;  // CTA queue capacity (>= one chunk of 256 * kPV)
 
 __global__ void pull_records_kernel(GraphView g, const uint32_t* __restrict__ ni, uint32_t n,
                                     uint4* rec) {
@@ -307,6 +308,43 @@ __device__ __forceinline__ void warp_queue_append(BlockQueue<kCap>& q, const boo
   }
 }
 
+#ifndef MG_PULL_BITS_LEADER
+#define MG_PULL_BITS_LEADER 0
+#endif
+#ifndef MG_PULL_LAZY_FLUSH
+#define MG_PULL_LAZY_FLUSH 1
+#endif
+#ifndef MG_PULL_GRID
+#define MG_PULL_GRID 4
+#endif
+
+#ifndef MG_PULL_BITS_PLAIN
+#define MG_PULL_BITS_PLAIN 0
+#endif
+#ifndef MG_PULL_CNT32
+#define MG_PULL_CNT32 1
+#endif
+
+#if MG_PULL_BITS_PLAIN
+__device__ __forceinline__ void warp_set_bits(uint32_t* bits, bool pred, uint32_t v) {
+  if (pred) atomicOr(&bits[v >> 5], 1u << (v & 31));
+}
+#elif MG_PULL_BITS_LEADER
+// set the visited bits of the lanes' discoveries with one atomicOr per
+// distinct word: a leader loop over the words, each OR formed by one REDUX
+__device__ __forceinline__ void warp_set_bits(uint32_t* bits, bool pred, uint32_t v) {
+  unsigned pending = __ballot_sync(0xffffffffu, pred);
+  const uint32_t wd = v >> 5, bit = 1u << (v & 31);
+  while (pending) {
+    const int leader = __ffs(pending) - 1;
+    const uint32_t lw = __shfl_sync(0xffffffffu, wd, leader);
+    const bool mine = pred && wd == lw;
+    const uint32_t b = __reduce_or_sync(0xffffffffu, mine ? bit : 0u);
+    if (lane_id() == (unsigned)leader) atomicOr(&bits[lw], b);
+    pending &= ~__ballot_sync(0xffffffffu, mine);
+  }
+}
+#else
 // set the visited bits of the lanes' discoveries with one atomicOr per run of
 // lanes hitting the same word (records are sorted, so a warp's discoveries
 // form few runs): a segmented OR by shuffles, the run head issues the atomic
@@ -323,6 +361,7 @@ __device__ __forceinline__ void warp_set_bits(uint32_t* bits, bool pred, uint32_
   const uint32_t pw = __shfl_up_sync(0xffffffffu, wd, 1);
   if (pred && (lane == 0 || pw != wd)) atomicOr(&bits[wd], b);
 }
+#endif
 
 // pull step, stage 1 (primitives.cpp:230-251): one thread per unvisited record
 // tests the record's two arcs against the frontier bitmap; a hit labels the
@@ -340,9 +379,15 @@ __global__ void __launch_bounds__(256, 4)
                              uint32_t* ul_out_cnt, uint32_t* longq, uint32_t* long_cnt,
                              Counters* ctr, unsigned long long* scanned_out,
                              unsigned long long* deg_out) {
+#if MG_PULL_CNT32
+  uint32_t scanned = 0, opened = 0, degs = 0;  // per-thread partials fit 32 bits
+#else
   unsigned long long scanned = 0, opened = 0, degs = 0;
+#endif
   uint32_t found_n = 0;
-  __shared__ BlockQueue<256 * kPV> q_found, q_keep, q_long;
+  // queues hold up to kPullQ entries and are flushed only when one could
+  // overflow in the next chunk (one barrier per chunk otherwise)
+  __shared__ BlockQueue<kPullQ> q_found, q_keep, q_long;
   __shared__ uint32_t s_found;
   q_found.reset();
   q_keep.reset();
@@ -393,18 +438,22 @@ __global__ void __launch_bounds__(256, 4)
     warp_queue_append<kPV>(q_keep, keep, pos);
     warp_queue_append<kPV>(q_long, lng, pos);
     __syncthreads();
-    if (threadIdx.x == 0) {
-      q_found.base = q_found.n ? atomicAdd(&ctr->out_cnt, q_found.n) : 0u;
-      q_keep.base = q_keep.n ? atomicAdd(ul_out_cnt, q_keep.n) : 0u;
-      q_long.base = q_long.n ? atomicAdd(long_cnt, q_long.n) : 0u;
+    const bool last = base + gridDim.x * chunk >= nul;
+    if (!MG_PULL_LAZY_FLUSH || last || q_found.n > kPullQ - chunk || q_keep.n > kPullQ - chunk ||
+        q_long.n > kPullQ - chunk) {  // CTA-uniform: read after the barrier
+      if (threadIdx.x == 0) {
+        q_found.base = q_found.n ? atomicAdd(&ctr->out_cnt, q_found.n) : 0u;
+        q_keep.base = q_keep.n ? atomicAdd(ul_out_cnt, q_keep.n) : 0u;
+        q_long.base = q_long.n ? atomicAdd(long_cnt, q_long.n) : 0u;
+      }
+      __syncthreads();
+      for (uint32_t k = threadIdx.x; k < q_found.n; k += 256) out[q_found.base + k] = q_found.buf[k];
+      for (uint32_t k = threadIdx.x; k < q_keep.n; k += 256) ul_out[q_keep.base + k] = q_keep.buf[k];
+      for (uint32_t k = threadIdx.x; k < q_long.n; k += 256) longq[q_long.base + k] = q_long.buf[k];
+      __syncthreads();
+      if (threadIdx.x == 0) q_found.n = q_keep.n = q_long.n = 0;
+      __syncthreads();
     }
-    __syncthreads();
-    for (uint32_t k = threadIdx.x; k < q_found.n; k += 256) out[q_found.base + k] = q_found.buf[k];
-    for (uint32_t k = threadIdx.x; k < q_keep.n; k += 256) ul_out[q_keep.base + k] = q_keep.buf[k];
-    for (uint32_t k = threadIdx.x; k < q_long.n; k += 256) longq[q_long.base + k] = q_long.buf[k];
-    __syncthreads();
-    if (threadIdx.x == 0) q_found.n = q_keep.n = q_long.n = 0;
-    __syncthreads();
   }
   if (!emit_found) {
     unsigned m = __reduce_add_sync(0xffffffffu, found_n);
@@ -710,7 +759,7 @@ struct DobfsPrim : PrimBase {
     // cost test needs no extra host round trip
     unsigned long long* deg_out = reports_deg && !c.want_deg ? &c.ctr()->next_deg : nullptr;
     if (nul) {
-      MGB_LAUNCH(dobfs_pull_thread_kernel, grid_for(nul, 256 * kPV, kNumSMs * 8), 256, 0,
+      MGB_LAUNCH(dobfs_pull_thread_kernel, grid_for(nul, 256 * kPV, kNumSMs * MG_PULL_GRID), 256, 0,
                  w.stream, w.pull_rec.ptr, ul, nul, w.su32[0].ptr, w.su32[1].ptr, w.su32[2].ptr,
                  w.su32[3].ptr, next_label, mark_preds ? 1 : 0, c.owner_view(), emit ? 1 : 0,
                  w.output.ptr, w.ul_buf[dst].ptr, ulcnt, w.ul_buf[2].ptr, cnts + 1, c.ctr(),
@@ -833,7 +882,7 @@ __device__ __forceinline__ void visit_batch(const SsspDev<T>& f, const uint32_t*
   T nd[K], cur[K];
 #pragma unroll
   for (int k = 0; k < K; ++k) {
-    nd[k] = pass[k] ? __ldg(&f.fdist[src[k]]) + (T)__ldg(&f.w[eid[k]]) : (T)0;
+    nd[k] = pass[k] ? __ldg(&f.fdist[src[k]]) + (T)ld_stream(&f.w[eid[k]]) : (T)0;
     cur[k] = pass[k] ? __ldcg(&f.dists[nb[k]]) : (T)0;
   }
   T old[K];
