@@ -268,8 +268,17 @@ __global__ void select_nonisolated_kernel(const uint32_t* __restrict__ hosted, u
 // positions; the first pull of a run walks all records without a list.
 constexpr int kPullK = 2;      // arcs held in the record
 constexpr int kPullGroup = 8;  // lanes per vertex in the long-row pass
-constexpr int kPV = 8;         // records per thread per iteration (loads in flight)
-constexpr uint32_t kPullQ = 3072;  // CTA queue capacity (>= one chunk of 256 * kPV)
+#ifndef MG_PULL_PV
+#define MG_PULL_PV 8
+#endif
+#ifndef MG_PULL_MINB
+#define MG_PULL_MINB 4
+#endif
+#ifndef MG_PULL_STREAM
+#define MG_PULL_STREAM 1
+#endif
+constexpr int kPV = MG_PULL_PV;  // records per thread per iteration (loads in flight)
+constexpr uint32_t kPullQ = 256 * kPV + 1024;  // CTA queue capacity (> one chunk of 256 * kPV)
 
 __global__ void pull_records_kernel(GraphView g, const uint32_t* __restrict__ ni, uint32_t n,
                                     uint4* rec) {
@@ -371,7 +380,7 @@ __device__ __forceinline__ void warp_set_bits(uint32_t* bits, bool pred, uint32_
 // partition) the discovered vertices are only counted (and their degrees
 // summed into deg_out when non-null): the next superstep rebuilds the frontier
 // list from the visited bitmap only if it pushes.
-__global__ void __launch_bounds__(256, 4)
+__global__ void __launch_bounds__(256, MG_PULL_MINB)
     dobfs_pull_thread_kernel(const uint4* __restrict__ rec, const uint32_t* __restrict__ ul,
                              uint32_t nul, uint32_t* labels, uint32_t* preds, uint32_t* vis,
                              const uint32_t* __restrict__ fb, uint32_t next_label, int mark_preds,
@@ -405,7 +414,11 @@ __global__ void __launch_bounds__(256, 4)
     }
 #pragma unroll
     for (int j = 0; j < kPV; ++j)  // coalesced 16-byte records, kPV in flight
+#if MG_PULL_STREAM
+      r[j] = pos[j] != kInfLabel ? __ldcs(&rec[pos[j]]) : make_uint4(0, 0, kInfLabel, kInfLabel);
+#else
       r[j] = pos[j] != kInfLabel ? __ldg(&rec[pos[j]]) : make_uint4(0, 0, kInfLabel, kInfLabel);
+#endif
     bool open[kPV], h0[kPV], h1[kPV];
 #pragma unroll
     for (int j = 0; j < kPV; ++j) {
@@ -425,7 +438,11 @@ __global__ void __launch_bounds__(256, 4)
       opened += open[j];
       if (found[j]) {
         scanned += h0[j] ? 1 : 2;
+#if MG_PULL_STREAM
+        __stcs(&labels[v], next_label);
+#else
         labels[v] = next_label;
+#endif
         if (mark_preds) preds[v] = ow.to_global(h0[j] ? r[j].z : r[j].w);
         ++found_n;
         degs += d;
