@@ -1376,9 +1376,10 @@ __device__ __forceinline__ void bc_finish(uint32_t v, uint32_t source, double sv
 
 __global__ void __launch_bounds__(256)
     bc_backward_thread_kernel(GraphView g, const uint32_t* __restrict__ list, const uint32_t* nlist,
-                              const double* __restrict__ sigma, double* delta, double* bc,
-                              const double* __restrict__ coef, uint32_t source, Counters* ctr) {
-  const uint32_t n = *nlist;
+                              uint32_t nfix, const double* __restrict__ sigma, double* delta,
+                              double* bc, const double* __restrict__ coef, uint32_t source,
+                              Counters* ctr) {
+  const uint32_t n = nlist ? *nlist : nfix;
   unsigned long long scanned = 0;
   for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
     const uint32_t v = list[i];
@@ -1400,9 +1401,10 @@ __global__ void __launch_bounds__(256)
 
 __global__ void __launch_bounds__(256)
     bc_backward_warp_kernel(GraphView g, const uint32_t* __restrict__ list, const uint32_t* nlist,
-                            const double* __restrict__ sigma, double* delta, double* bc,
-                            const double* __restrict__ coef, uint32_t source, Counters* ctr) {
-  const uint32_t n = *nlist;
+                            uint32_t nfix, const double* __restrict__ sigma, double* delta,
+                            double* bc, const double* __restrict__ coef, uint32_t source,
+                            Counters* ctr) {
+  const uint32_t n = nlist ? *nlist : nfix;
   const uint32_t warps = gridDim.x * blockDim.x / 32;
   unsigned long long scanned = 0;
   for (uint32_t i = (blockIdx.x * blockDim.x + threadIdx.x) / 32; i < n; i += warps) {
@@ -1419,11 +1421,103 @@ __global__ void __launch_bounds__(256)
   warp_add_u64(&ctr->edges, scanned);
 }
 
+// Level buckets for the backward phase: the hosted vertices are counting-
+// sorted once by (label, long row) — bucket 2L: short rows of level L, 2L+1:
+// long rows — so every backward superstep works on a contiguous slice
+// instead of rescanning all hosted vertices per level.  Per-CTA shared
+// histograms, one small scan (bucket-major), a scatter with shared cursors.
+constexpr uint32_t kBcBuckets = 2048;  // 2 * (max_level + 1) must fit
+constexpr uint32_t kBcBucketCtas = kNumSMs * 4;
+
+__global__ void __launch_bounds__(256)
+    bc_bucket_count_kernel(const uint32_t* __restrict__ hosted, uint32_t nh,
+                           const uint32_t* __restrict__ labels, const uint32_t* __restrict__ off,
+                           uint32_t max_level, uint32_t nb, uint32_t* cta_hist) {
+  __shared__ uint32_t h[kBcBuckets];
+  for (uint32_t b = threadIdx.x; b < nb; b += blockDim.x) h[b] = 0;
+  __syncthreads();
+  const uint32_t per = (nh + gridDim.x - 1) / gridDim.x;
+  const uint32_t lo = blockIdx.x * per, hi = lo + per < nh ? lo + per : nh;
+  for (uint32_t i = lo + threadIdx.x; i < hi; i += blockDim.x) {
+    const uint32_t v = hosted[i], l = labels[v];
+    if (l <= max_level) atomicAdd(&h[2 * l + (off[v + 1] - off[v] >= kBcWarpDeg ? 1 : 0)], 1u);
+  }
+  __syncthreads();
+  for (uint32_t b = threadIdx.x; b < nb; b += blockDim.x) cta_hist[b * gridDim.x + blockIdx.x] = h[b];
+}
+
+// exclusive scan of the bucket-major CTA histogram in one CTA; bucket b starts
+// at the scanned entry of (b, CTA 0), the total closes the table
+__global__ void __launch_bounds__(1024)
+    bc_bucket_scan_kernel(uint32_t* cta_hist, uint32_t nb, uint32_t nctas, uint32_t* start) {
+  using Scan = cub::BlockScan<uint32_t, 1024>;
+  __shared__ typename Scan::TempStorage tmp;
+  __shared__ uint32_t carry;
+  const uint32_t n = nb * nctas;
+  if (threadIdx.x == 0) carry = 0;
+  __syncthreads();
+  for (uint32_t base = 0; base < n; base += 1024) {
+    const uint32_t i = base + threadIdx.x;
+    uint32_t d = i < n ? cta_hist[i] : 0u, excl, total;
+    Scan(tmp).ExclusiveSum(d, excl, total);
+    if (i < n) {
+      cta_hist[i] = carry + excl;
+      if (i % nctas == 0) start[i / nctas] = carry + excl;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) carry += total;
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) start[nb] = carry;
+}
+
+__global__ void __launch_bounds__(256)
+    bc_bucket_scatter_kernel(const uint32_t* __restrict__ hosted, uint32_t nh,
+                             const uint32_t* __restrict__ labels, const uint32_t* __restrict__ off,
+                             uint32_t max_level, uint32_t nb, const uint32_t* __restrict__ cta_off,
+                             uint32_t* out) {
+  __shared__ uint32_t cur[kBcBuckets];
+  for (uint32_t b = threadIdx.x; b < nb; b += blockDim.x) cur[b] = cta_off[b * gridDim.x + blockIdx.x];
+  __syncthreads();
+  const uint32_t per = (nh + gridDim.x - 1) / gridDim.x;
+  const uint32_t lo = blockIdx.x * per, hi = lo + per < nh ? lo + per : nh;
+  for (uint32_t i = lo + threadIdx.x; i < hi; i += blockDim.x) {
+    const uint32_t v = hosted[i], l = labels[v];
+    if (l <= max_level)
+      out[atomicAdd(&cur[2 * l + (off[v + 1] - off[v] >= kBcWarpDeg ? 1 : 0)], 1u)] = v;
+  }
+}
+
+// per backward superstep: the level's slice becomes the output (the broadcast
+// of the superstep), the deepest level gets coef = 1/sigma, and the level
+// below the current one (finished last superstep) gets its coefficients
+__global__ void bc_level_prep_kernel(const uint32_t* __restrict__ list, uint32_t l0, uint32_t l1,
+                                     uint32_t c0, uint32_t c1, int deepest,
+                                     const double* __restrict__ sigma,
+                                     const double* __restrict__ delta, double* coef, uint32_t* out,
+                                     Counters* ctr) {
+  const uint32_t stride = gridDim.x * blockDim.x;
+  for (uint32_t i = l0 + blockIdx.x * blockDim.x + threadIdx.x; i < l1; i += stride) {
+    const uint32_t v = list[i];
+    out[i - l0] = v;
+    if (deepest) coef[v] = 1.0 / sigma[v];  // delta = 0 on the deepest level
+  }
+  for (uint32_t i = c0 + blockIdx.x * blockDim.x + threadIdx.x; i < c1; i += stride) {
+    const uint32_t v = list[i];
+    coef[v] = (1.0 + delta[v]) / sigma[v];
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) ctr->out_cnt = l1 - l0;
+}
+
 struct BcPrim : PrimBase {
   uint32_t source;
   int phase = kFwd;
   uint32_t max_level = 0;
   uint64_t backward_from = 0;
+  // per worker: level buckets built for this run, host copy of the bucket table
+  std::vector<char> bucketed = std::vector<char>(kMaxWorkers, 0);
+  std::vector<std::vector<uint32_t>> bucket_starts =
+      std::vector<std::vector<uint32_t>>(kMaxWorkers);
   BcPrim(uint32_t s) : source(s) {
     name = "bc";
     nvv = 2;
@@ -1462,20 +1556,68 @@ struct BcPrim : PrimBase {
         c.prev->inflight_records == 0) {
       phase = kBwd;
       backward_from = c.iter;
-      max_level = (uint32_t)c.prev->max_u(0);
+      // one partition: the deepest label is the last superstep that found
+      // anything (superstep t labels t+1; superstep c.iter-1 found nothing)
+      max_level = c.P->n == 1 ? (uint32_t)c.iter - 1 : (uint32_t)c.prev->max_u(0);
+      std::fill(bucketed.begin(), bucketed.end(), 0);
     }
     if (first && phase == kBwd && c.iter - backward_from >= max_level) phase = kDone;
     uint32_t nh = (uint32_t)w.hosted_host.size();
     if (phase == kFwd) {
       c.pipeline(dev(c), w.nv);
-      if (nh)
+      if (nh && c.P->n > 1)  // the global max hosted label; n = 1 derives it
         MGB_LAUNCH(max_hosted_label_kernel, grid_for(nh, 256, kNumSMs * 4), 256, 0, w.stream,
                    w.su32[0].ptr, w.hosted.ptr, nh, c.ctr());
       c.report.u[1] = kFwd;
       c.report.u[0] = 0;  // filled from the device counter
       return;
     }
-    if (phase == kBwd) {
+    if (phase == kBwd && 2ull * (max_level + 1) <= kBcBuckets) {
+      const uint32_t level = max_level - (uint32_t)(c.iter - backward_from);
+      const uint32_t nb = 2 * (max_level + 1);
+      c.ensure_output(nh);
+      std::vector<uint32_t>& bucket_start = bucket_starts[w.p];
+      if (!bucketed[w.p]) {  // once per run: counting sort of the hosted vertices by level
+        bucketed[w.p] = 1;
+        if (w.aux[0].n < nh + 1ull) w.aux[0].alloc(nh + 1ull);
+        if (w.aux[1].n < (uint64_t)nb * kBcBucketCtas) w.aux[1].alloc((uint64_t)nb * kBcBucketCtas);
+        if (w.aux[2].n < nb + 1ull) w.aux[2].alloc(nb + 1ull);
+        MGB_LAUNCH(bc_bucket_count_kernel, kBcBucketCtas, 256, 0, w.stream, w.hosted.ptr, nh,
+                   w.su32[0].ptr, w.off.ptr, max_level, nb, w.aux[1].ptr);
+        MGB_LAUNCH(bc_bucket_scan_kernel, 1, 1024, 0, w.stream, w.aux[1].ptr, nb, kBcBucketCtas,
+                   w.aux[2].ptr);
+        MGB_LAUNCH(bc_bucket_scatter_kernel, kBcBucketCtas, 256, 0, w.stream, w.hosted.ptr, nh,
+                   w.su32[0].ptr, w.off.ptr, max_level, nb, w.aux[1].ptr, w.aux[0].ptr);
+        bucket_start.assign(nb + 1, 0);
+        MGB_CUDA(cudaMemcpyAsync(bucket_start.data(), w.aux[2].ptr, 4ull * (nb + 1),
+                                 cudaMemcpyDeviceToHost, w.stream));
+        MGB_CUDA(cudaStreamSynchronize(w.stream));
+      }
+      const uint32_t* list = w.aux[0].ptr;
+      const uint32_t s0 = bucket_start[2 * level], s1 = bucket_start[2 * level + 1],
+                     s2 = bucket_start[2 * level + 2];
+      const bool deepest = level == max_level;
+      const uint32_t c0 = deepest ? 0 : bucket_start[2 * level + 2];
+      const uint32_t c1 = deepest ? 0 : bucket_start[2 * level + 4];
+      const uint32_t work = (s2 - s0) > (c1 - c0) ? (s2 - s0) : (c1 - c0);
+      MGB_LAUNCH(bc_level_prep_kernel, grid_for(work, 256, kNumSMs * 8), 256, 0, w.stream, list,
+                 s0, s2, c0, c1, deepest ? 1 : 0, w.sf64[0].ptr, w.sf64[1].ptr, w.sf64[3].ptr,
+                 w.output.ptr, c.ctr());
+      if (!deepest) {  // the deepest level only broadcasts
+        if (s1 > s0)
+          MGB_LAUNCH(bc_backward_thread_kernel, grid_for(s1 - s0, 256, kNumSMs * 8), 256, 0,
+                     w.stream, w.graph(), list + s0, nullptr, s1 - s0, w.sf64[0].ptr,
+                     w.sf64[1].ptr, w.sf64[2].ptr, w.sf64[3].ptr, source, c.ctr());
+        if (s2 > s1)
+          MGB_LAUNCH(bc_backward_warp_kernel, grid_for((uint64_t)(s2 - s1) * 32, 256, kNumSMs * 8),
+                     256, 0, w.stream, w.graph(), list + s1, nullptr, s2 - s1, w.sf64[0].ptr,
+                     w.sf64[1].ptr, w.sf64[2].ptr, w.sf64[3].ptr, source, c.ctr());
+      }
+      c.report.u[0] = max_level;
+      c.report.u[1] = kBwd;
+      return;
+    }
+    if (phase == kBwd) {  // very deep BFS trees: one selection pass per level
       uint32_t level = max_level - (uint32_t)(c.iter - backward_from);
       c.ensure_output(nh);
       if (w.aux[0].n < nh + 1ull) w.aux[0].alloc(nh + 1ull);  // short rows of the level
@@ -1490,10 +1632,10 @@ struct BcPrim : PrimBase {
                    w.sf64[0].ptr, w.sf64[1].ptr, w.sf64[3].ptr);
         if (level < max_level) {  // the deepest level only broadcasts
           MGB_LAUNCH(bc_backward_thread_kernel, kNumSMs * 8, 256, 0, w.stream, w.graph(),
-                     w.aux[0].ptr, cnts, w.sf64[0].ptr, w.sf64[1].ptr, w.sf64[2].ptr,
+                     w.aux[0].ptr, cnts, 0u, w.sf64[0].ptr, w.sf64[1].ptr, w.sf64[2].ptr,
                      w.sf64[3].ptr, source, c.ctr());
           MGB_LAUNCH(bc_backward_warp_kernel, kNumSMs * 8, 256, 0, w.stream, w.graph(),
-                     w.aux[1].ptr, cnts + 1, w.sf64[0].ptr, w.sf64[1].ptr, w.sf64[2].ptr,
+                     w.aux[1].ptr, cnts + 1, 0u, w.sf64[0].ptr, w.sf64[1].ptr, w.sf64[2].ptr,
                      w.sf64[3].ptr, source, c.ctr());
         }
       }
