@@ -1845,6 +1845,104 @@ __global__ void __launch_bounds__(256)
   }
 }
 
+// Fused superstep (locality-ordered single partition): pull this superstep's
+// accumulator from contrib_cur and immediately apply the NEXT pr_update
+// (primitives.cpp:697-711) and contribution rank/deg — the update of
+// superstep t+1 needs only accum_t and dangling_t, both final here — so one
+// pass per superstep replaces pull + update/contrib.  Next-superstep scalars
+// go to u[1] (max relative delta, ordered bits), u[2] (rank sum), u[3]
+// (dangling mass) as doubles; contributions are double-buffered.
+struct PrFuse {
+  const uint32_t* __restrict__ pdeg;
+  double* rank;
+  double* contrib_next;
+  double base, damping, dangling_n;
+  const double* dangling_ptr;  // superstep 0: dangling_0 on the device
+  double nv;
+  int count_edges;             // superstep 0's arcs were counted by its contribution pass
+};
+
+__device__ __forceinline__ void pr_fuse_finish(const PrFuse& f, uint32_t v, double s, double dn,
+                                               double& dmax, double& sum, double& dangl,
+                                               uint32_t& scanned) {
+  const double nr = f.base + f.damping * (s + dn);
+  const double rel = fabs(nr - f.rank[v]) / fmax(nr, 1e-300);
+  dmax = fmax(dmax, rel);
+  f.rank[v] = nr;
+  sum += nr;
+  const uint32_t d = f.pdeg[v];
+  if (d == 0) {
+    dangl += nr;
+    f.contrib_next[v] = 0.0;
+  } else {
+    f.contrib_next[v] = nr / (double)d;
+    scanned += d;
+  }
+}
+
+__device__ __forceinline__ void pr_fuse_reduce(Counters* ctr, double dmax, double sum,
+                                               double dangl, uint32_t scanned) {
+  for (int o = 16; o > 0; o >>= 1) {
+    dmax = fmax(dmax, __shfl_xor_sync(0xffffffffu, dmax, o));
+    sum += __shfl_xor_sync(0xffffffffu, sum, o);
+    dangl += __shfl_xor_sync(0xffffffffu, dangl, o);
+  }
+  if (scanned) warp_add_u64(&ctr->edges, scanned);
+  if (lane_id() == 0) {
+    atomicMax(&ctr->u[1], (unsigned long long)__double_as_longlong(dmax));
+    atomicAdd(reinterpret_cast<double*>(&ctr->u[2]), sum);
+    if (dangl != 0.0) atomicAdd(reinterpret_cast<double*>(&ctr->u[3]), dangl);
+  }
+}
+
+__global__ void __launch_bounds__(256)
+    pr_pull_update_kernel(const uint32_t* __restrict__ toff, const uint32_t* __restrict__ tcol,
+                          uint32_t nv, const double* __restrict__ contrib, PrFuse f,
+                          Counters* ctr) {
+  const double dn = f.dangling_ptr ? *f.dangling_ptr / f.nv : f.dangling_n;
+  double dmax = 0.0, sum = 0.0, dangl = 0.0;
+  uint32_t scanned = 0;
+  for (uint32_t v = blockIdx.x * blockDim.x + threadIdx.x; v < nv; v += gridDim.x * blockDim.x) {
+    const uint32_t b = __ldg(&toff[v]), e = __ldg(&toff[v + 1]);
+    if (e - b >= kPullLong) continue;  // warp kernel
+    double s0 = 0.0, s1 = 0.0;
+    uint32_t k = b;
+    for (; k + 3 < e; k += 4) {
+      const uint32_t u0 = __ldg(&tcol[k]), u1 = __ldg(&tcol[k + 1]);
+      const uint32_t u2 = __ldg(&tcol[k + 2]), u3 = __ldg(&tcol[k + 3]);
+      const double c0 = __ldg(&contrib[u0]), c1 = __ldg(&contrib[u1]);
+      const double c2 = __ldg(&contrib[u2]), c3 = __ldg(&contrib[u3]);
+      s0 += c0;
+      s1 += c1;
+      s0 += c2;
+      s1 += c3;
+    }
+    for (; k < e; ++k) s0 += __ldg(&contrib[__ldg(&tcol[k])]);
+    pr_fuse_finish(f, v, s0 + s1, dn, dmax, sum, dangl, scanned);
+  }
+  pr_fuse_reduce(ctr, dmax, sum, dangl, f.count_edges ? scanned : 0u);
+}
+
+__global__ void __launch_bounds__(256)
+    pr_pull_update_warp_kernel(const uint32_t* __restrict__ toff,
+                               const uint32_t* __restrict__ tcol,
+                               const uint32_t* __restrict__ rows, uint32_t nrows,
+                               const double* __restrict__ contrib, PrFuse f, Counters* ctr) {
+  const double dn = f.dangling_ptr ? *f.dangling_ptr / f.nv : f.dangling_n;
+  double dmax = 0.0, sum = 0.0, dangl = 0.0;
+  uint32_t scanned = 0;
+  const uint32_t warps = gridDim.x * blockDim.x / 32;
+  for (uint32_t i = (blockIdx.x * blockDim.x + threadIdx.x) / 32; i < nrows; i += warps) {
+    const uint32_t v = rows[i];
+    double s = 0.0;
+    for (uint32_t k = toff[v] + lane_id(); k < toff[v + 1]; k += 32)
+      s += __ldg(&contrib[__ldg(&tcol[k])]);
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    if (lane_id() == 0) pr_fuse_finish(f, v, s, dn, dmax, sum, dangl, scanned);
+  }
+  pr_fuse_reduce(ctr, dmax, sum, dangl, f.count_edges ? scanned : 0u);
+}
+
 __global__ void unpermute_f64_kernel(const double* __restrict__ src, const uint32_t* __restrict__ perm,
                                      uint32_t n, double* dst) {
   for (uint32_t v = blockIdx.x * blockDim.x + threadIdx.x; v < n; v += gridDim.x * blockDim.x)
@@ -2025,18 +2123,49 @@ struct PrPrim : PrimBase {
                  0, w.stream, w.toff.ptr, w.tcol.ptr, w.tlong.ptr, w.n_tlong, w.sf64[2].ptr,
                  w.sf64[1].ptr);
   }
+  // Fused ordered form.  Superstep t reports the reference's values of its own
+  // update (delta_t, sum_t, dangling_t), which the fused pass of superstep t-1
+  // already produced, and runs the fused pass for t+1 unless delta_t < eps
+  // stops the run here (then rank already holds rank_t, the reference's
+  // result).  On a max-iteration stop the pass of the last superstep is the
+  // reference's finalize update (primitives.cpp:801-810).
+  double next_delta = 0, next_sum = 0, next_dangling = 0;
+  uint64_t edges_per_step = 0;
   void body_ordered(Ctx& c) {
     Worker& w = *c.w;
     const bool first = c.worker() == c.P->local_workers.front();
+    const double n = (double)c.P->nv;
+    bool run_pass = true;
     if (c.iter >= 1) {
-      update_contrib(c, c.prev->sum_f(0), true);
+      const WorkerReport& pr = c.prev->reports[w.p];
+      if (c.iter == 1) edges_per_step = pr.edges_delta;
+      std::memcpy(&next_delta, &pr.u[1], 8);
+      std::memcpy(&next_sum, &pr.u[2], 8);
+      std::memcpy(&next_dangling, &pr.u[3], 8);
+      c.report.f[0] = next_dangling;  // pushed mass of rank_t
+      c.report.f[1] = next_delta;     // pr_update of superstep t
+      c.report.f[2] = next_sum;
       if (first) ++updates;
+      run_pass = !(next_delta < epsilon);
+      if (!run_pass && edges_per_step)  // the push of rank_t still counts (E:66)
+        MGB_LAUNCH(add_u64_kernel, 1, 1, 0, w.stream, &c.ctr()->edges,
+                   (unsigned long long)edges_per_step);
     } else {
-      update_contrib(c, 0.0, false);
+      update_contrib(c, 0.0, false);  // contrib_0, dangling_0 -> f[0], W
       c.report.f[1] = INFINITY;
     }
     if (first && c.prev && c.iter >= 2) rank_sums.push_back(c.prev->sum_f(2));
-    pull(w);
+    if (!run_pass) return;
+    double* cur = (c.iter & 1) ? w.sf64[0].ptr : w.sf64[2].ptr;
+    double* nxt = (c.iter & 1) ? w.sf64[2].ptr : w.sf64[0].ptr;
+    PrFuse f{w.pr_pdeg.ptr, w.sf64[3].ptr, nxt, (1.0 - damping) / n, damping,
+             next_dangling / n, c.iter == 0 ? &c.ctr()->f[0] : nullptr, n, c.iter == 0 ? 0 : 1};
+    if (w.nv)
+      MGB_LAUNCH(pr_pull_update_kernel, grid_for(w.nv, 256, kNumSMs * 16), 256, 0, w.stream,
+                 w.toff.ptr, w.tcol.ptr, w.nv, cur, f, c.ctr());
+    if (w.n_tlong)
+      MGB_LAUNCH(pr_pull_update_warp_kernel, grid_for((uint64_t)w.n_tlong * 32, 256, kNumSMs * 8),
+                 256, 0, w.stream, w.toff.ptr, w.tcol.ptr, w.tlong.ptr, w.n_tlong, cur, f, c.ctr());
   }
   void body(Ctx& c) {  // primitives.cpp:747-782
     Worker& w = *c.w;
@@ -2081,9 +2210,11 @@ struct PrPrim : PrimBase {
     if (first && c.worker() == 0 && last.iteration >= 1) rank_sums.push_back(last.sum_f(2));
     Worker& w = *c.w;
     if (!delta_stopped) {
-      MGB_CUDA(cudaMemsetAsync(c.ctr(), 0, sizeof(Counters), w.stream));
-      if (w.pr_reordered) update_contrib(c, last.sum_f(0), true);
-      else update(c, last.sum_f(0), true);
+      // ordered form: the last superstep's fused pass already applied it
+      if (!w.pr_reordered) {
+        MGB_CUDA(cudaMemsetAsync(c.ctr(), 0, sizeof(Counters), w.stream));
+        update(c, last.sum_f(0), true);
+      }
       if (first) ++updates;
     }
     if (w.pr_reordered && w.nv)  // ranks back to vertex IDs
