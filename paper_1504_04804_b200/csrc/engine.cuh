@@ -129,11 +129,108 @@ __global__ void __launch_bounds__(256)
 
 // publish per-destination counts into the peers' slot counters; the system
 // fence makes the record stores visible before the count (P2P over NVLink)
+// (multi-process, device protocol: then raise this superstep's publish flag
+// in every peer's mailbox once all counts are out)
 static __global__ void publish_kernel(const Counters* ctr, uint32_t* const* cnt_ptr, uint32_t n,
-                               uint32_t p) {
+                                      uint32_t p, Mailbox* const* mbox, uint32_t parity,
+                                      uint32_t epoch) {
   uint32_t d = threadIdx.x;
   __threadfence_system();
   if (d < n && d != p) *cnt_ptr[d] = ctr->send_cnt[d] < 0xFFFFFFFFu ? ctr->send_cnt[d] : 0u;
+  if (!mbox) return;
+  __threadfence_system();
+  __syncthreads();
+  if (d < n && d != p) *reinterpret_cast<volatile uint32_t*>(&mbox[d]->pub[parity][p]) = epoch;
+}
+
+// ~60 s at ~2 GHz: a peer that never arrives turns into an error, not a hang
+constexpr long long kSpinCycles = 120000000000ll;
+
+// multi-process, device protocol: the merge may start once every peer raised
+// its publish flag for this superstep (replaces the host barrier, E:922)
+static __global__ void mp_wait_pub_kernel(Mailbox* mine, uint32_t parity, uint32_t epoch,
+                                          uint32_t n, uint32_t me, uint32_t* err) {
+  const uint32_t q = threadIdx.x;
+  if (q < n && q != me) {
+    const volatile uint32_t* f = &mine->pub[parity][q];
+    const long long t0 = clock64();
+    while (*f != epoch) {
+      __nanosleep(200);
+      if (clock64() - t0 > kSpinCycles) {
+        atomicExch(err, 1u);
+        break;
+      }
+    }
+  }
+  __threadfence();
+}
+
+// host-known part of a WorkerReport (set by the primitive's host hooks)
+struct HostReportPart {
+  double f[4];
+  unsigned long long u[4];
+  int next_is_out;
+};
+
+// multi-process, device protocol: build this rank's WorkerReport, store it
+// into every rank's mailbox (arrival flag last), hand the own counters to the
+// host and clear them, wait for all ranks' reports and copy the n reports to
+// the mapped host page — the WorkerReport all-gather of the completion step
+// (E:784-820) without a host barrier
+static __global__ void mp_report_kernel(Counters* ctr, Counters* host_ctr, HostReportPart hp,
+                                        Mailbox* const* mbox, uint32_t n, uint32_t me,
+                                        uint32_t epoch, DevReport* host_out, uint32_t* err) {
+  const uint32_t slot = epoch & 1u;
+  if (threadIdx.x == 0) {
+    DevReport r;
+    r.out_frontier = ctr->out_cnt;
+    r.next_frontier = hp.next_is_out ? ctr->out_cnt : ctr->next_cnt;
+    r.edges_delta = ctr->edges;
+    r.combine_delta = ctr->combine;
+    for (int k = 0; k < 4; ++k) {
+      r.f[k] = hp.f[k] != 0.0 ? hp.f[k] : ctr->f[k];
+      r.u[k] = hp.u[k] != 0ull ? hp.u[k] : ctr->u[k];
+    }
+    for (uint32_t q = 0; q < kMaxMpRanks; ++q) r.send_cnt[q] = q < n ? ctr->send_cnt[q] : 0u;
+    r.overflow = ctr->overflow;
+    r.epoch = 0;
+    for (uint32_t d = 0; d < n; ++d) {
+      DevReport* dst = &mbox[d]->rep[slot][me];
+      const uint32_t* src = reinterpret_cast<const uint32_t*>(&r);
+      uint32_t* o = reinterpret_cast<uint32_t*>(dst);
+      for (uint32_t i = 0; i + 1 < sizeof(DevReport) / 4; ++i) o[i] = src[i];
+    }
+    __threadfence_system();
+    for (uint32_t d = 0; d < n; ++d)
+      *reinterpret_cast<volatile uint32_t*>(&mbox[d]->rep[slot][me].epoch) = epoch;
+  }
+  __syncthreads();
+  {  // own counters to the host, cleared for the next superstep
+    uint32_t* src = reinterpret_cast<uint32_t*>(ctr);
+    volatile uint32_t* dst = reinterpret_cast<volatile uint32_t*>(host_ctr);
+    for (uint32_t i = threadIdx.x; i < sizeof(Counters) / 4; i += blockDim.x) {
+      dst[i] = src[i];
+      src[i] = 0u;
+    }
+  }
+  const uint32_t q = threadIdx.x;
+  if (q < n) {
+    const volatile uint32_t* f = &mbox[me]->rep[slot][q].epoch;
+    const long long t0 = clock64();
+    while (*f != epoch) {
+      __nanosleep(200);
+      if (clock64() - t0 > kSpinCycles) {
+        atomicExch(err, 1u);
+        break;
+      }
+    }
+  }
+  __threadfence();
+  __syncthreads();
+  const uint32_t words = n * (uint32_t)(sizeof(DevReport) / 4);
+  const volatile uint32_t* src = reinterpret_cast<const volatile uint32_t*>(mbox[me]->rep[slot]);
+  volatile uint32_t* dst = reinterpret_cast<volatile uint32_t*>(host_out);
+  for (uint32_t i = threadIdx.x; i < words; i += blockDim.x) dst[i] = src[i];
 }
 
 // merge (engine.hpp:823-852): combine every received record; an accepted
@@ -431,6 +528,12 @@ void run_primitive(Plan& P, Prim& prim, const mg_config& cfg) {
   }
   trace("workers prepared");
   if (P.shm) fabric_sync(P);  // collective: map peers' (possibly regrown) arenas
+  const bool dev_fabric = P.shm && P.device_fabric;
+  uint32_t* mp_err = dev_fabric ? reinterpret_cast<uint32_t*>(P.host_reports_dev + kMaxMpRanks)
+                                : nullptr;
+  uint32_t* mp_err_host = dev_fabric ? reinterpret_cast<uint32_t*>(P.host_reports + kMaxMpRanks)
+                                     : nullptr;
+  if (dev_fabric) *reinterpret_cast<volatile uint32_t*>(mp_err_host) = 0;
   build_send_tables(P);
   trace("send tables");
   P.h_matrix.assign(n, std::vector<uint64_t>(n, 0));
@@ -482,6 +585,7 @@ void run_primitive(Plan& P, Prim& prim, const mg_config& cfg) {
   for (uint64_t iter = 0;; ++iter) {
     const GlobalView* prev = rs.views.empty() ? nullptr : &rs.views.back();
     const uint32_t parity = iter & 1u;
+    if (dev_fabric) ++P.mp_epoch;  // same sequence on every rank (same decisions)
     std::vector<int> step_comm(n, comm);
     // body + split/pack + publish
     for (uint32_t p : P.local_workers) {
@@ -532,12 +636,18 @@ void run_primitive(Plan& P, Prim& prim, const mg_config& cfg) {
       });
       if (n > 1) {
         MGB_LAUNCH(publish_kernel, 1, 64, 0, w.stream, w.ctr.ptr, w.send_cnt_ptr.ptr + parity * n,
-                   n, p);
+                   n, p, dev_fabric ? P.mbox_ptrs.ptr : nullptr, parity, P.mp_epoch);
         MGB_CUDA(cudaEventRecord(w.ev_x1, w.stream));
       }
       MGB_CUDA(cudaEventRecord(rs.packed[p], w.stream));
     }
-    if (P.shm) {
+    if (dev_fabric) {
+      // peers in other processes: wait on the device for their publish flags
+      Worker& w = *P.workers[P.rank];
+      DeviceGuard dg(w.dev);
+      MGB_LAUNCH(mp_wait_pub_kernel, 1, 32, 0, w.stream,
+                 reinterpret_cast<Mailbox*>(P.mbox.ptr), parity, P.mp_epoch, n, P.rank, mp_err);
+    } else if (P.shm) {
       // peers in other processes: their pack + publish kernels must have
       // completed (system-scope fenced) before this rank merges (E:922)
       for (uint32_t p : P.local_workers) MGB_CUDA(cudaStreamSynchronize(P.workers[p]->stream));
@@ -563,7 +673,18 @@ void run_primitive(Plan& P, Prim& prim, const mg_config& cfg) {
         });
       }
       prim.after_merge(c);
-      MGB_LAUNCH(report_kernel, 1, 128, 0, w.stream, w.ctr.ptr, w.host_ctr_dev);
+      if (dev_fabric) {
+        HostReportPart hp{};
+        for (int k = 0; k < 4; ++k) {
+          hp.f[k] = c.report.f[k];
+          hp.u[k] = c.report.u[k];
+        }
+        hp.next_is_out = 0;
+        MGB_LAUNCH(mp_report_kernel, 1, 128, 0, w.stream, w.ctr.ptr, w.host_ctr_dev, hp,
+                   P.mbox_ptrs.ptr, n, P.rank, P.mp_epoch, P.host_reports_dev, mp_err);
+      } else {
+        MGB_LAUNCH(report_kernel, 1, 128, 0, w.stream, w.ctr.ptr, w.host_ctr_dev);
+      }
     }
     // barrier + completion (E:940, E:784-820)
     GlobalView view;
@@ -614,8 +735,30 @@ void run_primitive(Plan& P, Prim& prim, const mg_config& cfg) {
       std::vector<WorkerReport> reports;
       std::vector<std::vector<uint32_t>> sends;
       bool overflow = false;
-      fabric_exchange_reports(P, view.reports[me], *P.workers[me]->host_ctr, reports, sends,
-                              overflow);
+      if (dev_fabric) {  // gathered on the devices by mp_report_kernel
+        if (*reinterpret_cast<volatile uint32_t*>(mp_err_host))
+          throw Error(MG_EWORKER, "fabric: a peer rank did not arrive within the timeout");
+        reports.assign(n, WorkerReport{});
+        sends.assign(n, std::vector<uint32_t>(n, 0));
+        for (uint32_t q = 0; q < n; ++q) {
+          const DevReport& d = P.host_reports[q];
+          if (d.epoch != P.mp_epoch) throw Error(MG_EWORKER, "fabric: stale report");
+          WorkerReport& x = reports[q];
+          x.out_frontier = d.out_frontier;
+          x.next_frontier = d.next_frontier;
+          x.edges_delta = d.edges_delta;
+          x.combine_delta = d.combine_delta;
+          for (int k = 0; k < 4; ++k) {
+            x.f[k] = d.f[k];
+            x.u[k] = d.u[k];
+          }
+          for (uint32_t e = 0; e < n; ++e) sends[q][e] = d.send_cnt[e];
+          overflow |= d.overflow != 0;
+        }
+      } else {
+        fabric_exchange_reports(P, view.reports[me], *P.workers[me]->host_ctr, reports, sends,
+                                overflow);
+      }
       if (overflow) throw Error(MG_EWORKER, "inbox overflow on a peer worker");
       view.reports = reports;
       it_edges = it_comb = 0;

@@ -26,7 +26,6 @@ void device_rmat_csr(int dev, int scale, int ef, uint64_t seed, int with_w, uint
 
 namespace {
 
-constexpr uint32_t kMaxMpRanks = 32;  // 96 B of slot layout per rank in a 4 KiB blob
 
 struct SlotOff {
   uint64_t ids, va[kMaxAssoc], vv[kMaxAssoc], cap;
@@ -37,6 +36,7 @@ struct AttachBlob {
   uint32_t has_arena, pad;
   cudaIpcMemHandle_t arena;
   cudaIpcMemHandle_t cnt;
+  cudaIpcMemHandle_t mbox;
   SlotOff slots[2][kMaxMpRanks];  // [parity][src] in this rank's arena
 };
 static_assert(sizeof(AttachBlob) <= ShmFabric::kBlobBytes, "attach blob too large");
@@ -60,8 +60,20 @@ void fabric_sync(Plan& P) {
   const uint32_t n = P.n, me = P.rank;
   Worker& w = *P.workers[me];
   DeviceGuard dg(w.dev);
+  if (!P.mbox.ptr) {  // device-side protocol state, once per plan
+    P.mbox.alloc(sizeof(Mailbox));
+    MGB_CUDA(cudaMemset(P.mbox.ptr, 0, sizeof(Mailbox)));
+    MGB_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&P.host_reports),
+                           sizeof(DevReport) * (kMaxMpRanks + 1),
+                           cudaHostAllocMapped | cudaHostAllocPortable));
+    std::memset(P.host_reports, 0, sizeof(DevReport) * (kMaxMpRanks + 1));
+    MGB_CUDA(cudaHostGetDevicePointer(reinterpret_cast<void**>(&P.host_reports_dev),
+                                      P.host_reports, 0));
+    P.device_fabric = getenv("MG_HOST_FABRIC") == nullptr;
+  }
   AttachBlob mine;
   std::memset(&mine, 0, sizeof(mine));
+  MGB_CUDA(cudaIpcGetMemHandle(&mine.mbox, P.mbox.ptr));
   mine.gen = w.arena_gen;
   mine.has_arena = w.arena.ptr ? 1 : 0;
   if (w.arena.ptr) MGB_CUDA(cudaIpcGetMemHandle(&mine.arena, w.arena.ptr));
@@ -84,12 +96,15 @@ void fabric_sync(Plan& P) {
     P.peer_cnt.assign(n, nullptr);
     P.peer_gen.assign(n, ~0ull);
     P.peer_slots.assign(2 * n, SlotView{});
+    P.peer_mbox.assign(n, nullptr);
   }
   for (uint32_t q = 0; q < n; ++q) {
     if (q == me) continue;
     const AttachBlob& b = all[q];
     if (!P.peer_cnt[q])
       MGB_CUDA(cudaIpcOpenMemHandle(&P.peer_cnt[q], b.cnt, cudaIpcMemLazyEnablePeerAccess));
+    if (!P.peer_mbox[q])
+      MGB_CUDA(cudaIpcOpenMemHandle(&P.peer_mbox[q], b.mbox, cudaIpcMemLazyEnablePeerAccess));
     if (P.peer_gen[q] != b.gen) {
       if (P.peer_arena[q]) MGB_CUDA(cudaIpcCloseMemHandle(P.peer_arena[q]));
       P.peer_arena[q] = nullptr;
@@ -112,6 +127,13 @@ void fabric_sync(Plan& P) {
       }
       P.peer_slots[par * n + q] = v;
     }
+  }
+  if (!P.mbox_ptrs.ptr) {
+    std::vector<Mailbox*> ptrs(n);
+    for (uint32_t q = 0; q < n; ++q)
+      ptrs[q] = reinterpret_cast<Mailbox*>(q == me ? (void*)P.mbox.ptr : P.peer_mbox[q]);
+    P.mbox_ptrs.upload(ptrs.data(), n, w.stream);
+    MGB_CUDA(cudaStreamSynchronize(w.stream));
   }
 }
 

@@ -70,6 +70,11 @@ void plan_free(Plan* P) {
     if (P->peer_arena[i]) cudaIpcCloseMemHandle(P->peer_arena[i]);
   for (size_t i = 0; i < P->peer_cnt.size(); ++i)
     if (P->peer_cnt[i]) cudaIpcCloseMemHandle(P->peer_cnt[i]);
+  for (size_t i = 0; i < P->peer_mbox.size(); ++i)
+    if (P->peer_mbox[i]) cudaIpcCloseMemHandle(P->peer_mbox[i]);
+  P->mbox.free_();
+  P->mbox_ptrs.free_();
+  if (P->host_reports) cudaFreeHost(P->host_reports);
   P->g_off.free_(); P->g_col.free_(); P->g_w.free_();
   delete P;
 }

@@ -69,6 +69,29 @@ struct Counters {
   uint32_t recv_cnt[kMaxWorkers];  // records received from each source (merge)
 };
 
+// ---------------------------------------------------------------------------
+// device-side superstep protocol of multi-process plans (one rank per GPU):
+// every rank owns a Mailbox in its HBM, mapped by its peers over CUDA IPC.
+// Peers store their publish flags and their superstep reports into it, so the
+// "records delivered" barrier and the WorkerReport all-gather + convergence
+// test (engine.hpp:449-473, :784-820) run on the devices; the host only
+// synchronises its own stream once per superstep.
+constexpr uint32_t kMaxMpRanks = 32;
+
+struct DevReport {  // WorkerReport + per-destination send counts, one rank, one superstep
+  unsigned long long out_frontier, next_frontier, edges_delta, combine_delta;
+  double f[4];
+  unsigned long long u[4];
+  uint32_t send_cnt[kMaxMpRanks];
+  uint32_t overflow;
+  uint32_t epoch;  // written last (volatile store): the report's arrival flag
+};
+
+struct Mailbox {
+  uint32_t pub[2][kMaxMpRanks];   // [parity][src]: epoch whose records src delivered
+  DevReport rep[2][kMaxMpRanks];  // [epoch parity][src]
+};
+
 struct Worker {
   uint32_t p = 0;
   int dev = 0;
@@ -184,6 +207,15 @@ struct Plan {
   std::vector<void*> peer_cnt;       // mapped inbox counters of peers
   std::vector<uint64_t> peer_gen;    // arena generation each mapping belongs to
   std::vector<SlotView> peer_slots;  // [2][n]: peer q's slot for records from this rank
+  // device-side protocol (default for multi-process plans; MG_HOST_FABRIC=1
+  // selects the shared-memory barrier + all-gather instead)
+  bool device_fabric = true;
+  DevArray<uint8_t> mbox;              // this rank's Mailbox
+  std::vector<void*> peer_mbox;        // mapped peer mailboxes
+  DevArray<Mailbox*> mbox_ptrs;        // [n]: every rank's Mailbox (own included)
+  DevReport* host_reports = nullptr;   // mapped pinned: [kMaxMpRanks] + error word
+  DevReport* host_reports_dev = nullptr;
+  uint32_t mp_epoch = 0;               // superstep counter, identical on every rank
 };
 
 struct WorkerReport;

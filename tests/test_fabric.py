@@ -74,8 +74,10 @@ def test_fabric_rejects_bad_arguments():
         mg.PartitionPlan.multiprocess(g, np.array([0, 0, 1, 1], np.uint32), 2, 5, 0, "k")
 
 
-def _gpu_worker(rank, world, port, q, case):
+def _gpu_worker(rank, world, port, q, case, fabric="device"):
     sys.path.insert(0, ROOT)
+    if fabric == "host":  # shared-memory barrier + all-gather instead of device mailboxes
+        os.environ["MG_HOST_FABRIC"] = "1"
     try:
         import torch.distributed as dist
 
@@ -120,9 +122,12 @@ def _gpu_worker(rank, world, port, q, case):
 
 
 @pytest.mark.gpu
-def test_two_processes_one_gpu_cuda_ipc_exchange():
+@pytest.mark.parametrize("fabric", ["device", "host"])
+def test_two_processes_one_gpu_cuda_ipc_exchange(fabric):
+    """device: publish flags and WorkerReports through IPC-mapped mailboxes,
+    the barrier and the all-gather on the GPUs; host: the shm rendezvous"""
     import paper_1504_04804_b200 as mg
-    res = _spawn(_gpu_worker, 2, "rmat12")
+    res = _spawn(_gpu_worker, 2, "rmat12", fabric)
     assert all(rc == 0 for _, rc, _ in res), res
     outs = [o for _, _, o in res]
     for o in outs:
