@@ -327,12 +327,47 @@ __device__ __forceinline__ void warp_queue_append(BlockQueue<kCap>& q, const boo
 #define MG_PULL_GRID 4
 #endif
 
+#ifndef MG_ABLATE  // experiment switch: drop pieces of the pull kernel to price them
+#define MG_ABLATE 0
+#endif
 #ifndef MG_PULL_BITS_PLAIN
 #define MG_PULL_BITS_PLAIN 0
 #endif
 #ifndef MG_PULL_CNT32
 #define MG_PULL_CNT32 1
 #endif
+
+#ifndef MG_PULL_BITS_SMEM
+#define MG_PULL_BITS_SMEM 1
+#endif
+constexpr uint32_t kBitSlots = 64;  // per-warp shared words for the visited-bit merge
+
+// set the visited bits of the lanes' discoveries: the lanes OR their bits into
+// a per-warp shared window of words (shared atomics resolve same-word lanes in
+// hardware), then one lane per distinct word issues the global atomicOr.
+// Records are sorted, so a warp's discoveries fall in a few adjacent words; a
+// lane outside the window (sparse lists) uses its own global atomic.
+__device__ __forceinline__ void warp_set_bits_smem(uint32_t* bits, uint32_t* win, bool pred,
+                                                   uint32_t v) {
+  const unsigned lane = lane_id();
+  const unsigned m = __ballot_sync(0xffffffffu, pred);
+  if (!m) return;
+  const uint32_t w0 = __shfl_sync(0xffffffffu, v >> 5, __ffs(m) - 1);
+  const uint32_t idx = (v >> 5) - w0;
+  const bool in = pred && idx < kBitSlots;
+  if (in) atomicOr(&win[idx], 1u << (v & 31));
+  else if (pred) atomicOr(&bits[v >> 5], 1u << (v & 31));
+  __syncwarp();
+  // the first lane of each word flushes it
+  const uint32_t wd = v >> 5;
+  const uint32_t pw = __shfl_up_sync(0xffffffffu, in ? wd : 0xFFFFFFFFu, 1);
+  const unsigned firsts = __ballot_sync(0xffffffffu, in && (lane == 0 || pw != wd));
+  if ((firsts >> lane) & 1u) {
+    atomicOr(&bits[wd], win[idx]);
+    win[idx] = 0u;
+  }
+  __syncwarp();
+}
 
 #if MG_PULL_BITS_PLAIN
 __device__ __forceinline__ void warp_set_bits(uint32_t* bits, bool pred, uint32_t v) {
@@ -398,6 +433,8 @@ __global__ void __launch_bounds__(256, MG_PULL_MINB)
   // overflow in the next chunk (one barrier per chunk otherwise)
   __shared__ BlockQueue<kPullQ> q_found, q_keep, q_long;
   __shared__ uint32_t s_found;
+  __shared__ uint32_t s_win[256 / 32][kBitSlots];  // visited-bit merge windows
+  for (uint32_t i = threadIdx.x; i < 8 * kBitSlots; i += blockDim.x) (&s_win[0][0])[i] = 0u;
   q_found.reset();
   q_keep.reset();
   q_long.reset();
@@ -439,7 +476,7 @@ __global__ void __launch_bounds__(256, MG_PULL_MINB)
       if (found[j]) {
         scanned += h0[j] ? 1 : 2;
 #if MG_PULL_STREAM
-        __stcs(&labels[v], next_label);
+        if (!(MG_ABLATE & 1)) __stcs(&labels[v], next_label);
 #else
         labels[v] = next_label;
 #endif
@@ -449,11 +486,17 @@ __global__ void __launch_bounds__(256, MG_PULL_MINB)
       } else if (open[j]) {
         scanned += d < (uint32_t)kPullK ? d : (uint32_t)kPullK;
       }
-      warp_set_bits(vis, found[j], v);
+#if MG_PULL_BITS_SMEM
+      if (!(MG_ABLATE & 2)) warp_set_bits_smem(vis, s_win[threadIdx.x >> 5], found[j], v);
+#else
+      if (!(MG_ABLATE & 2)) warp_set_bits(vis, found[j], v);
+#endif
     }
     if (emit_found) warp_queue_append<kPV>(q_found, found, vv);
-    warp_queue_append<kPV>(q_keep, keep, pos);
-    warp_queue_append<kPV>(q_long, lng, pos);
+    if (!(MG_ABLATE & 4)) {
+      warp_queue_append<kPV>(q_keep, keep, pos);
+      warp_queue_append<kPV>(q_long, lng, pos);
+    }
     __syncthreads();
     const bool last = base + gridDim.x * chunk >= nul;
     if (!MG_PULL_LAZY_FLUSH || last || q_found.n > kPullQ - chunk || q_keep.n > kPullQ - chunk ||
