@@ -486,12 +486,13 @@ __global__ void __launch_bounds__(256, MG_PULL_MINB)
       } else if (open[j]) {
         scanned += d < (uint32_t)kPullK ? d : (uint32_t)kPullK;
       }
-#if MG_PULL_BITS_SMEM
+#if MG_PULL_BITS_SMEM == 1
       if (!(MG_ABLATE & 2)) warp_set_bits_smem(vis, s_win[threadIdx.x >> 5], found[j], v);
-#else
+#elif MG_PULL_BITS_SMEM == 0
       if (!(MG_ABLATE & 2)) warp_set_bits(vis, found[j], v);
 #endif
     }
+
     if (emit_found) warp_queue_append<kPV>(q_found, found, vv);
     if (!(MG_ABLATE & 4)) {
       warp_queue_append<kPV>(q_keep, keep, pos);
