@@ -354,8 +354,9 @@ class BufferStats:
 class RunStats:
     """RunStats (engine.hpp:261-298)"""
 
-    def __init__(self, plan: PartitionPlan, st):
+    def __init__(self, plan: PartitionPlan, st, primitive="?"):
         n = st.n
+        self.primitive = primitive
         self.n = n
         self.supersteps = st.supersteps
         self.edges_examined = st.edges_examined
@@ -396,6 +397,26 @@ class RunStats:
 
     def h_total(self):
         return int(self.h_matrix.sum())
+
+    def to_json(self, partitioner="unspecified", duplication="all", h_inflation=1):
+        """the reference's RunStats JSON document (stats_json.hpp:28-61), same keys"""
+        return {
+            "primitive": self.primitive, "n": int(self.n), "partitioner": partitioner,
+            "duplication": duplication, "communication": self.communication,
+            "policy": self.policy, "S": int(self.supersteps), "W": int(self.edges_examined),
+            "C": int(self.combine_ops), "H": self.h_matrix.astype(int).tolist(),
+            "H_total": self.h_total(),
+            "H_per_iter_by_src": self.h_per_iter_by_src.astype(int).tolist(),
+            "out_per_iter": self.out_per_iter.astype(int).tolist(),
+            "edges_per_iter": self.edges_per_iter.astype(int).tolist(),
+            "wall_ms": float(self.wall_ms), "exchange_ms": float(self.exchange_ms),
+            "h_inflation": int(h_inflation), "wire_records": int(self.wire_records),
+            "stop_reason": self.stop_reason, "peak_bytes": int(self.peak_bytes),
+            "reallocs": int(self.reallocs),
+            "buffers": [{role: {"reallocs": int(b.realloc_count), "peak_items": int(b.peak_items),
+                                "peak_bytes": int(b.peak_bytes)} for role, b in wb.items()}
+                        for wb in self.worker_buffers],
+        }
 
     def h_from(self, i):
         return int(self.h_matrix[i].sum())
@@ -440,7 +461,7 @@ def bfs(plan: PartitionPlan, opt: BfsOptions = BfsOptions(), cfg: EngineConfig =
     _check(lib().mg_bfs(plan._h, opt.source, int(opt.mark_preds), C.byref(_cfg(cfg)), _p(labels),
                         _p(preds), C.byref(st)))
     r = Result()
-    r.labels, r.preds, r.stats = labels, preds, RunStats(plan, st)
+    r.labels, r.preds, r.stats = labels, preds, RunStats(plan, st, "bfs")
     return r
 
 
@@ -457,7 +478,7 @@ def dobfs(plan: PartitionPlan, opt: DobfsOptions = DobfsOptions(), cfg: EngineCo
                           C.byref(_cfg(cfg)), _p(labels), _p(preds), _p(dl), len(dl), C.byref(ln),
                           C.byref(fw), C.byref(bw), C.byref(st)))
     r = Result()
-    r.labels, r.preds, r.stats = labels, preds, RunStats(plan, st)
+    r.labels, r.preds, r.stats = labels, preds, RunStats(plan, st, "dobfs")
     r.direction_log = dl[:ln.value].copy()
     r.forward_edges, r.backward_edges = fw.value, bw.value
     return r
@@ -484,7 +505,7 @@ def sssp(plan: PartitionPlan, source=0, mark_preds=False, cfg: EngineConfig = No
     _check(lib().mg_sssp(plan._h, source, int(mark_preds), C.byref(_cfg(cfg)), _p(d), _p(preds),
                          C.byref(st)))
     r = Result()
-    r.dists, r.preds, r.stats = d, preds, RunStats(plan, st)
+    r.dists, r.preds, r.stats = d, preds, RunStats(plan, st, "sssp")
     return r
 
 
@@ -494,7 +515,7 @@ def cc(plan: PartitionPlan, cfg: EngineConfig = None, download=True):
     st = abi.mg_stats()
     _check(lib().mg_cc(plan._h, C.byref(_cfg(cfg)), _p(comp), C.byref(st)))
     r = Result()
-    r.components, r.stats = comp, RunStats(plan, st)
+    r.components, r.stats = comp, RunStats(plan, st, "cc")
     return r
 
 
@@ -507,7 +528,7 @@ def bc(plan: PartitionPlan, source=0, cfg: EngineConfig = None, download=True):
     st = abi.mg_stats()
     _check(lib().mg_bc(plan._h, source, C.byref(_cfg(cfg)), _p(b), _p(s), _p(lab), C.byref(st)))
     r = Result()
-    r.bc, r.sigma, r.labels, r.stats = b, s, lab, RunStats(plan, st)
+    r.bc, r.sigma, r.labels, r.stats = b, s, lab, RunStats(plan, st, "bc")
     return r
 
 
@@ -524,7 +545,7 @@ def pagerank(plan: PartitionPlan, opt: PrOptions = PrOptions(), cfg: EngineConfi
                              _p(ranks), C.byref(it), _p(sums), cap, C.byref(ln), C.byref(st)))
     r = Result()
     r.ranks, r.iterations, r.rank_sums = ranks, it.value, sums[:ln.value].copy()
-    r.stats = RunStats(plan, st)
+    r.stats = RunStats(plan, st, "pagerank")
     return r
 
 

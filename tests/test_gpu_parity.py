@@ -363,3 +363,20 @@ def test_drop_package_fault_injection_changes_h():
                mg.EngineConfig(drop_package=mg.DropPackage(0, 1, 1)))
     assert r.stats.h_matrix[0][1] == 0  # the only 0->1 package was dropped
     assert r.labels[2] == mg.kInfLabel
+
+
+def test_run_stats_json_has_the_reference_schema():
+    """RunStats.to_json mirrors stats_json.hpp:28-61 key for key"""
+    import json
+    g = mg.Csr.rmat(10, 8, 3)
+    plan, _ = plan_for(g, 2, 5)
+    r = mg.bfs(plan, mg.BfsOptions(source=0))
+    j = r.stats.to_json(partitioner="random", duplication="all")
+    assert set(j) == {"primitive", "n", "partitioner", "duplication", "communication", "policy",
+                      "S", "W", "C", "H", "H_total", "H_per_iter_by_src", "out_per_iter",
+                      "edges_per_iter", "wall_ms", "exchange_ms", "h_inflation",
+                      "wire_records", "stop_reason", "peak_bytes", "reallocs", "buffers"}
+    assert j["primitive"] == "bfs" and j["n"] == 2 and j["S"] == r.stats.supersteps
+    assert j["H_total"] == sum(map(sum, j["H"])) == r.stats.h_total()
+    assert len(j["buffers"]) == 2
+    json.dumps(j)  # serialisable
