@@ -1099,18 +1099,28 @@ __global__ void cc_jump_kernel(uint32_t* comp, uint32_t nv) {
 }
 
 // delta encoding: emit local vertices whose value changed since the snapshot
-__global__ void cc_delta_kernel(uint32_t* comp, uint32_t* snapshot, uint32_t nv, uint32_t* out,
-                                Counters* ctr) {
+// (CTA-aggregated appends: one global atomic per CTA round; with
+// write_list == 0 the changed vertices are only counted)
+__global__ void __launch_bounds__(256)
+    cc_delta_kernel(uint32_t* comp, uint32_t* snapshot, uint32_t nv, uint32_t* out,
+                    Counters* ctr, int write_list) {
+  using Scan = cub::BlockScan<uint32_t, 256>;
+  __shared__ typename Scan::TempStorage tmp;
+  __shared__ uint32_t s_base;
   for (uint32_t base = blockIdx.x * blockDim.x; base < nv; base += gridDim.x * blockDim.x) {
     uint32_t w = base + threadIdx.x;
-    bool ch = false;
+    uint32_t ch = 0;
     if (w < nv) {
       uint32_t c = comp[w];
       ch = c != snapshot[w];
       if (ch) snapshot[w] = c;
     }
-    uint32_t slot = warp_append(&ctr->out_cnt, ch);
-    if (ch) out[slot] = w;
+    uint32_t excl, total;
+    Scan(tmp).ExclusiveSum(ch, excl, total);
+    if (threadIdx.x == 0) s_base = total ? atomicAdd(&ctr->out_cnt, total) : 0u;
+    __syncthreads();
+    if (ch && write_list) out[s_base + excl] = w;
+    __syncthreads();
   }
 }
 
@@ -1147,6 +1157,79 @@ __global__ void __launch_bounds__(256)
     }
   }
   if (__any_sync(0xffffffffu, any) && lane_id() == 0) *hooked = 1;
+}
+
+// --- sampled hooking (Afforest-style) for a symmetric single partition -----
+// 1. link every vertex to its first kCcLink neighbours, compress;
+// 2. sample roots, the most frequent one is the giant component's;
+// 3. hook sweeps over the arcs of the vertices NOT in the giant (after step 1)
+//    until no hook.  On a symmetric graph every arc between the giant and
+//    another tree is also an arc of the other tree's vertex, so skipping the
+//    giant's rows loses no union; the fixpoint (every set's minimum) is the
+//    same as the reference's full sweeps, so labels are identical.
+constexpr uint32_t kCcLink = 2;
+constexpr uint32_t kCcSamples = 1024;
+
+__global__ void __launch_bounds__(256)
+    cc_link_kernel(const uint32_t* __restrict__ toff, const uint32_t* __restrict__ tcol,
+                   uint32_t nv, uint32_t* comp) {
+  for (uint32_t u = blockIdx.x * blockDim.x + threadIdx.x; u < nv; u += gridDim.x * blockDim.x) {
+    const uint32_t b = toff[u], e = toff[u + 1];
+    for (uint32_t k = b; k < e && k < b + kCcLink; ++k) {
+      uint32_t ru = cc_root(comp, u), rv = cc_root(comp, __ldg(&tcol[k]));
+      if (ru == rv) continue;
+      atomicMin(&comp[ru > rv ? ru : rv], ru < rv ? ru : rv);
+    }
+  }
+}
+
+__global__ void cc_sample_kernel(const uint32_t* comp, uint32_t nv, uint32_t* out) {
+  const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < kCcSamples) out[i] = comp[(uint32_t)(((uint64_t)i * 2654435761ull) % nv)];
+}
+
+__global__ void __launch_bounds__(256)
+    cc_hook_rest_kernel(const uint32_t* __restrict__ toff, const uint32_t* __restrict__ tcol,
+                        uint32_t nv, const uint32_t* __restrict__ comp0, uint32_t giant,
+                        uint32_t* comp, uint32_t* hooked, unsigned long long* scanned_out) {
+  const unsigned sub = threadIdx.x & (kCcGroup - 1);
+  const uint32_t groups = gridDim.x * (blockDim.x / kCcGroup);
+  bool any = false;
+  uint32_t scanned = 0;
+  for (uint32_t u = blockIdx.x * (blockDim.x / kCcGroup) + threadIdx.x / kCcGroup; u < nv;
+       u += groups) {
+    if (comp0[u] == giant) continue;
+    const uint32_t b = toff[u], e = toff[u + 1];
+    if (sub == 0) scanned += e - b;
+    for (uint32_t k = b + sub; k < e; k += kCcGroup) {
+      uint32_t ru = cc_root(comp, u), rv = cc_root(comp, __ldg(&tcol[k]));
+      if (ru == rv) continue;
+      atomicMin(&comp[ru > rv ? ru : rv], ru < rv ? ru : rv);
+      any = true;
+    }
+  }
+  if (__any_sync(0xffffffffu, any) && lane_id() == 0) *hooked = 1;
+  warp_add_u64(scanned_out, scanned);
+}
+
+// is the (ordered) transpose symmetric?  every arc (u <- v) needs (v <- u):
+// a binary search in v's sorted row; any miss clears *sym
+__global__ void __launch_bounds__(256)
+    cc_symmetric_kernel(const uint32_t* __restrict__ toff, const uint32_t* __restrict__ tcol,
+                        uint32_t nv, uint32_t* sym) {
+  const uint32_t warps = gridDim.x * blockDim.x / 32;
+  for (uint32_t u = (blockIdx.x * blockDim.x + threadIdx.x) / 32; u < nv; u += warps) {
+    for (uint32_t k = toff[u] + lane_id(); k < toff[u + 1]; k += 32) {
+      const uint32_t v = tcol[k];
+      uint32_t lo = toff[v], hi = toff[v + 1];
+      while (lo < hi) {
+        const uint32_t m = (lo + hi) >> 1;
+        if (tcol[m] < u) lo = m + 1;
+        else hi = m;
+      }
+      if (lo == toff[v + 1] || tcol[lo] != u) *sym = 0u;
+    }
+  }
 }
 
 // labels back in vertex IDs: the component label is its smallest vertex ID.
@@ -1186,11 +1269,12 @@ __global__ void __launch_bounds__(256)
   __syncthreads();
   if (threadIdx.x == 0) atomicMin(&minid[s_root], s_min);
 }
+// gather form: coalesced writes in vertex order, random reads of comp_p
 __global__ void cc_labels_kernel(const uint32_t* __restrict__ comp_p,
-                                 const uint32_t* __restrict__ iperm,
+                                 const uint32_t* __restrict__ perm,
                                  const uint32_t* __restrict__ minid, uint32_t n, uint32_t* comp) {
-  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
-    comp[iperm[i]] = minid[comp_p[i]];
+  for (uint32_t v = blockIdx.x * blockDim.x + threadIdx.x; v < n; v += gridDim.x * blockDim.x)
+    comp[v] = minid[comp_p[perm[v]]];
 }
 
 struct CcPrim : PrimBase {
@@ -1235,6 +1319,17 @@ struct CcPrim : PrimBase {
     uint64_t scanned = 0;
     const uint64_t local_edges = w.ne;  // every hosted arc once per hook pass
     uint32_t* comp = comp_arr(w);
+    if (ordered && c.P->n == 1) {
+      // one partition receives nothing, so superstep 0's fixpoint is final
+      if (c.iter == 0) {
+        if (symmetric(w)) {
+          sampled_fixpoint(c, comp);
+          h = 0;
+        }
+      } else {
+        h = 0;
+      }
+    }
     while (h) {
       MGB_CUDA(cudaMemsetAsync(hooked, 0, 4, w.stream));
       if (ordered)
@@ -1252,8 +1347,9 @@ struct CcPrim : PrimBase {
     }
     c.ensure_output(w.nv);
     if (w.nv)
-      MGB_LAUNCH(cc_delta_kernel, grid_for(w.nv, 256, kNumSMs * 16), 256, 0, w.stream, comp,
-                 w.su32[1].ptr, w.nv, w.output.ptr, c.ctr());
+      MGB_LAUNCH(cc_delta_kernel, grid_for(w.nv, 256, kNumSMs * 8), 256, 0, w.stream, comp,
+                 w.su32[1].ptr, w.nv, w.output.ptr, c.ctr(),
+                 (c.P->n > 1 || c.want_deg) ? 1 : 0);  // one partition: only the count is read
     add_edges(c, scanned);
   }
   void finalize(Ctx& c, const GlobalView&) {
@@ -1263,9 +1359,62 @@ struct CcPrim : PrimBase {
     MGB_LAUNCH(cc_min_id_kernel, grid_for(w.nv, 256, kNumSMs * 4), 256, 0, w.stream,
                w.aux[5].ptr, w.pr_iperm.ptr, w.nv, w.su32[1].ptr);
     MGB_LAUNCH(cc_labels_kernel, grid_for(w.nv, 256, kNumSMs * 8), 256, 0, w.stream,
-               w.aux[5].ptr, w.pr_iperm.ptr, w.su32[1].ptr, w.nv, w.su32[0].ptr);
+               w.aux[5].ptr, w.pr_perm.ptr, w.su32[1].ptr, w.nv, w.su32[0].ptr);
   }
   static void add_edges(Ctx& c, uint64_t k);
+  // plan lifetime: is the ordered transpose symmetric (sampled hooking valid)?
+  static bool symmetric(Worker& w) {
+    if (w.cc_symmetric < 0) {
+      DevArray<uint32_t> f;
+      f.alloc(1);
+      uint32_t one = 1;
+      MGB_CUDA(cudaMemcpy(f.ptr, &one, 4, cudaMemcpyHostToDevice));
+      MGB_LAUNCH(cc_symmetric_kernel, grid_for((uint64_t)w.nv * 32, 256, kNumSMs * 16), 256, 0,
+                 w.stream, w.toff.ptr, w.tcol.ptr, w.nv, f.ptr);
+      MGB_CUDA(cudaMemcpyAsync(&one, f.ptr, 4, cudaMemcpyDeviceToHost, w.stream));
+      MGB_CUDA(cudaStreamSynchronize(w.stream));
+      w.cc_symmetric = one ? 1 : 0;
+    }
+    return w.cc_symmetric == 1;
+  }
+  void sampled_fixpoint(Ctx& c, uint32_t* comp) {
+    Worker& w = *c.w;
+    const unsigned g = grid_for(w.nv, 256, kNumSMs * 16);
+    MGB_LAUNCH(cc_link_kernel, g, 256, 0, w.stream, w.toff.ptr, w.tcol.ptr, w.nv, comp);
+    MGB_LAUNCH(cc_jump_kernel, g, 256, 0, w.stream, comp, w.nv);
+    if (w.aux[4].n < w.nv || !w.aux[4].ptr) w.aux[4].alloc(w.nv);  // roots after linking
+    if (w.aux[3].n < kCcSamples || !w.aux[3].ptr) w.aux[3].alloc(kCcSamples);
+    MGB_CUDA(cudaMemcpyAsync(w.aux[4].ptr, comp, 4ull * w.nv, cudaMemcpyDeviceToDevice,
+                             w.stream));
+    MGB_LAUNCH(cc_sample_kernel, kCcSamples / 256, 256, 0, w.stream, comp, w.nv, w.aux[3].ptr);
+    std::vector<uint32_t> smp(kCcSamples);
+    MGB_CUDA(cudaMemcpyAsync(smp.data(), w.aux[3].ptr, 4ull * kCcSamples,
+                             cudaMemcpyDeviceToHost, w.stream));
+    MGB_CUDA(cudaStreamSynchronize(w.stream));
+    std::sort(smp.begin(), smp.end());
+    uint32_t giant = smp[0], best = 0;
+    for (size_t i = 0; i < smp.size();) {
+      size_t j = i;
+      while (j < smp.size() && smp[j] == smp[i]) ++j;
+      if (j - i > best) {
+        best = (uint32_t)(j - i);
+        giant = smp[i];
+      }
+      i = j;
+    }
+    uint32_t* hooked = w.su32[3].ptr;
+    // arcs examined: kCcLink per vertex in the link pass, then the rest passes
+    CcPrim::add_edges(c, (uint64_t)w.nv * kCcLink < w.ne ? (uint64_t)w.nv * kCcLink : w.ne);
+    for (uint32_t h = 1; h;) {
+      MGB_CUDA(cudaMemsetAsync(hooked, 0, 4, w.stream));
+      MGB_LAUNCH(cc_hook_rest_kernel, grid_for((uint64_t)w.nv * kCcGroup, 256, kNumSMs * 16),
+                 256, 0, w.stream, w.toff.ptr, w.tcol.ptr, w.nv, w.aux[4].ptr, giant, comp,
+                 hooked, &c.ctr()->edges);
+      MGB_LAUNCH(cc_jump_kernel, g, 256, 0, w.stream, comp, w.nv);
+      MGB_CUDA(cudaMemcpyAsync(&h, hooked, 4, cudaMemcpyDeviceToHost, w.stream));
+      MGB_CUDA(cudaStreamSynchronize(w.stream));
+    }
+  }
 };
 
 __global__ void add_u64_kernel(unsigned long long* dst, unsigned long long v) { *dst += v; }
