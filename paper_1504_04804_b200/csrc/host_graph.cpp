@@ -438,4 +438,15 @@ std::vector<uint32_t> bfs_locality_order(const uint32_t* off, const uint32_t* co
   return perm;
 }
 
+// byte levels -> u32 labels (255 -> kInvalid = the unreached label), the host
+// half of the split label download; cloned for AVX2 where the CPU has it
+__attribute__((target_clones("avx2", "default"))) void widen_labels_u8(const uint8_t* src,
+                                                                         uint32_t* dst,
+                                                                         size_t n) {
+  for (size_t i = 0; i < n; ++i) {
+    const uint32_t v = src[i];
+    dst[i] = v == 255u ? kInvalid : v;
+  }
+}
+
 }  // namespace mgb

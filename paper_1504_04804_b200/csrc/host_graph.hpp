@@ -10,6 +10,7 @@
 // reference built in oracle/_ref.
 #pragma once
 
+#include <cstddef>
 #include <cstdint>
 #include <stdexcept>
 #include <string>
@@ -76,6 +77,9 @@ struct HostPlan {
 };
 
 HostPlan build_plan(const HostCsr& g, const std::vector<uint32_t>& owner, uint32_t n, int dup);
+
+// u8 levels (255 = unreached) -> u32 labels (split label download, plan.cu)
+void widen_labels_u8(const uint8_t* src, uint32_t* dst, size_t n);
 
 // FIFO-BFS (Cuthill-McKee order without degree sort) vertex order: perm[old] = new
 std::vector<uint32_t> bfs_locality_order(const uint32_t* off, const uint32_t* col, uint32_t nv);

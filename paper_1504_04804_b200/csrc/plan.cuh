@@ -9,7 +9,11 @@
 // NVLink when the workers sit on different GPUs.
 #pragma once
 
+#include <condition_variable>
+#include <functional>
 #include <memory>
+#include <mutex>
+#include <thread>
 #include <vector>
 
 #include "common.cuh"
@@ -164,6 +168,25 @@ struct Worker {
   GraphView graph() const { return {nv, ne, off.ptr, col.ptr, w.ptr}; }
 };
 
+// persistent host worker threads (result widening); run() blocks until every
+// thread has run f(thread, threads)
+class HostPool {
+ public:
+  explicit HostPool(unsigned n);
+  ~HostPool();
+  void run(const std::function<void(unsigned, unsigned)>& f);
+
+ private:
+  unsigned n_;
+  std::vector<std::thread> threads_;
+  std::mutex m_;
+  std::condition_variable cv_, done_;
+  std::function<void(unsigned, unsigned)> job_;
+  uint64_t gen_ = 0;
+  unsigned pending_ = 0;
+  bool stop_ = false;
+};
+
 struct Plan {
   uint32_t n = 1;
   int dup = 0;
@@ -217,6 +240,11 @@ struct Plan {
   DevReport* host_reports = nullptr;   // mapped pinned: [kMaxMpRanks] + error word
   DevReport* host_reports_dev = nullptr;
   uint32_t mp_epoch = 0;               // superstep counter, identical on every rank
+  // split label download (gather_labels_u32)
+  uint8_t* label_stage = nullptr;      // pinned byte staging
+  uint64_t label_stage_n = 0;
+  DevArray<uint8_t> label_dev;
+  std::unique_ptr<HostPool> pool;
 };
 
 struct WorkerReport;

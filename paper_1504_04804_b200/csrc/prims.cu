@@ -17,6 +17,8 @@
 namespace mgb {
 
 void gather_u32(Plan& P, const std::vector<const uint32_t*>& pw, uint32_t* out);
+void gather_labels_u32(Plan& P, const std::vector<const uint32_t*>& pw, uint32_t* out,
+                       uint64_t max_label);
 void gather_u64(Plan& P, const std::vector<const unsigned long long*>& pw, uint64_t* out);
 void gather_f64(Plan& P, const std::vector<const double*>& pw, double* out);
 
@@ -2490,7 +2492,8 @@ int mg_bfs(mg_plan* plan, uint32_t source, int mark_preds, const mg_config* cfg,
     P.last = mg_stats{};
     run_primitive(P, prim, c);
     P.last_result_kind = 0;
-    gather_u32(P, pw(P, &Worker::su32, 0), labels);
+    // BFS levels: the largest label is S - 1 (CLI:339-346)
+    gather_labels_u32(P, pw(P, &Worker::su32, 0), labels, P.last.supersteps);
     if (mark_preds) gather_u32(P, pw(P, &Worker::su32, 1), preds);
     finish_stats(P, stats);
   });
@@ -2528,7 +2531,7 @@ int mg_dobfs(mg_plan* plan, uint32_t source, double do_a, double do_b, int mark_
     P.last = mg_stats{};
     run_primitive(P, prim, c);
     P.last_result_kind = 0;
-    gather_u32(P, pw(P, &Worker::su32, 0), labels);
+    gather_labels_u32(P, pw(P, &Worker::su32, 0), labels, P.last.supersteps);
     if (mark_preds) gather_u32(P, pw(P, &Worker::su32, 1), preds);
     if (len) *len = prim.dir_log.size();
     for (uint64_t i = 0; direction_log && i < prim.dir_log.size() && i < cap; ++i)

@@ -104,6 +104,10 @@ def test_c2_dobfs_rmat26_paths_agree():
         assert list(a.direction_log) == list(b.direction_log)
         assert a.stats.supersteps == b.stats.supersteps == c.stats.supersteps
         assert a.stats.edges_examined == b.stats.edges_examined  # W as the reference counts it
+        # the split download (bytes + host widening) equals a plain u32 fetch
+        if src == 4301304:
+            from paper_1504_04804_b200 import abi
+            assert np.array_equal(d.labels, plan.fetch(abi.MG_RES_LABELS, np.uint32))
         reached = a.labels != mg.kInfLabel
         assert a.labels[src] == 0 and int(a.labels[reached].max()) + 1 == a.stats.supersteps
 
