@@ -112,6 +112,32 @@ def test_c2_dobfs_rmat26_paths_agree():
         assert a.labels[src] == 0 and int(a.labels[reached].max()) + 1 == a.stats.supersteps
 
 
+def test_c2_dobfs_rmat24_parent_tree_is_legal():
+    """preds of the exact-cost DOBFS form a legal BFS tree (test_primitives.cpp:66-78
+    at scale): every reached v != s has label(pred) = label(v) - 1 and (pred, v)
+    is an arc — checked with a sorted (row, col) key search on the GPU"""
+    plan = mg.PartitionPlan.rmat_device(24, 16, 1)
+    off, col, _ = plan.download_graph().arrays()
+    exact = mg.EngineConfig(policy=mg.AllocPolicyKind.Maximum, fused=mg.FusedMode.On,
+                            dobfs_exact_cost=True)
+    r = mg.dobfs(plan, mg.DobfsOptions(source=0, mark_preds=True), exact)
+    arcs = Arcs(off, col)
+    lab = bfs_certificate(arcs, r.labels, 0)
+    pred = to_t(r.preds.astype(np.int64))
+    v = torch.nonzero(lab != INF).squeeze(1)
+    v = v[v != 0]
+    p = pred[v]
+    assert bool((p >= 0).all()) and bool((p < arcs.nv).all())
+    assert torch.equal(lab[p], lab[v] - 1), "parent not on the previous level"
+    keys = []
+    for rows, dst, _ in arcs.chunks():
+        keys.append(rows * arcs.nv + dst)
+    keys = torch.cat(keys)  # CSR order = sorted by (row, col)
+    q = p * arcs.nv + v
+    pos = torch.searchsorted(keys, q)
+    assert bool((pos < len(keys)).all()) and torch.equal(keys[pos], q), "parent arc missing"
+
+
 # --------------------------------------------------------------------------- C3
 def test_c3_sssp_rmat24_shortest_path_certificate():
     plan = mg.PartitionPlan.rmat_device(24, 16, 1, weights=(1, 64, 102))
