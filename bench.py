@@ -233,13 +233,16 @@ def run_ours(args, rank, world, local, workload):
         if world > 1:
             torch.distributed.barrier()
         torch.cuda.synchronize()
-        acc = {"dev_ms": 0.0, "pull": [0.0, 0.0, 0], "push": [0.0, 0.0, 0]}
+        acc = {"dev_ms": 0.0, "pull": [0.0, 0.0, 0], "push": [0.0, 0.0, 0], "xms": 0.0,
+               "xbytes": 0}
         l0 = mg.kernel_launch_count()
         clocks = Clocks(local)
         w0 = time.perf_counter()
         for s in steps:
             st = dobfs_stats(mg, plan, s, cfg, do_a, do_b)
             acc["dev_ms"] += st.device_ms
+            acc["xms"] += st.exchange_ms  # pack + publish kernels (records into peer HBM)
+            acc["xbytes"] += st.exchange_bytes
             for key, ms, b, n in (("pull", st.kernel_ms, st.kernel_bytes, st.kernel_launches),
                                   ("push", st.kernel2_ms, st.kernel2_bytes,
                                    st.kernel2_launches)):
@@ -357,6 +360,14 @@ def run_ours(args, rank, world, local, workload):
             "e2e": round(refsched["e2e"], 3),
             "note": "dobfs_exact_cost off: every superstep runs in the direction the reference "
                     "rule picks (push advance for forward steps)"},
+        "exchange": None if world == 1 else {
+            "bytes_per_step": main["xbytes"] / args.steps,
+            "pack_ms_per_step": round(main["xms"] / args.steps, 4),
+            "achieved": round(main["xbytes"] / (main["xms"] * 1e-3) / 1e9, 1) if main["xms"] else None,
+            "peak": 900.0, "unit": "GB/s",
+            "peak_kind": "NVLink 5 nominal per direction per GPU",
+            "note": "rank 0: record bytes its pack kernels stored into peer inboxes / their "
+                    "CUDA-event time (with every rank on one GPU this is HBM, not NVLink)"},
         "cpu_baseline": cpu,
         "clocks": clk,
         "gpu_launches": launches,
