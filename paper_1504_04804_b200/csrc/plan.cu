@@ -48,6 +48,7 @@ static void free_worker(Worker& w) {
   for (auto& a : w.ul_buf) a.free_();
   w.toff.free_(); w.tcol.free_(); w.tlong.free_();
   w.pr_perm.free_(); w.pr_pdeg.free_(); w.pr_iperm.free_();
+  w.bc_acc.free_();
   if (w.host_ctr) cudaFreeHost(w.host_ctr);
   if (w.stream) cudaStreamDestroy(w.stream);
   for (cudaEvent_t e : {w.ev_start, w.ev_end, w.ev_x0, w.ev_x1, w.ev_k0, w.ev_k1})

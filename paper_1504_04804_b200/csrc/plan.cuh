@@ -155,6 +155,7 @@ struct Worker {
   DevArray<uint32_t> pr_perm, pr_pdeg;  // vertex -> ordered position; out-degree by position
   DevArray<uint32_t> pr_iperm;          // ordered position -> vertex
   int cc_symmetric = -1;                // ordered transpose symmetric? (-1: not checked)
+  DevArray<double> bc_acc;              // BC: huge-row partial sums
   uint32_t n_nonisolated = 0;
   bool nonisolated_ready = false;
   std::vector<uint32_t> hosted_host;  // hosted local IDs (host copy)

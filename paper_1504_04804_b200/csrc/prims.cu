@@ -7,6 +7,7 @@
 // the per-vertex hooks with atomics whose outcome is independent of thread
 // order (atomicCAS / atomicMin / atomicExch stamps), so labels, distances and
 // components are bit-identical to the sequential reference.
+#include <cub/block/block_reduce.cuh>
 #include <cub/device/device_radix_sort.cuh>
 
 #include <cmath>
@@ -1621,7 +1622,90 @@ __global__ void __launch_bounds__(256)
 // long rows — so every backward superstep works on a contiguous slice
 // instead of rescanning all hosted vertices per level.  Per-CTA shared
 // histograms, one small scan (bucket-major), a scatter with shared cursors.
-constexpr uint32_t kBcBuckets = 2048;  // 2 * (max_level + 1) must fit
+constexpr uint32_t kBcBuckets = 2048;  // kBcClasses * (max_level + 1) must fit
+// row classes inside a level: thread rows, warp rows, and huge rows that are
+// cut into kBcChunk-arc chunks over many CTAs (a hub row of 1e6 arcs on one
+// warp left the GPU at 3.5% SM throughput for 2.7 ms)
+constexpr uint32_t kBcClasses = 3;
+#ifndef MG_BC_HUGE
+#define MG_BC_HUGE 8192
+#endif
+#ifndef MG_BC_CHUNK
+#define MG_BC_CHUNK 4096
+#endif
+constexpr uint32_t kBcHugeDeg = MG_BC_HUGE;
+constexpr uint32_t kBcChunk = MG_BC_CHUNK;
+__device__ __forceinline__ uint32_t bc_row_class(uint32_t deg) {
+  return deg < kBcWarpDeg ? 0u : (deg < kBcHugeDeg ? 1u : 2u);
+}
+
+// huge rows of a level: chunk prefix (one CTA; few rows), chunked sums with
+// one f64 atomic per chunk, then the per-row finish
+__global__ void __launch_bounds__(1024)
+    bc_huge_prefix_kernel(const uint32_t* __restrict__ rows, uint32_t n,
+                          const uint32_t* __restrict__ off, uint32_t* chunk_start,
+                          double* acc) {
+  using Scan = cub::BlockScan<uint32_t, 1024>;
+  __shared__ typename Scan::TempStorage tmp;
+  __shared__ uint32_t carry;
+  if (threadIdx.x == 0) carry = 0;
+  __syncthreads();
+  for (uint32_t base = 0; base < n; base += 1024) {
+    const uint32_t i = base + threadIdx.x;
+    uint32_t c = 0;
+    if (i < n) {
+      const uint32_t v = rows[i];
+      c = (off[v + 1] - off[v] + kBcChunk - 1) / kBcChunk;
+      acc[i] = 0.0;
+    }
+    uint32_t excl, total;
+    Scan(tmp).ExclusiveSum(c, excl, total);
+    if (i < n) chunk_start[i] = carry + excl;
+    __syncthreads();
+    if (threadIdx.x == 0) carry += total;
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) chunk_start[n] = carry;
+}
+
+__global__ void __launch_bounds__(256)
+    bc_huge_chunks_kernel(GraphView g, const uint32_t* __restrict__ rows, uint32_t n,
+                          const uint32_t* __restrict__ chunk_start,
+                          const double* __restrict__ coef, double* acc) {
+  using Reduce = cub::BlockReduce<double, 256>;
+  __shared__ typename Reduce::TempStorage tmp;
+  const uint32_t total = chunk_start[n];
+  for (uint32_t c = blockIdx.x; c < total; c += gridDim.x) {
+    uint32_t lo = 0, hi = n - 1;  // last row with chunk_start <= c
+    while (lo < hi) {
+      const uint32_t m = (lo + hi + 1) >> 1;
+      if (chunk_start[m] <= c) lo = m;
+      else hi = m - 1;
+    }
+    const uint32_t v = rows[lo];
+    const uint32_t b = g.off[v] + (c - chunk_start[lo]) * kBcChunk;
+    const uint32_t e = b + kBcChunk < g.off[v + 1] ? b + kBcChunk : g.off[v + 1];
+    double sum = 0.0;
+    for (uint32_t k = b + threadIdx.x; k < e; k += 256) sum += __ldg(&coef[ld_stream(&g.col[k])]);
+    sum = Reduce(tmp).Sum(sum);
+    if (threadIdx.x == 0) atomicAdd(&acc[lo], sum);
+    __syncthreads();
+  }
+}
+
+__global__ void bc_huge_finish_kernel(GraphView g, const uint32_t* __restrict__ rows, uint32_t n,
+                                      const double* __restrict__ acc, const double* sigma,
+                                      double* delta, double* bc, uint32_t source, Counters* ctr) {
+  unsigned long long scanned = 0;
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    const uint32_t v = rows[i];
+    const double dv = sigma[v] * acc[i];
+    delta[v] = dv;
+    if (v != source) bc[v] += dv;
+    scanned += g.off[v + 1] - g.off[v];
+  }
+  warp_add_u64(&ctr->edges, scanned);
+}
 constexpr uint32_t kBcBucketCtas = kNumSMs * 4;
 
 __global__ void __launch_bounds__(256)
@@ -1635,7 +1719,7 @@ __global__ void __launch_bounds__(256)
   const uint32_t lo = blockIdx.x * per, hi = lo + per < nh ? lo + per : nh;
   for (uint32_t i = lo + threadIdx.x; i < hi; i += blockDim.x) {
     const uint32_t v = hosted[i], l = labels[v];
-    if (l <= max_level) atomicAdd(&h[2 * l + (off[v + 1] - off[v] >= kBcWarpDeg ? 1 : 0)], 1u);
+    if (l <= max_level) atomicAdd(&h[kBcClasses * l + bc_row_class(off[v + 1] - off[v])], 1u);
   }
   __syncthreads();
   for (uint32_t b = threadIdx.x; b < nb; b += blockDim.x) cta_hist[b * gridDim.x + blockIdx.x] = h[b];
@@ -1679,7 +1763,7 @@ __global__ void __launch_bounds__(256)
   for (uint32_t i = lo + threadIdx.x; i < hi; i += blockDim.x) {
     const uint32_t v = hosted[i], l = labels[v];
     if (l <= max_level)
-      out[atomicAdd(&cur[2 * l + (off[v + 1] - off[v] >= kBcWarpDeg ? 1 : 0)], 1u)] = v;
+      out[atomicAdd(&cur[kBcClasses * l + bc_row_class(off[v + 1] - off[v])], 1u)] = v;
   }
 }
 
@@ -1767,9 +1851,9 @@ struct BcPrim : PrimBase {
       c.report.u[0] = 0;  // filled from the device counter
       return;
     }
-    if (phase == kBwd && 2ull * (max_level + 1) <= kBcBuckets) {
+    if (phase == kBwd && (uint64_t)kBcClasses * (max_level + 1) <= kBcBuckets) {
       const uint32_t level = max_level - (uint32_t)(c.iter - backward_from);
-      const uint32_t nb = 2 * (max_level + 1);
+      const uint32_t nb = kBcClasses * (max_level + 1);
       c.ensure_output(nh);
       std::vector<uint32_t>& bucket_start = bucket_starts[w.p];
       if (!bucketed[w.p]) {  // once per run: counting sort of the hosted vertices by level
@@ -1789,14 +1873,15 @@ struct BcPrim : PrimBase {
         MGB_CUDA(cudaStreamSynchronize(w.stream));
       }
       const uint32_t* list = w.aux[0].ptr;
-      const uint32_t s0 = bucket_start[2 * level], s1 = bucket_start[2 * level + 1],
-                     s2 = bucket_start[2 * level + 2];
+      const uint32_t K = kBcClasses;
+      const uint32_t s0 = bucket_start[K * level], s1 = bucket_start[K * level + 1],
+                     s2 = bucket_start[K * level + 2], s3 = bucket_start[K * level + 3];
       const bool deepest = level == max_level;
-      const uint32_t c0 = deepest ? 0 : bucket_start[2 * level + 2];
-      const uint32_t c1 = deepest ? 0 : bucket_start[2 * level + 4];
-      const uint32_t work = (s2 - s0) > (c1 - c0) ? (s2 - s0) : (c1 - c0);
+      const uint32_t c0 = deepest ? 0 : bucket_start[K * (level + 1)];
+      const uint32_t c1 = deepest ? 0 : bucket_start[K * (level + 2)];
+      const uint32_t work = (s3 - s0) > (c1 - c0) ? (s3 - s0) : (c1 - c0);
       MGB_LAUNCH(bc_level_prep_kernel, grid_for(work, 256, kNumSMs * 8), 256, 0, w.stream, list,
-                 s0, s2, c0, c1, deepest ? 1 : 0, w.sf64[0].ptr, w.sf64[1].ptr, w.sf64[3].ptr,
+                 s0, s3, c0, c1, deepest ? 1 : 0, w.sf64[0].ptr, w.sf64[1].ptr, w.sf64[3].ptr,
                  w.output.ptr, c.ctr());
       if (!deepest) {  // the deepest level only broadcasts
         if (s1 > s0)
@@ -1807,6 +1892,18 @@ struct BcPrim : PrimBase {
           MGB_LAUNCH(bc_backward_warp_kernel, grid_for((uint64_t)(s2 - s1) * 32, 256, kNumSMs * 8),
                      256, 0, w.stream, w.graph(), list + s1, nullptr, s2 - s1, w.sf64[0].ptr,
                      w.sf64[1].ptr, w.sf64[2].ptr, w.sf64[3].ptr, source, c.ctr());
+        if (s3 > s2) {  // huge rows: chunks over many CTAs
+          const uint32_t nh_ = s3 - s2;
+          if (w.aux[3].n < nh_ + 1ull) w.aux[3].alloc(nh_ + 1ull);
+          if (w.bc_acc.n < nh_) w.bc_acc.alloc(nh_);
+          MGB_LAUNCH(bc_huge_prefix_kernel, 1, 1024, 0, w.stream, list + s2, nh_, w.off.ptr,
+                     w.aux[3].ptr, w.bc_acc.ptr);
+          MGB_LAUNCH(bc_huge_chunks_kernel, kNumSMs * 8, 256, 0, w.stream, w.graph(), list + s2,
+                     nh_, w.aux[3].ptr, w.sf64[3].ptr, w.bc_acc.ptr);
+          MGB_LAUNCH(bc_huge_finish_kernel, grid_for(nh_, 256, kNumSMs), 256, 0, w.stream,
+                     w.graph(), list + s2, nh_, w.bc_acc.ptr, w.sf64[0].ptr, w.sf64[1].ptr,
+                     w.sf64[2].ptr, source, c.ctr());
+        }
       }
       c.report.u[0] = max_level;
       c.report.u[1] = kBwd;
