@@ -151,10 +151,11 @@ typedef struct mg_config {
   uint64_t max_supersteps;        /* default 1000000                               */
   uint64_t hard_cap_bytes;        /* per-worker budget, 0 = unlimited              */
   double factors[MG_NUM_ROLES];   /* sizing factors (FixedPrealloc / PreallocFused) */
-  /* DOBFS, single partition only: run a logically-forward superstep with the
-   * pull kernel when the exact frontier degree sum exceeds 4x the unvisited
-   * list (Beamer's exact cost rule).  The output set is the same; labels,
-   * direction log, S and the reported W follow the reference rule.  0 = off. */
+  /* DOBFS and BFS, single partition only: run a logically-forward superstep
+   * with the pull kernel when the exact frontier degree sum exceeds 4x the
+   * unvisited list (Beamer's exact cost rule).  The output set is the same;
+   * labels, direction log, S and the reported W follow the reference rule
+   * (BFS: every superstep forward).  0 = off. */
   int dobfs_exact_cost;
 } mg_config;
 

@@ -2585,9 +2585,19 @@ int mg_bfs(mg_plan* plan, uint32_t source, int mark_preds, const mg_config* cfg,
     Plan& P = *reinterpret_cast<Plan*>(plan);
     check_source(P, source, "bfs");
     mg_config c = cfg_or_default(cfg);
-    BfsPrim prim(source, mark_preds != 0);
     P.last = mg_stats{};
-    run_primitive(P, prim, c);
+    if (c.dobfs_exact_cost && P.n == 1) {
+      // extension: the BFS schedule (every superstep logically forward: a
+      // direction rule that never switches) on the DOBFS machinery, heavy
+      // supersteps run physically as pulls; labels, S and W are BFS's
+      DobfsPrim prim(source, INFINITY, 0.1, mark_preds != 0, true, 1);
+      prim.name = "bfs";
+      prim.communication = MG_COMM_SELECTIVE;
+      run_primitive(P, prim, c);
+    } else {
+      BfsPrim prim(source, mark_preds != 0);
+      run_primitive(P, prim, c);
+    }
     P.last_result_kind = 0;
     // BFS levels: the largest label is S - 1 (CLI:339-346)
     gather_labels_u32(P, pw(P, &Worker::su32, 0), labels, P.last.supersteps);

@@ -98,7 +98,10 @@ def test_c2_dobfs_rmat26_paths_agree():
         b = mg.dobfs(plan, mg.DobfsOptions(source=src), MAXCFG)
         c = mg.bfs(plan, mg.BfsOptions(source=src), MAXCFG)
         d = mg.dobfs(plan, mg.DobfsOptions(source=src, do_a=0.001), exact)
+        e = mg.bfs(plan, mg.BfsOptions(source=src), exact)  # BFS schedule, pulls where cheaper
         assert np.array_equal(a.labels, b.labels)
+        assert np.array_equal(c.labels, e.labels)
+        assert c.stats.edges_examined == e.stats.edges_examined
         assert np.array_equal(a.labels, c.labels)
         assert np.array_equal(a.labels, d.labels)
         assert list(a.direction_log) == list(b.direction_log)

@@ -380,3 +380,25 @@ def test_run_stats_json_has_the_reference_schema():
     assert j["H_total"] == sum(map(sum, j["H"])) == r.stats.h_total()
     assert len(j["buffers"]) == 2
     json.dumps(j)  # serialisable
+
+
+@pytest.mark.parametrize("scale,ef,seed", [(12, 16, 1), (14, 16, 3)])
+def test_bfs_exact_cost_extension_keeps_bfs_semantics(scale, ef, seed):
+    """BFS with dobfs_exact_cost: heavy supersteps pull physically; labels, S and
+    W equal the plain BFS (and the oracle); preds stay a legal tree"""
+    g = mg.Csr.rmat(scale, ef, seed)
+    off, col, _ = g.arrays()
+    plan = mg.PartitionPlan(g, None, 1)
+    for src in (0, 5):
+        a = mg.bfs(plan, mg.BfsOptions(source=src))
+        b = mg.bfs(plan, mg.BfsOptions(source=src, mark_preds=True),
+                   mg.EngineConfig(dobfs_exact_cost=True))
+        assert np.array_equal(b.labels, seq.bfs_levels(off, col, src))
+        assert np.array_equal(a.labels, b.labels)
+        assert a.stats.supersteps == b.stats.supersteps
+        assert a.stats.edges_examined == b.stats.edges_examined
+        for v in np.nonzero(b.labels != mg.kInfLabel)[0][:500]:
+            if v == src:
+                continue
+            p = int(b.preds[v])
+            assert b.labels[p] + 1 == b.labels[v] and v in col[off[p]:off[p + 1]]

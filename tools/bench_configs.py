@@ -48,7 +48,7 @@ def emit(**kw):
 
 def main():
     ap = argparse.ArgumentParser()
-    ap.add_argument("--configs", default="1,3,4,5")
+    ap.add_argument("--configs", default="1,2,3,4,5")
     ap.add_argument("--reps", type=int, default=5)
     ap.add_argument("--cpu-seconds", type=float, default=30.0)
     ap.add_argument("--no-cpu", action="store_true")
@@ -75,6 +75,23 @@ def main():
             ms, k = cpu(lambda: rp.bfs(0).stats.wall_ms, a.cpu_seconds)
             out.update(cpu_ms=ms, cpu_gteps=ar / (ms * 1e-3) / 1e9, cpu_cores=1, cpu_runs=k)
         emit(**out)
+
+    if 2 in cfgs:  # BFS on the C2 graph (RMAT-26/16): the reference's push schedule, and
+        # the exact-cost extension (heavy supersteps as pulls, same labels/S/W)
+        plan = mg.PartitionPlan.rmat_device(26, 16, 1)
+        off, _, _ = plan.download_graph().arrays()
+        deg = np.diff(off.astype(np.int64))
+        exact = mg.EngineConfig(policy=mg.AllocPolicyKind.Maximum, fused=mg.FusedMode.On,
+                                dobfs_exact_cost=True)
+        for name, cfg in (("bfs", MAXCFG), ("bfs_exact_cost", exact)):
+            r = mg.bfs(plan, mg.BfsOptions(source=0), cfg)
+            ar = reached(r.labels, deg, mg.kInfLabel)
+            mean, best = timeit(lambda: mg.bfs(plan, mg.BfsOptions(source=0), cfg,
+                                              download=False).stats.device_ms, a.reps)
+            emit(config=2, primitive=name, graph="rmat26_ef16", reached_arcs=ar,
+                 device_ms_mean=mean, device_ms_min=best, gteps=ar / (mean * 1e-3) / 1e9,
+                 supersteps=int(r.stats.supersteps), edges_examined=int(r.stats.edges_examined))
+        del plan, off, deg
 
     if cfgs & {3, 5}:  # RMAT-24/16 (device hashed generator), weights U[1,64] seed+101
         plan = mg.PartitionPlan.rmat_device(a.scale24, 16, 1, weights=(1, 64, 102))
