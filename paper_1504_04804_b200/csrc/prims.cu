@@ -83,23 +83,39 @@ __device__ __forceinline__ void atomic_max_pos_f64(double* addr, double v) {
 // ===========================================================================
 // BFS (primitives.cpp:60-126)
 
+// Single partition of >= 2^22 vertices: visited state as a bitmap (|V|/8 bytes,
+// L2-resident at RMAT-26) instead of probing the 4-byte label of every arc's
+// head (RMAT-26 BFS 20.1 -> 16.4 ms); the
+// test-and-set makes each discovery unique, so the keep stamp is not needed.
+// Several partitions keep the label CAS (remote combines lower labels).
 struct BfsDev {
   uint32_t* labels;
   uint32_t* preds;
   uint32_t* seen;
+  uint32_t* vis;  // visited bitmap (single partition) or nullptr
   OwnerView ow;
   uint32_t iter;
   int mark_preds;
-  // visit: unvisited -> label iter+1 (+pred); the CAS makes the discovery unique
-  // (called only for arcs whose prefilter() saw an unvisited label)
+  // visit: unvisited -> label iter+1 (+pred); the CAS / test-and-set makes the
+  // discovery unique (called only for arcs whose prefilter() saw it unvisited)
   __device__ bool visit(uint32_t u, uint32_t v, uint32_t) const {
-    if (atomicCAS(&labels[v], kInfLabel, iter + 1) != kInfLabel) return false;
+    if (vis) {
+      const uint32_t bit = 1u << (v & 31);
+      if (atomicOr(&vis[v >> 5], bit) & bit) return false;
+      labels[v] = iter + 1;
+    } else if (atomicCAS(&labels[v], kInfLabel, iter + 1) != kInfLabel) {
+      return false;
+    }
     if (mark_preds) preds[v] = ow.to_global(u);
     return true;
   }
   // keep: per-superstep stamp dedup (primitives.cpp:89-94)
-  __device__ bool keep(uint32_t v) const { return atomicExch(&seen[v], iter + 1) != iter + 1; }
-  __device__ bool prefilter(uint32_t v) const { return __ldcg(&labels[v]) == kInfLabel; }
+  __device__ bool keep(uint32_t v) const {
+    return vis || atomicExch(&seen[v], iter + 1) != iter + 1;
+  }
+  __device__ bool prefilter(uint32_t v) const {
+    return vis ? !((__ldcg(&vis[v >> 5]) >> (v & 31)) & 1u) : __ldcg(&labels[v]) == kInfLabel;
+  }
   // combine (primitives.cpp:98-107): iter+1 < label -> set, enqueue iff hosted
   __device__ bool combine(uint32_t v, const uint32_t* va, const double*, uint32_t it) const {
     uint32_t cand = it + 1;
@@ -117,9 +133,34 @@ struct BfsDev {
   __device__ uint32_t peer_id(uint32_t v, uint32_t, uint32_t) const { return v; }
 };
 
+// batched visits: the whole batch's test-and-sets in flight together
+template <int K>
+__device__ __forceinline__ void visit_batch(const BfsDev& f, const uint32_t* src,
+                                            const uint32_t* nb, const uint32_t* eid,
+                                            const bool* pass, bool* acc) {
+  if (!f.vis) {
+#pragma unroll
+    for (int k = 0; k < K; ++k) acc[k] = pass[k] && f.visit(src[k], nb[k], eid[k]);
+    return;
+  }
+  uint32_t old[K];
+#pragma unroll
+  for (int k = 0; k < K; ++k)
+    old[k] = pass[k] ? atomicOr(&f.vis[nb[k] >> 5], 1u << (nb[k] & 31)) : ~0u;
+#pragma unroll
+  for (int k = 0; k < K; ++k) {
+    acc[k] = !(old[k] & (1u << (nb[k] & 31)));
+    if (acc[k]) {
+      f.labels[nb[k]] = f.iter + 1;
+      if (f.mark_preds) f.preds[nb[k]] = f.ow.to_global(src[k]);
+    }
+  }
+}
+
 struct BfsPrim : PrimBase {
   uint32_t source;
   bool mark_preds;
+  bool bitmap = false;  // single partition: visited bitmap in su32[3]
   BfsPrim(uint32_t s, bool m) : source(s), mark_preds(m) {
     name = "bfs";
     nva = m ? 1 : 0;
@@ -127,16 +168,25 @@ struct BfsPrim : PrimBase {
   }
   void init(Ctx& c) {  // primitives.cpp:71-79
     Worker& w = *c.w;
+    // the bitmap pays off once the label array outgrows L2 (small graphs keep
+    // the label CAS: one launch less at init, same result)
+    bitmap = c.P->n == 1 && w.nv >= (1u << 22);
     fill(w.su32[0], w.nv, 0xFF, w.stream);  // labels = inf
-    fill(w.su32[2], w.nv, 0, w.stream);     // seen
+    if (bitmap) {
+      fill(w.su32[3], (w.nv + 31) / 32 + 1, 0, w.stream);  // visited bitmap
+      MGB_LAUNCH(or_word_kernel, 1, 1, 0, w.stream, w.su32[3].ptr + (source >> 5),
+                 1u << (source & 31));
+    } else {
+      fill(w.su32[2], w.nv, 0, w.stream);  // seen
+    }
     if (mark_preds) fill(w.su32[1], w.nv, 0xFF, w.stream);
     MGB_LAUNCH(set_one_kernel<uint32_t>, 1, 1, 0, w.stream, w.su32[0].ptr, source, 0u);
     if (c.P->owner_host[source] == w.p) c.push_initial({source});
   }
   BfsDev dev(Ctx& c) {
     Worker& w = *c.w;
-    return {w.su32[0].ptr, w.su32[1].ptr, w.su32[2].ptr, c.owner_view(), (uint32_t)c.iter,
-            mark_preds ? 1 : 0};
+    return {w.su32[0].ptr, w.su32[1].ptr, w.su32[2].ptr, bitmap ? w.su32[3].ptr : nullptr,
+            c.owner_view(), (uint32_t)c.iter, mark_preds ? 1 : 0};
   }
   void body(Ctx& c) { c.pipeline(dev(c), c.w->nv); }
 };
