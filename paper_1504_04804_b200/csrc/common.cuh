@@ -51,21 +51,13 @@ inline unsigned grid_for(uint64_t items, unsigned per_block, unsigned cap = kNum
 
 __device__ __forceinline__ unsigned lane_id() { return threadIdx.x & 31u; }
 
-// Loads of arrays streamed once per superstep (col_indices, weights): with
-// MG_STREAM_HINTS they are issued evict-first (ld.global.cs) so they do not
-// push the randomly probed state arrays (labels, distances, bitmaps) out of L2
-// (measured: SSSP RMAT-24 12.4 -> 11.8 ms).  An accessPolicyWindow pinning the
-// distance array measured slower (the window reset costs more than it saves).
-#ifndef MG_STREAM_HINTS
-#define MG_STREAM_HINTS 1
-#endif
+// Loads of arrays streamed once per superstep (col_indices, weights) are
+// issued evict-first (ld.global.cs) so they do not push the randomly probed
+// state arrays (labels, distances, bitmaps) out of L2 (measured: SSSP RMAT-24
+// 12.4 -> 11.8 ms).
 template <class T>
 __device__ __forceinline__ T ld_stream(const T* p) {
-#if MG_STREAM_HINTS
   return __ldcs(p);
-#else
-  return __ldg(p);
-#endif
 }
 
 // Warp-aggregated append: every active lane with `pred` gets a slot in the

@@ -321,16 +321,7 @@ __global__ void select_nonisolated_kernel(const uint32_t* __restrict__ hosted, u
 // positions; the first pull of a run walks all records without a list.
 constexpr int kPullK = 2;      // arcs held in the record
 constexpr int kPullGroup = 8;  // lanes per vertex in the long-row pass
-#ifndef MG_PULL_PV
-#define MG_PULL_PV 8
-#endif
-#ifndef MG_PULL_MINB
-#define MG_PULL_MINB 4
-#endif
-#ifndef MG_PULL_STREAM
-#define MG_PULL_STREAM 1
-#endif
-constexpr int kPV = MG_PULL_PV;  // records per thread per iteration (loads in flight)
+constexpr int kPV = 8;         // records per thread per iteration (loads in flight)
 constexpr uint32_t kPullQ = 256 * kPV + 1024;  // CTA queue capacity (> one chunk of 256 * kPV)
 
 __global__ void pull_records_kernel(GraphView g, const uint32_t* __restrict__ ni, uint32_t n,
@@ -370,29 +361,6 @@ __device__ __forceinline__ void warp_queue_append(BlockQueue<kCap>& q, const boo
   }
 }
 
-#ifndef MG_PULL_BITS_LEADER
-#define MG_PULL_BITS_LEADER 0
-#endif
-#ifndef MG_PULL_LAZY_FLUSH
-#define MG_PULL_LAZY_FLUSH 1
-#endif
-#ifndef MG_PULL_GRID
-#define MG_PULL_GRID 4
-#endif
-
-#ifndef MG_ABLATE  // experiment switch: drop pieces of the pull kernel to price them
-#define MG_ABLATE 0
-#endif
-#ifndef MG_PULL_BITS_PLAIN
-#define MG_PULL_BITS_PLAIN 0
-#endif
-#ifndef MG_PULL_CNT32
-#define MG_PULL_CNT32 1
-#endif
-
-#ifndef MG_PULL_BITS_SMEM
-#define MG_PULL_BITS_SMEM 1
-#endif
 constexpr uint32_t kBitSlots = 64;  // per-warp shared words for the visited-bit merge
 
 // set the visited bits of the lanes' discoveries: the lanes OR their bits into
@@ -422,44 +390,6 @@ __device__ __forceinline__ void warp_set_bits_smem(uint32_t* bits, uint32_t* win
   __syncwarp();
 }
 
-#if MG_PULL_BITS_PLAIN
-__device__ __forceinline__ void warp_set_bits(uint32_t* bits, bool pred, uint32_t v) {
-  if (pred) atomicOr(&bits[v >> 5], 1u << (v & 31));
-}
-#elif MG_PULL_BITS_LEADER
-// set the visited bits of the lanes' discoveries with one atomicOr per
-// distinct word: a leader loop over the words, each OR formed by one REDUX
-__device__ __forceinline__ void warp_set_bits(uint32_t* bits, bool pred, uint32_t v) {
-  unsigned pending = __ballot_sync(0xffffffffu, pred);
-  const uint32_t wd = v >> 5, bit = 1u << (v & 31);
-  while (pending) {
-    const int leader = __ffs(pending) - 1;
-    const uint32_t lw = __shfl_sync(0xffffffffu, wd, leader);
-    const bool mine = pred && wd == lw;
-    const uint32_t b = __reduce_or_sync(0xffffffffu, mine ? bit : 0u);
-    if (lane_id() == (unsigned)leader) atomicOr(&bits[lw], b);
-    pending &= ~__ballot_sync(0xffffffffu, mine);
-  }
-}
-#else
-// set the visited bits of the lanes' discoveries with one atomicOr per run of
-// lanes hitting the same word (records are sorted, so a warp's discoveries
-// form few runs): a segmented OR by shuffles, the run head issues the atomic
-__device__ __forceinline__ void warp_set_bits(uint32_t* bits, bool pred, uint32_t v) {
-  const uint32_t wd = pred ? v >> 5 : 0xFFFFFFFFu;
-  uint32_t b = pred ? 1u << (v & 31) : 0u;
-  const unsigned lane = lane_id();
-#pragma unroll
-  for (int o = 1; o < 32; o <<= 1) {
-    const uint32_t ob = __shfl_down_sync(0xffffffffu, b, o);
-    const uint32_t ow = __shfl_down_sync(0xffffffffu, wd, o);
-    if (lane + o < 32 && ow == wd) b |= ob;
-  }
-  const uint32_t pw = __shfl_up_sync(0xffffffffu, wd, 1);
-  if (pred && (lane == 0 || pw != wd)) atomicOr(&bits[wd], b);
-}
-#endif
-
 // pull step, stage 1 (primitives.cpp:230-251): one thread per unvisited record
 // tests the record's two arcs against the frontier bitmap; a hit labels the
 // vertex, a short row without a hit stays unvisited, a longer row goes to the
@@ -468,7 +398,7 @@ __device__ __forceinline__ void warp_set_bits(uint32_t* bits, bool pred, uint32_
 // partition) the discovered vertices are only counted (and their degrees
 // summed into deg_out when non-null): the next superstep rebuilds the frontier
 // list from the visited bitmap only if it pushes.
-__global__ void __launch_bounds__(256, MG_PULL_MINB)
+__global__ void __launch_bounds__(256, 4)
     dobfs_pull_thread_kernel(const uint4* __restrict__ rec, const uint32_t* __restrict__ ul,
                              uint32_t nul, uint32_t* labels, uint32_t* preds, uint32_t* vis,
                              const uint32_t* __restrict__ fb, uint32_t next_label, int mark_preds,
@@ -476,11 +406,7 @@ __global__ void __launch_bounds__(256, MG_PULL_MINB)
                              uint32_t* ul_out_cnt, uint32_t* longq, uint32_t* long_cnt,
                              Counters* ctr, unsigned long long* scanned_out,
                              unsigned long long* deg_out) {
-#if MG_PULL_CNT32
   uint32_t scanned = 0, opened = 0, degs = 0;  // per-thread partials fit 32 bits
-#else
-  unsigned long long scanned = 0, opened = 0, degs = 0;
-#endif
   uint32_t found_n = 0;
   // queues hold up to kPullQ entries and are flushed only when one could
   // overflow in the next chunk (one barrier per chunk otherwise)
@@ -503,12 +429,8 @@ __global__ void __launch_bounds__(256, MG_PULL_MINB)
       pos[j] = i < nul ? (ul ? __ldg(&ul[i]) : i) : kInfLabel;
     }
 #pragma unroll
-    for (int j = 0; j < kPV; ++j)  // coalesced 16-byte records, kPV in flight
-#if MG_PULL_STREAM
+    for (int j = 0; j < kPV; ++j)  // coalesced 16-byte records, kPV in flight, evict-first
       r[j] = pos[j] != kInfLabel ? __ldcs(&rec[pos[j]]) : make_uint4(0, 0, kInfLabel, kInfLabel);
-#else
-      r[j] = pos[j] != kInfLabel ? __ldg(&rec[pos[j]]) : make_uint4(0, 0, kInfLabel, kInfLabel);
-#endif
     bool open[kPV], h0[kPV], h1[kPV];
 #pragma unroll
     for (int j = 0; j < kPV; ++j) {
@@ -528,32 +450,22 @@ __global__ void __launch_bounds__(256, MG_PULL_MINB)
       opened += open[j];
       if (found[j]) {
         scanned += h0[j] ? 1 : 2;
-#if MG_PULL_STREAM
-        if (!(MG_ABLATE & 1)) __stcs(&labels[v], next_label);
-#else
-        labels[v] = next_label;
-#endif
+        __stcs(&labels[v], next_label);
         if (mark_preds) preds[v] = ow.to_global(h0[j] ? r[j].z : r[j].w);
         ++found_n;
         degs += d;
       } else if (open[j]) {
         scanned += d < (uint32_t)kPullK ? d : (uint32_t)kPullK;
       }
-#if MG_PULL_BITS_SMEM == 1
-      if (!(MG_ABLATE & 2)) warp_set_bits_smem(vis, s_win[threadIdx.x >> 5], found[j], v);
-#elif MG_PULL_BITS_SMEM == 0
-      if (!(MG_ABLATE & 2)) warp_set_bits(vis, found[j], v);
-#endif
+      warp_set_bits_smem(vis, s_win[threadIdx.x >> 5], found[j], v);
     }
 
     if (emit_found) warp_queue_append<kPV>(q_found, found, vv);
-    if (!(MG_ABLATE & 4)) {
-      warp_queue_append<kPV>(q_keep, keep, pos);
-      warp_queue_append<kPV>(q_long, lng, pos);
-    }
+    warp_queue_append<kPV>(q_keep, keep, pos);
+    warp_queue_append<kPV>(q_long, lng, pos);
     __syncthreads();
     const bool last = base + gridDim.x * chunk >= nul;
-    if (!MG_PULL_LAZY_FLUSH || last || q_found.n > kPullQ - chunk || q_keep.n > kPullQ - chunk ||
+    if (last || q_found.n > kPullQ - chunk || q_keep.n > kPullQ - chunk ||
         q_long.n > kPullQ - chunk) {  // CTA-uniform: read after the barrier
       if (threadIdx.x == 0) {
         q_found.base = q_found.n ? atomicAdd(&ctr->out_cnt, q_found.n) : 0u;
@@ -873,7 +785,7 @@ struct DobfsPrim : PrimBase {
     // cost test needs no extra host round trip
     unsigned long long* deg_out = reports_deg && !c.want_deg ? &c.ctr()->next_deg : nullptr;
     if (nul) {
-      MGB_LAUNCH(dobfs_pull_thread_kernel, grid_for(nul, 256 * kPV, kNumSMs * MG_PULL_GRID), 256, 0,
+      MGB_LAUNCH(dobfs_pull_thread_kernel, grid_for(nul, 256 * kPV, kNumSMs * 4), 256, 0,
                  w.stream, w.pull_rec.ptr, ul, nul, w.su32[0].ptr, w.su32[1].ptr, w.su32[2].ptr,
                  w.su32[3].ptr, next_label, mark_preds ? 1 : 0, c.owner_view(), emit ? 1 : 0,
                  w.output.ptr, w.ul_buf[dst].ptr, ulcnt, w.ul_buf[2].ptr, cnts + 1, c.ctr(),
@@ -1677,14 +1589,8 @@ constexpr uint32_t kBcBuckets = 2048;  // kBcClasses * (max_level + 1) must fit
 // cut into kBcChunk-arc chunks over many CTAs (a hub row of 1e6 arcs on one
 // warp left the GPU at 3.5% SM throughput for 2.7 ms)
 constexpr uint32_t kBcClasses = 3;
-#ifndef MG_BC_HUGE
-#define MG_BC_HUGE 8192
-#endif
-#ifndef MG_BC_CHUNK
-#define MG_BC_CHUNK 4096
-#endif
-constexpr uint32_t kBcHugeDeg = MG_BC_HUGE;
-constexpr uint32_t kBcChunk = MG_BC_CHUNK;
+constexpr uint32_t kBcHugeDeg = 8192;
+constexpr uint32_t kBcChunk = 4096;
 __device__ __forceinline__ uint32_t bc_row_class(uint32_t deg) {
   return deg < kBcWarpDeg ? 0u : (deg < kBcHugeDeg ? 1u : 2u);
 }
