@@ -151,11 +151,13 @@ typedef struct mg_config {
   uint64_t max_supersteps;        /* default 1000000                               */
   uint64_t hard_cap_bytes;        /* per-worker budget, 0 = unlimited              */
   double factors[MG_NUM_ROLES];   /* sizing factors (FixedPrealloc / PreallocFused) */
-  /* DOBFS and BFS, single partition only: run a logically-forward superstep
-   * with the pull kernel when the exact frontier degree sum exceeds 4x the
-   * unvisited list (Beamer's exact cost rule).  The output set is the same;
-   * labels, direction log, S and the reported W follow the reference rule
-   * (BFS: every superstep forward).  0 = off. */
+  /* DOBFS (any number of partitions) and BFS (single partition): run a
+   * logically-forward superstep with the pull kernels when the exact frontier
+   * degree sum exceeds 4x the unvisited list (Beamer's exact cost rule; summed
+   * over all partitions so every worker takes the same direction).  The
+   * output set is the same; labels, direction log, S and the reported W
+   * follow the reference rule (BFS: every superstep forward); the records
+   * sent (H) can only shrink.  0 = off. */
   int dobfs_exact_cost;
 } mg_config;
 

@@ -632,7 +632,7 @@ void run_primitive(Plan& P, Prim& prim, const mg_config& cfg) {
                    256, 0, w.stream, dev, c.owner_view(), w.graph(), w.output.ptr, w.ctr.ptr,
                    w.next_input.ptr, w.send_table.ptr + parity * n, n,
                    step_comm[p] == MG_COMM_BROADCAST ? 1 : 0, drop, prim.nva, prim.nvv,
-                   want_deg ? 1 : 0);
+                   (want_deg || prim.reports_deg) ? 1 : 0);
       });
       if (n > 1) {
         MGB_LAUNCH(publish_kernel, 1, 64, 0, w.stream, w.ctr.ptr, w.send_cnt_ptr.ptr + parity * n,
@@ -669,7 +669,8 @@ void run_primitive(Plan& P, Prim& prim, const mg_config& cfg) {
           MGB_LAUNCH(merge_kernel<decltype(dev)>, grid, 256, 0, w.stream, dev,
                      w.recv_table.ptr + parity * n, w.inbox_cnt.ptr + parity * kMaxWorkers, p,
                      (uint32_t)(iter + 1), (uint32_t)iter, w.merge_stamp.ptr, w.next_input.ptr,
-                     w.ctr.ptr, w.graph(), prim.nva, prim.nvv, 1, want_deg ? 1 : 0);
+                     w.ctr.ptr, w.graph(), prim.nva, prim.nvv, 1,
+                     (want_deg || prim.reports_deg) ? 1 : 0);
         });
       }
       prim.after_merge(c);

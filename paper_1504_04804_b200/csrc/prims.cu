@@ -609,6 +609,13 @@ __global__ void __launch_bounds__(256)
   }
 }
 
+// u[0] = the worker's unvisited-list length after this superstep (the pull's
+// kept count, or unchanged), u[1] = Σdeg of its next frontier
+__global__ void dobfs_share_kernel(Counters* ctr, int pulled, uint32_t ul_keep) {
+  ctr->u[0] = pulled ? ctr->misc : ul_keep;
+  ctr->u[1] = ctr->next_deg;
+}
+
 struct DobfsPrim : PrimBase {
   uint32_t source;
   double do_a, do_b;
@@ -625,7 +632,7 @@ struct DobfsPrim : PrimBase {
   uint64_t physical_pull_steps = 0;
   DobfsPrim(uint32_t s, double a, double b, bool m, bool exact, uint32_t nparts)
       : source(s), do_a(a), do_b(b), mark_preds(m), exact_cost(exact) {
-    reports_deg = exact && nparts == 1;
+    reports_deg = exact;  // n = 1: by the pull / push kernels; n > 1: by split + merge
     name = "dobfs";
     nva = m ? 1 : 0;
     communication = MG_COMM_BROADCAST;
@@ -715,6 +722,7 @@ struct DobfsPrim : PrimBase {
       dir_log.push_back(dir);
     }
     const uint64_t nw = words(w.nv);
+    pulled_ = false;
     if (list_free[w.p]) {
       // the previous (pull) superstep only counted its discoveries: rebuild the
       // input frontier list from the visited bitmap (vis & ~vis_prev); a pull
@@ -739,6 +747,19 @@ struct DobfsPrim : PrimBase {
       logical_w = c.degsum();
       physical_pull = logical_w > 4ull * ul_len[w.p];
       if (physical_pull) ++physical_pull_steps;
+    } else if (dir == 0 && exact_cost && c.P->n > 1 && c.iter > 0) {
+      // several partitions: every worker must take the same physical direction
+      // (a pull covers only the hosted vertices, a push only the hosted
+      // frontier), so the test uses the global sums every worker reported
+      // last superstep: u[1] = Σdeg of its next frontier, u[0] = its list length
+      uint64_t gw = 0, gul = 0;
+      for (const WorkerReport& r : c.prev->reports) {
+        gw += r.u[1];
+        gul += r.u[0];
+      }
+      physical_pull = gw > 4ull * gul;
+      logical_w = c.in_degsum == kUnknownDeg ? c.degsum() : c.in_degsum;
+      if (physical_pull) ++physical_pull_steps;
     }
     if (!physical_pull) {
       MGB_CUDA(cudaMemcpyAsync(w.aux[4].ptr, w.su32[2].ptr, 4 * nw, cudaMemcpyDeviceToDevice,
@@ -751,11 +772,12 @@ struct DobfsPrim : PrimBase {
         prof_kind_[w.p] = 1;
         prof_nul_[w.p] = c.in_count;
       }
-      if (reports_deg && !c.want_deg)
+      if (reports_deg && !c.want_deg && c.P->n == 1)
         MGB_LAUNCH(degsum_dev_kernel, kNumSMs * 4, 256, 0, w.stream, w.graph(), w.output.ptr,
                    &c.ctr()->out_cnt, &c.ctr()->next_deg);
       return;
     }
+    pulled_ = true;
     // backward: the (global) input frontier is exactly what became visited in
     // the previous superstep, so its bitmap is vis & ~vis_prev — one streaming
     // pass over |V|/32 words instead of an atomic per frontier vertex
@@ -783,7 +805,8 @@ struct DobfsPrim : PrimBase {
     unsigned long long* scanned = dir == 1 ? &c.ctr()->edges : &c.ctr()->u[3];
     // exact-cost runs report Σdeg of the next frontier so the next superstep's
     // cost test needs no extra host round trip
-    unsigned long long* deg_out = reports_deg && !c.want_deg ? &c.ctr()->next_deg : nullptr;
+    unsigned long long* deg_out =
+        reports_deg && !c.want_deg && c.P->n == 1 ? &c.ctr()->next_deg : nullptr;
     if (nul) {
       MGB_LAUNCH(dobfs_pull_thread_kernel, grid_for(nul, 256 * kPV, kNumSMs * 4), 256, 0,
                  w.stream, w.pull_rec.ptr, ul, nul, w.su32[0].ptr, w.su32[1].ptr, w.su32[2].ptr,
@@ -835,6 +858,14 @@ struct DobfsPrim : PrimBase {
   }
   std::vector<int> prof_kind_ = std::vector<int>(kMaxWorkers, 0);
   void finalize(Ctx& c, const GlobalView&) { collect_profile(c); }
+  // several partitions with the exact-cost test: share this worker's list
+  // length and next-frontier degree sum through the report (u[0], u[1])
+  bool pulled_ = false;
+  void after_merge(Ctx& c) {
+    if (!(exact_cost && c.P->n > 1)) return;
+    MGB_LAUNCH(dobfs_share_kernel, 1, 1, 0, c.w->stream, c.ctr(), pulled_ ? 1 : 0,
+               ul_len[c.w->p]);
+  }
   std::vector<bool> pending_ul_ = std::vector<bool>(kMaxWorkers, false);
   std::vector<bool> list_free;  // per worker: last pull step counted, did not list
   std::vector<bool> prof_pending_ = std::vector<bool>(kMaxWorkers, false);

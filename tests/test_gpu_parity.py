@@ -402,3 +402,28 @@ def test_bfs_exact_cost_extension_keeps_bfs_semantics(scale, ef, seed):
                 continue
             p = int(b.preds[v])
             assert b.labels[p] + 1 == b.labels[v] and v in col[off[p]:off[p + 1]]
+
+
+@pytest.mark.parametrize("n", [2, 3, 4])
+def test_dobfs_exact_cost_several_partitions(n):
+    """exact-cost DOBFS on several partitions: one global physical direction per
+    superstep; labels, direction log, S and W stay the reference's; the records
+    sent (H) can only shrink (a pull discovers hosted vertices once)"""
+    g = mg.Csr.rmat(13, 16, 2)
+    off, col, _ = g.arrays()
+    plan, owner = plan_for(g, n, 9 * n + 1)
+    want = seq.bfs_levels(off, col, 0)
+    for do_a in (0.01, 0.001):
+        a = mg.dobfs(plan, mg.DobfsOptions(source=0, do_a=do_a))
+        b = mg.dobfs(plan, mg.DobfsOptions(source=0, do_a=do_a, mark_preds=True),
+                     mg.EngineConfig(dobfs_exact_cost=True))
+        assert np.array_equal(b.labels, want)
+        assert list(a.direction_log) == list(b.direction_log)
+        assert a.stats.supersteps == b.stats.supersteps
+        assert a.stats.edges_examined == b.stats.edges_examined
+        assert b.stats.h_total() <= a.stats.h_total()
+        for v in np.nonzero(b.labels != mg.kInfLabel)[0][:300]:
+            if v == 0:
+                continue
+            p = int(b.preds[v])
+            assert b.labels[p] + 1 == b.labels[v] and v in col[off[p]:off[p + 1]]
