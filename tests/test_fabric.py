@@ -143,3 +143,49 @@ def test_two_processes_one_gpu_cuda_ipc_exchange(fabric):
     assert outs[0]["bfs_H"] == single.stats.h_matrix.tolist()
     dob = mg.dobfs(mg.PartitionPlan(g, owner, 2), mg.DobfsOptions(source=0))
     assert outs[0]["dobfs_dir"] == [int(x) for x in dob.direction_log]
+
+
+def _gpu_worker_dobfs(rank, world, port, q, fabric):
+    sys.path.insert(0, ROOT)
+    if fabric == "host":
+        os.environ["MG_HOST_FABRIC"] = "1"
+    try:
+        import torch.distributed as dist
+
+        import paper_1504_04804_b200 as mg
+        from oracle import seq
+        dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank,
+                                world_size=world)
+        obj = [uuid.uuid4().hex if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0)
+        g = mg.Csr.rmat(11, 16, 4)
+        off, col, _ = g.arrays()
+        owner = mg.partition_random(g.num_vertices, world, 5)
+        mine = owner == rank
+        plan = mg.PartitionPlan.multiprocess(g, owner, world, rank, 0, obj[0])
+        want = seq.bfs_levels(off, col, 0)
+        out = {}
+        for name, cfg in (("ref", None), ("exact", mg.EngineConfig(dobfs_exact_cost=True))):
+            r = mg.dobfs(plan, mg.DobfsOptions(source=0), cfg)
+            out[name] = bool(np.array_equal(r.labels[mine], want[mine]))
+            out[name + "_dir"] = [int(x) for x in r.direction_log]
+            out[name + "_S"] = int(r.stats.supersteps)
+        del plan
+        dist.barrier()
+        dist.destroy_process_group()
+        q.put((rank, 0, out))
+    except Exception as ex:  # pragma: no cover
+        q.put((rank, 1, repr(ex)))
+
+
+@pytest.mark.gpu
+def test_three_processes_dobfs_device_fabric_and_exact_cost():
+    """three ranks (one GPU): reference schedule and the exact-cost extension
+    through the device-side protocol agree with the oracle and with each other"""
+    res = _spawn(_gpu_worker_dobfs, 3, "device")
+    assert all(rc == 0 for _, rc, _ in res), res
+    outs = [o for _, _, o in res]
+    for o in outs:
+        assert o["ref"] and o["exact"], o
+        assert o["ref_dir"] == o["exact_dir"] and o["ref_S"] == o["exact_S"]
+    assert all(o["ref_dir"] == outs[0]["ref_dir"] for o in outs)
