@@ -33,34 +33,43 @@ constexpr int kWarpQ = 384;       // warp-private output staging entries
 constexpr int kStage = 1536;      // max tile vertices staged in shared memory
 
 // lb 1: row starts + CTA-local exclusive prefix of degrees
+// (n_in_ptr: the frontier length read on the device — graph-captured
+// supersteps; the CTAs then walk the virtual blocks of 256 entries)
 static __global__ void __launch_bounds__(kLbBlock)
     lb_degree_kernel(const uint32_t* __restrict__ off, const uint32_t* __restrict__ in,
                      uint32_t n_in, uint32_t* __restrict__ rowstart,
-                     unsigned long long* __restrict__ prefix, unsigned long long* block_sum) {
+                     unsigned long long* __restrict__ prefix, unsigned long long* block_sum,
+                     const uint32_t* n_in_ptr = nullptr) {
   using Scan = cub::BlockScan<unsigned long long, kLbBlock>;
   __shared__ typename Scan::TempStorage tmp;
-  uint32_t i = blockIdx.x * kLbBlock + threadIdx.x;
-  unsigned long long d = 0;
-  if (i < n_in) {
-    uint32_t u = in[i];
-    uint32_t rs = off[u];
-    d = off[u + 1] - rs;
-    rowstart[i] = rs;
+  if (n_in_ptr) n_in = *n_in_ptr;
+  const uint32_t nb = (n_in + kLbBlock - 1) / kLbBlock;
+  for (uint32_t vb = blockIdx.x; vb < nb; vb += gridDim.x) {
+    uint32_t i = vb * kLbBlock + threadIdx.x;
+    unsigned long long d = 0;
+    if (i < n_in) {
+      uint32_t u = in[i];
+      uint32_t rs = off[u];
+      d = off[u + 1] - rs;
+      rowstart[i] = rs;
+    }
+    unsigned long long excl, total;
+    Scan(tmp).ExclusiveSum(d, excl, total);
+    if (i < n_in) prefix[i] = excl;
+    if (threadIdx.x == 0) block_sum[vb] = total;
+    __syncthreads();
   }
-  unsigned long long excl, total;
-  Scan(tmp).ExclusiveSum(d, excl, total);
-  if (i < n_in) prefix[i] = excl;
-  if (threadIdx.x == 0) block_sum[blockIdx.x] = total;
 }
 
 // lb 2: scan the CTA sums in one CTA; block_sum becomes exclusive offsets,
 // block_sum[nb] the total (= edges examined)
 static __global__ void __launch_bounds__(1024)
     lb_scan_kernel(unsigned long long* block_sum, uint32_t nb, unsigned long long* total_out,
-                   unsigned long long* edges) {
+                   unsigned long long* edges, const uint32_t* n_in_ptr = nullptr) {
   using Scan = cub::BlockScan<unsigned long long, 1024>;
   __shared__ typename Scan::TempStorage tmp;
   __shared__ unsigned long long carry;
+  if (n_in_ptr) nb = (*n_in_ptr + kLbBlock - 1) / kLbBlock;
   if (threadIdx.x == 0) carry = 0;
   __syncthreads();
   for (uint32_t base = 0; base < nb; base += 1024) {
@@ -126,7 +135,9 @@ __device__ __forceinline__ void visit_batch(const F& f, const uint32_t* src, con
 static __global__ void lb_tiles_kernel(const unsigned long long* __restrict__ prefix,
                                        const unsigned long long* __restrict__ block_off,
                                        uint32_t n_in, const unsigned long long* total_ptr,
-                                       uint32_t* tile_lo, uint32_t max_tiles) {
+                                       uint32_t* tile_lo, uint32_t max_tiles,
+                                       const uint32_t* n_in_ptr = nullptr) {
+  if (n_in_ptr) n_in = *n_in_ptr;
   const unsigned long long total = *total_ptr;
   const unsigned long long ts = lb_tile_size(total);
   const unsigned long long ntiles = (total + ts - 1) / ts;
@@ -150,7 +161,9 @@ __global__ void __launch_bounds__(kExpBlock)
                      const unsigned long long* __restrict__ prefix,
                      const unsigned long long* __restrict__ block_off,
                      const unsigned long long* total_ptr, const uint32_t* __restrict__ tile_lo,
-                     uint32_t* __restrict__ out, uint32_t* out_cnt) {
+                     uint32_t* __restrict__ out, uint32_t* out_cnt,
+                     const uint32_t* n_in_ptr = nullptr) {
+  if (n_in_ptr) n_in = *n_in_ptr;
   __shared__ unsigned long long s_pref[kStage + 1];
   __shared__ uint32_t s_row[kStage];
   __shared__ uint32_t s_src[kStage];

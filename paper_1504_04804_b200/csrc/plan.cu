@@ -46,6 +46,13 @@ static void free_worker(Worker& w) {
   w.nonisolated.free_();
   w.pull_rec.free_();
   for (auto& a : w.ul_buf) a.free_();
+  for (int i = 0; i < 2; ++i)
+    if (w.loop_exec[i]) cudaGraphExecDestroy(w.loop_exec[i]);
+  if (w.loop_host) cudaFreeHost(w.loop_host);
+  if (w.loop_hist_host) cudaFreeHost(w.loop_hist_host);
+  w.loop_state.free_(); w.loop_hist.free_(); w.loop_front[0].free_(); w.loop_front[1].free_();
+  w.loop_lb_row.free_(); w.loop_tiles.free_(); w.loop_lb_pref.free_(); w.loop_lb_bsum.free_();
+  w.loop_total.free_();
   w.toff.free_(); w.tcol.free_(); w.tlong.free_();
   w.pr_perm.free_(); w.pr_pdeg.free_(); w.pr_iperm.free_();
   w.bc_acc.free_();

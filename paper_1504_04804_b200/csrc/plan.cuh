@@ -146,6 +146,16 @@ struct Worker {
   DevArray<uint32_t> nonisolated;     // hosted vertices with out-degree > 0 (ascending)
   DevArray<uint4> pull_rec;           // DOBFS pull records {v, deg, arc0, arc1} per nonisolated
   DevArray<uint32_t> ul_buf[3];       // DOBFS unvisited lists (ping-pong) + long-row queue
+  // device-driven DOBFS (graph mode): loop state, history, fixed frontier and
+  // advance scratch, the instantiated graphs (by mark_preds)
+  DevArray<uint8_t> loop_state, loop_hist;
+  void* loop_host = nullptr;       // pinned copy of the loop state
+  void* loop_hist_host = nullptr;  // pinned per-superstep history
+  DevArray<uint32_t> loop_front[2], loop_lb_row, loop_tiles;
+  DevArray<unsigned long long> loop_lb_pref, loop_lb_bsum, loop_total;
+  cudaGraphExec_t loop_exec[2] = {nullptr, nullptr};  // by mark_preds
+  uint32_t loop_n_pull[2] = {0, 0}, loop_n_push[2] = {0, 0};
+  std::vector<const void*> loop_ptrs[2];  // device pointers each graph captured
   // transpose of the sub-graph (in-arcs from hosted vertices), rows sorted by
   // source; built once per plan for the pull-form PageRank accumulation
   DevArray<uint32_t> toff, tcol, tlong;

@@ -203,6 +203,28 @@ struct BfsPrim : PrimBase {
 // examined-edge count W are those of the reference's scan (first hit in arc
 // order), so labels, direction log and W match it exactly.
 
+// ---- device-driven supersteps (see DobfsGraph below) ------------------------
+struct DobfsLoop {
+  // per-run parameters, written by the host before the graph launch
+  double nv_d, ne_d, do_a, do_b;
+  uint32_t nv, source, max_supersteps, exact;
+  // superstep state, owned by the device
+  uint32_t iter, dir, switched, physical;
+  uint32_t in_count, ul_src, ul_len, n_nonisolated;
+  unsigned long long in_degsum, visited;
+};
+struct DobfsHist {
+  uint32_t dir, physical, out, pad;
+  unsigned long long edges;
+};
+// the pull kernels read their per-superstep arguments from the loop state
+// when dyn.st is set (graph-captured launches have fixed arguments)
+struct DobfsDyn {
+  const DobfsLoop* st;
+  uint32_t* ub0;
+  uint32_t* ub1;
+};
+
 struct DobfsDev {
   uint32_t* labels;
   uint32_t* preds;
@@ -211,6 +233,7 @@ struct DobfsDev {
   OwnerView ow;
   uint32_t iter;
   int mark_preds;
+  const uint32_t* iter_ptr;  // device-driven supersteps: the superstep index in memory
   // forward visit (primitives.cpp:216-222): test-and-set on the visited bitmap.
   // The pre-test reads L2 (ld.cg): an L1 copy would keep showing bits other
   // SMs have since set, turning every later test into an atomic.
@@ -256,11 +279,12 @@ __device__ __forceinline__ void visit_batch(const DobfsDev& f, const uint32_t* s
 #pragma unroll
   for (int k = 0; k < K; ++k)
     old[k] = pass[k] ? atomicOr(&f.vis[nb[k] >> 5], 1u << (nb[k] & 31)) : ~0u;
+  const uint32_t label = (f.iter_ptr ? *f.iter_ptr : f.iter) + 1;
 #pragma unroll
   for (int k = 0; k < K; ++k) {
     acc[k] = !(old[k] & (1u << (nb[k] & 31)));
     if (acc[k]) {
-      f.labels[nb[k]] = f.iter + 1;
+      f.labels[nb[k]] = label;
       if (f.mark_preds) f.preds[nb[k]] = f.ow.to_global(src[k]);
     }
   }
@@ -271,9 +295,12 @@ __device__ __forceinline__ void visit_batch(const DobfsDev& f, const uint32_t* s
 // (forward superstep run as a pull), saving two tiny copies per pull step.
 __global__ void frontier_diff_kernel(const uint32_t* __restrict__ vis, uint32_t* prev,
                                      uint32_t* __restrict__ fb, uint32_t nw, uint32_t* zero2,
-                                     unsigned long long* w_dst, unsigned long long w_val) {
+                                     unsigned long long* w_dst, unsigned long long w_val,
+                                     const DobfsLoop* st = nullptr,
+                                     unsigned long long* w_dyn = nullptr) {
   if (blockIdx.x == 0 && threadIdx.x == 0) {
     zero2[0] = zero2[1] = 0u;
+    if (st && st->dir == 0) *w_dyn = st->in_degsum;  // forward superstep run as a pull
     if (w_dst) *w_dst = w_val;
   }
   const uint4* v4 = reinterpret_cast<const uint4*>(vis);
@@ -405,7 +432,15 @@ __global__ void __launch_bounds__(256, 4)
                              OwnerView ow, int emit_found, uint32_t* out, uint32_t* ul_out,
                              uint32_t* ul_out_cnt, uint32_t* longq, uint32_t* long_cnt,
                              Counters* ctr, unsigned long long* scanned_out,
-                             unsigned long long* deg_out) {
+                             unsigned long long* deg_out, DobfsDyn dyn) {
+  if (dyn.st) {
+    const uint32_t src = dyn.st->ul_src;
+    nul = dyn.st->ul_len;
+    ul = src == 2 ? nullptr : (src == 0 ? dyn.ub0 : dyn.ub1);
+    ul_out = src == 0 ? dyn.ub1 : dyn.ub0;
+    next_label = dyn.st->iter + 1;
+    scanned_out = dyn.st->dir == 1 ? &ctr->edges : &ctr->u[3];
+  }
   uint32_t scanned = 0, opened = 0, degs = 0;  // per-thread partials fit 32 bits
   uint32_t found_n = 0;
   // queues hold up to kPullQ entries and are flushed only when one could
@@ -505,7 +540,13 @@ __global__ void __launch_bounds__(256)
                             const uint32_t* __restrict__ fb, uint32_t next_label, int mark_preds,
                             OwnerView ow, int emit_found, uint32_t* out, uint32_t* ul_out,
                             uint32_t* ul_out_cnt, Counters* ctr,
-                            unsigned long long* scanned_out, unsigned long long* deg_out) {
+                            unsigned long long* scanned_out, unsigned long long* deg_out,
+                            DobfsDyn dyn) {
+  if (dyn.st) {
+    ul_out = dyn.st->ul_src == 0 ? dyn.ub1 : dyn.ub0;
+    next_label = dyn.st->iter + 1;
+    scanned_out = dyn.st->dir == 1 ? &ctr->edges : &ctr->u[3];
+  }
   __shared__ BlockQueue<256 / kPullGroup * kGroupIters> q_found, q_keep;
   unsigned long long degs = 0;
   __shared__ uint32_t s_found;
@@ -616,6 +657,87 @@ __global__ void dobfs_share_kernel(Counters* ctr, int pulled, uint32_t ul_keep) 
   ctr->u[1] = ctr->next_deg;
 }
 
+// ---------------------------------------------------------------------------
+// Device-driven DOBFS (single partition, exact-cost direction, max policy):
+// the whole superstep loop is ONE CUDA graph — a WHILE node whose body is
+//   decide  (the reference direction rule, primitives.cpp:131-154, and the
+//            exact-cost physical choice, evaluated on the device in the same
+//            double arithmetic as the host path)
+//   IF pull { frontier_diff, pull_thread, pull_group }
+//   IF push { frontier list from vis & ~prev, prev = vis, degree / scan /
+//             tiles / expand, degree sum of the discoveries }
+//   end     (history, loop state, counters cleared, loop condition)
+// so no superstep waits for the host.  Results and statistics equal the
+// host-driven path's (tests/test_gpu_parity.py::test_dobfs_graph_*).
+constexpr uint32_t kLoopHist = 65536;  // supersteps recorded per run
+
+__global__ void dobfs_loop_init_kernel(DobfsLoop* st, uint32_t* labels, uint32_t* vis) {
+  const uint32_t s = st->source;
+  labels[s] = 0u;
+  vis[s >> 5] |= 1u << (s & 31);
+  st->iter = 0;
+  st->dir = 0;
+  st->switched = 0;
+  st->physical = 0;
+  st->in_count = 1;
+  st->ul_src = 2;  // every non-isolated record, no list
+  st->ul_len = st->n_nonisolated;
+  st->in_degsum = 0;
+  st->visited = 1;
+}
+
+__global__ void dobfs_loop_decide_kernel(DobfsLoop* st, DobfsHist* hist,
+                                         cudaGraphConditionalHandle h_pull,
+                                         cudaGraphConditionalHandle h_push) {
+  const uint32_t t = st->iter;
+  if (t >= 1) {  // primitives.cpp:197-205: decision on global quantities
+    st->visited += st->in_count;
+    const double fv = st->nv > 0 ? (double)st->in_count * st->ne_d / st->nv_d : 0.0;
+    const double bv = st->visited > 0 ? (double)((unsigned long long)st->nv - st->visited) *
+                                            st->nv_d / (double)st->visited
+                                      : 0.0;
+    uint32_t next;
+    if (st->dir == 0) next = (!st->switched && fv > bv * st->do_a) ? 1u : 0u;
+    else next = fv < bv * st->do_b ? 0u : 1u;
+    if (next == 1 && st->dir == 0) st->switched = 1;
+    st->dir = next;
+  }
+  uint32_t phys = st->dir == 1;
+  if (!phys && st->exact && t > 0 && st->in_count && st->in_degsum > 4ull * st->ul_len) phys = 1;
+  st->physical = phys;
+  hist[t].dir = st->dir;
+  hist[t].physical = phys;
+  if (!phys) st->in_count = 0;  // the push recounts its list from the bitmap
+  cudaGraphSetConditional(h_pull, phys);
+  cudaGraphSetConditional(h_push, phys ? 0u : 1u);
+}
+
+__global__ void dobfs_loop_end_kernel(DobfsLoop* st, Counters* ctr, DobfsHist* hist,
+                                      cudaGraphConditionalHandle h_while) {
+  __shared__ uint32_t s_out;
+  const uint32_t t = st->iter;
+  if (threadIdx.x == 0) {
+    const uint32_t out = ctr->out_cnt;
+    s_out = out;
+    hist[t].out = out;
+    hist[t].edges = ctr->edges;
+    if (st->physical) {  // the pull compacted the unvisited list (ping-pong)
+      st->ul_len = ctr->misc;
+      st->ul_src = st->ul_src == 0 ? 1 : 0;
+    }
+    st->in_count = out;
+    st->in_degsum = ctr->next_deg;
+  }
+  __syncthreads();
+  uint32_t* c = reinterpret_cast<uint32_t*>(ctr);
+  for (uint32_t i = threadIdx.x; i < sizeof(Counters) / 4; i += blockDim.x) c[i] = 0u;
+  if (threadIdx.x == 0) {
+    st->iter = t + 1;
+    const bool more = s_out > 0 && t + 1 < st->max_supersteps && t + 1 < kLoopHist;
+    cudaGraphSetConditional(h_while, more ? 1u : 0u);
+  }
+}
+
 struct DobfsPrim : PrimBase {
   uint32_t source;
   double do_a, do_b;
@@ -638,7 +760,7 @@ struct DobfsPrim : PrimBase {
     communication = MG_COMM_BROADCAST;
   }
   static uint64_t words(uint32_t nv) { return (nv + 31) / 32 + 1; }
-  void ensure_nonisolated(Worker& w) {
+  static void ensure_nonisolated(Worker& w) {
     if (w.nonisolated_ready) return;
     uint32_t nh = (uint32_t)w.hosted_host.size();
     w.nonisolated.alloc(nh ? nh : 1);
@@ -812,11 +934,12 @@ struct DobfsPrim : PrimBase {
                  w.stream, w.pull_rec.ptr, ul, nul, w.su32[0].ptr, w.su32[1].ptr, w.su32[2].ptr,
                  w.su32[3].ptr, next_label, mark_preds ? 1 : 0, c.owner_view(), emit ? 1 : 0,
                  w.output.ptr, w.ul_buf[dst].ptr, ulcnt, w.ul_buf[2].ptr, cnts + 1, c.ctr(),
-                 scanned, deg_out);
+                 scanned, deg_out, DobfsDyn{nullptr, nullptr, nullptr});
       MGB_LAUNCH(dobfs_pull_group_kernel, kNumSMs * 8, 256, 0, w.stream, w.graph(),
                  w.pull_rec.ptr, w.ul_buf[2].ptr, cnts + 1, w.su32[0].ptr, w.su32[1].ptr,
                  w.su32[2].ptr, w.su32[3].ptr, next_label, mark_preds ? 1 : 0, c.owner_view(),
-                 emit ? 1 : 0, w.output.ptr, w.ul_buf[dst].ptr, ulcnt, c.ctr(), scanned, deg_out);
+                 emit ? 1 : 0, w.output.ptr, w.ul_buf[dst].ptr, ulcnt, c.ctr(), scanned, deg_out,
+                 DobfsDyn{nullptr, nullptr, nullptr});
     }
     list_free[w.p] = !emit;
     if (c.P->profile) {
@@ -870,6 +993,265 @@ struct DobfsPrim : PrimBase {
   std::vector<bool> list_free;  // per worker: last pull step counted, did not list
   std::vector<bool> prof_pending_ = std::vector<bool>(kMaxWorkers, false);
   std::vector<uint32_t> prof_nul_ = std::vector<uint32_t>(kMaxWorkers, 0);
+};
+
+// one graph per (worker, mark_preds), built on first use
+struct DobfsGraph {
+  cudaGraphExec_t exec;
+  uint32_t n_pull, n_push;  // kernels in each branch (launch accounting)
+};
+
+struct DobfsGraphRun {
+  std::vector<int> dir_log;
+  std::vector<uint64_t> edges, out;
+  uint64_t launches = 0;
+  bool complete = true;
+};
+
+class DobfsGraphRunner {
+ public:
+  static bool eligible(const Plan& P, const mg_config& c) {
+    // The graph removes the per-superstep host round trip (~4 us each), which
+    // pays on small graphs (RMAT-18..22: 7-10% less device time); on RMAT-26
+    // the superstep kernels dominate and the host loop measured 1.3% faster
+    // (tools/graph_probe.py), so by default only graphs under 2^30 arcs use
+    // it.  MG_GRAPH_LOOP=1 forces it on, MG_NO_GRAPH (any value) forces off.
+    const char* force = getenv("MG_GRAPH_LOOP");
+    const bool big = P.ne >= (1ull << 30);
+    const bool off = getenv("MG_NO_GRAPH") != nullptr ||
+                     (force ? force[0] == '0' : big);
+    const bool fused = c.fused == MG_FUSED_ON || (c.fused == MG_FUSED_AUTO &&
+                                                  c.policy == MG_POLICY_FUSED);
+    return !off && P.n == 1 && P.dup == MG_DUP_ALL && c.dobfs_exact_cost && !P.profile &&
+           c.policy == MG_POLICY_MAX && fused && !c.drop_enabled && c.hard_cap_bytes == 0;
+  }
+
+  // runs one DOBFS (or the BFS schedule with do_a = inf); fills P.last & co.
+  static DobfsGraphRun run(Plan& P, uint32_t source, double do_a, double do_b, bool mark_preds,
+                           const mg_config& cfg, const char* name, int comm) {
+    auto t0 = std::chrono::steady_clock::now();
+    Worker& w = *P.workers[P.local_workers.front()];
+    DeviceGuard dg(w.dev);
+    DobfsPrim::ensure_nonisolated(w);
+    ensure_buffers(w);
+    const DobfsGraph G = graph(w, mark_preds);
+    const uint64_t nw = (w.nv + 31) / 32 + 1;
+    DobfsLoop h{};
+    h.nv_d = (double)P.nv;
+    h.ne_d = (double)P.ne;
+    h.do_a = do_a;
+    h.do_b = do_b;
+    h.nv = P.nv;
+    h.source = source;
+    h.max_supersteps = (uint32_t)(cfg.max_supersteps < kLoopHist ? cfg.max_supersteps : kLoopHist);
+    h.exact = 1;
+    h.n_nonisolated = w.n_nonisolated;
+    DobfsLoop* lh = static_cast<DobfsLoop*>(w.loop_host);
+    DobfsHist* hh = static_cast<DobfsHist*>(w.loop_hist_host);
+    *lh = h;
+    MGB_CUDA(cudaEventRecord(w.ev_start, w.stream));
+    MGB_CUDA(cudaMemcpyAsync(w.loop_state.ptr, w.loop_host, sizeof(DobfsLoop),
+                             cudaMemcpyHostToDevice, w.stream));
+    MGB_CUDA(cudaMemsetAsync(w.ctr.ptr, 0, sizeof(Counters), w.stream));
+    MGB_CUDA(cudaMemsetAsync(w.su32[0].ptr, 0xFF, 4ull * w.nv, w.stream));  // labels
+    MGB_CUDA(cudaMemsetAsync(w.su32[2].ptr, 0, 4 * nw, w.stream));          // visited
+    MGB_CUDA(cudaMemsetAsync(w.aux[4].ptr, 0, 4 * nw, w.stream));           // visited (prev)
+    if (mark_preds) MGB_CUDA(cudaMemsetAsync(w.su32[1].ptr, 0xFF, 4ull * w.nv, w.stream));
+    MGB_LAUNCH(dobfs_loop_init_kernel, 1, 1, 0, w.stream,
+               reinterpret_cast<DobfsLoop*>(w.loop_state.ptr), w.su32[0].ptr, w.su32[2].ptr);
+    MGB_CUDA(cudaGraphLaunch(G.exec, w.stream));
+    MGB_CUDA(cudaEventRecord(w.ev_end, w.stream));
+    MGB_CUDA(cudaMemcpyAsync(w.loop_host, w.loop_state.ptr, sizeof(DobfsLoop),
+                             cudaMemcpyDeviceToHost, w.stream));
+    MGB_CUDA(cudaStreamSynchronize(w.stream));
+    const uint32_t S = lh->iter;
+    MGB_CUDA(cudaMemcpy(hh, w.loop_hist.ptr, sizeof(DobfsHist) * S, cudaMemcpyDeviceToHost));
+    DobfsGraphRun r;
+    uint64_t W = 0, launches = 2;  // init kernel + graph
+    for (uint32_t t = 0; t < S; ++t) {
+      const DobfsHist& e = hh[t];
+      r.dir_log.push_back((int)e.dir);
+      r.edges.push_back(e.edges);
+      r.out.push_back(e.out);
+      W += e.edges;
+      launches += 2 + (e.physical ? G.n_pull : G.n_push);
+    }
+    r.launches = launches;
+    const bool hit_cap = S >= kLoopHist && cfg.max_supersteps > kLoopHist && S && r.out.back();
+    r.complete = !hit_cap;
+    float ms = 0;
+    cudaEventElapsedTime(&ms, w.ev_start, w.ev_end);
+    // statistics in the engine's shapes (run_primitive)
+    mg_stats& st = P.last;
+    st = mg_stats{};
+    st.n = 1;
+    st.stop_reason = (S && r.out.back() == 0) ? MG_STOP_FRONTIERS_EMPTY : MG_STOP_MAX_SUPERSTEPS;
+    st.communication = comm;
+    st.policy = cfg.policy;
+    st.supersteps = S;
+    st.edges_examined = W;
+    st.wall_ms =
+        std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+    st.device_ms = ms;
+    st.gpu_launches = launches;
+    P.h_matrix.assign(1, std::vector<uint64_t>(1, 0));
+    P.h_per_iter.assign(S, std::vector<uint64_t>(1, 0));
+    P.out_per_iter = r.out;
+    P.edges_per_iter = r.edges;
+    P.combine_per_iter.assign(S, 0);
+    collect_buffer_stats(P);
+    g_launches.fetch_add(launches, std::memory_order_relaxed);
+    (void)name;
+    return r;
+  }
+
+ private:
+  // every device pointer a captured graph holds; a change (a buffer another
+  // primitive regrew) forces a re-capture
+  static std::vector<const void*> pointers(const Worker& w) {
+    return {w.su32[0].ptr, w.su32[1].ptr, w.su32[2].ptr, w.su32[3].ptr, w.aux[2].ptr,
+            w.aux[4].ptr, w.ul_buf[0].ptr, w.ul_buf[1].ptr, w.ul_buf[2].ptr, w.pull_rec.ptr,
+            w.off.ptr, w.col.ptr, w.owner.ptr, w.ctr.ptr, w.loop_state.ptr, w.loop_hist.ptr,
+            w.loop_front[0].ptr, w.loop_front[1].ptr, w.loop_lb_row.ptr, w.loop_lb_pref.ptr,
+            w.loop_lb_bsum.ptr, w.loop_total.ptr, w.loop_tiles.ptr};
+  }
+  static void ensure_buffers(Worker& w) {
+    const uint64_t nw0 = (w.nv + 31) / 32 + 1;
+    if (w.su32[0].n < w.nv || !w.su32[0].ptr) w.su32[0].alloc(w.nv ? w.nv : 1);  // labels
+    if (w.su32[1].n < w.nv || !w.su32[1].ptr) w.su32[1].alloc(w.nv ? w.nv : 1);  // preds
+    if (w.su32[2].n < nw0 || !w.su32[2].ptr) w.su32[2].alloc(nw0);               // visited
+    if (w.su32[3].n < nw0 || !w.su32[3].ptr) w.su32[3].alloc(nw0);               // frontier
+    if (w.aux[4].n < nw0 || !w.aux[4].ptr) w.aux[4].alloc(nw0);                  // prev
+    if (w.aux[2].n < 4 || !w.aux[2].ptr) w.aux[2].alloc(4);
+    if (w.loop_state.ptr) return;
+    const uint64_t nw = (w.nv + 31) / 32 + 1;
+    const uint64_t k = w.n_nonisolated ? w.n_nonisolated : 1;
+    w.loop_state.alloc(sizeof(DobfsLoop));
+    w.loop_hist.alloc(sizeof(DobfsHist) * kLoopHist);
+    MGB_CUDA(cudaMallocHost(&w.loop_host, sizeof(DobfsLoop)));
+    MGB_CUDA(cudaMallocHost(&w.loop_hist_host, sizeof(DobfsHist) * kLoopHist));
+    for (int i = 0; i < 3; ++i)
+      if (w.ul_buf[i].n < k + 1 || !w.ul_buf[i].ptr) w.ul_buf[i].alloc(k + 1);
+    w.loop_front[0].alloc(w.nv ? w.nv : 1);
+    w.loop_front[1].alloc(w.nv ? w.nv : 1);
+    w.loop_lb_row.alloc(w.nv ? w.nv : 1);
+    w.loop_lb_pref.alloc(w.nv ? w.nv : 1);
+    w.loop_lb_bsum.alloc(w.nv / kLbBlock + 4);
+    w.loop_total.alloc(1);
+    const uint64_t max_tiles = (2 * w.ne + 1) / kTile + 2 + kMinTiles;
+    w.loop_tiles.alloc(max_tiles + 1);
+  }
+
+  static DobfsGraph graph(Worker& w, bool mark_preds) {
+    const int gi = mark_preds ? 1 : 0;
+    const std::vector<const void*> ptrs = pointers(w);
+    if (w.loop_exec[gi] && w.loop_ptrs[gi] == ptrs)
+      return {w.loop_exec[gi], w.loop_n_pull[gi], w.loop_n_push[gi]};
+    if (w.loop_exec[gi]) {  // a captured buffer moved
+      cudaGraphExecDestroy(w.loop_exec[gi]);
+      w.loop_exec[gi] = nullptr;
+    }
+    w.loop_ptrs[gi] = ptrs;
+    cudaStream_t s = w.stream;
+    const uint64_t nw = (w.nv + 31) / 32 + 1;
+    DobfsLoop* st = reinterpret_cast<DobfsLoop*>(w.loop_state.ptr);
+    DobfsHist* hist = reinterpret_cast<DobfsHist*>(w.loop_hist.ptr);
+    Counters* ctr = w.ctr.ptr;
+    cudaGraph_t g;
+    MGB_CUDA(cudaGraphCreate(&g, 0));
+    cudaGraphConditionalHandle h_while;
+    MGB_CUDA(cudaGraphConditionalHandleCreate(&h_while, g, 1, cudaGraphCondAssignDefault));
+    cudaGraphNodeParams wp = {};
+    wp.type = cudaGraphNodeTypeConditional;
+    wp.conditional.handle = h_while;
+    wp.conditional.type = cudaGraphCondTypeWhile;
+    wp.conditional.size = 1;
+    cudaGraphNode_t wnode;
+    MGB_CUDA(cudaGraphAddNode(&wnode, g, nullptr, 0, &wp));
+    cudaGraph_t body = wp.conditional.phGraph_out[0];
+    cudaGraphConditionalHandle h_pull, h_push;
+    MGB_CUDA(cudaGraphConditionalHandleCreate(&h_pull, body, 0, cudaGraphCondAssignDefault));
+    MGB_CUDA(cudaGraphConditionalHandleCreate(&h_push, body, 0, cudaGraphCondAssignDefault));
+    // decide
+    MGB_CUDA(cudaStreamBeginCaptureToGraph(s, body, nullptr, nullptr, 0,
+                                           cudaStreamCaptureModeRelaxed));
+    MGB_LAUNCH(dobfs_loop_decide_kernel, 1, 1, 0, s, st, hist, h_pull, h_push);
+    cudaGraph_t tmp;
+    MGB_CUDA(cudaStreamEndCapture(s, &tmp));
+    size_t nn = 0;
+    MGB_CUDA(cudaGraphGetNodes(body, nullptr, &nn));
+    std::vector<cudaGraphNode_t> nodes(nn);
+    MGB_CUDA(cudaGraphGetNodes(body, nodes.data(), &nn));
+    cudaGraphNode_t decide = nodes[0];
+    // IF pull / IF push
+    cudaGraphNode_t ifs[2];
+    cudaGraph_t bodies[2];
+    cudaGraphConditionalHandle hs[2] = {h_pull, h_push};
+    for (int i = 0; i < 2; ++i) {
+      cudaGraphNodeParams ip = {};
+      ip.type = cudaGraphNodeTypeConditional;
+      ip.conditional.handle = hs[i];
+      ip.conditional.type = cudaGraphCondTypeIf;
+      ip.conditional.size = 1;
+      MGB_CUDA(cudaGraphAddNode(&ifs[i], body, &decide, 1, &ip));
+      bodies[i] = ip.conditional.phGraph_out[0];
+    }
+    GraphView gv = w.graph();
+    OwnerView ow{w.owner.ptr, w.l2g.ptr, w.p, w.nlocal, MG_DUP_ALL};
+    uint32_t* cnts = w.aux[2].ptr;
+    DobfsDyn dyn{st, w.ul_buf[0].ptr, w.ul_buf[1].ptr};
+    const int mp = mark_preds ? 1 : 0;
+    uint64_t l0 = g_launches.load();
+    // pull branch
+    MGB_CUDA(cudaStreamBeginCaptureToGraph(s, bodies[0], nullptr, nullptr, 0,
+                                           cudaStreamCaptureModeRelaxed));
+    MGB_LAUNCH(frontier_diff_kernel, grid_for(nw, 256, kNumSMs * 8), 256, 0, s, w.su32[2].ptr,
+               w.aux[4].ptr, w.su32[3].ptr, (uint32_t)nw, cnts, nullptr, 0ull,
+               (const DobfsLoop*)st, &ctr->edges);
+    MGB_LAUNCH(dobfs_pull_thread_kernel, kNumSMs * 4, 256, 0, s, w.pull_rec.ptr, nullptr, 0u,
+               w.su32[0].ptr, w.su32[1].ptr, w.su32[2].ptr, w.su32[3].ptr, 0u, mp, ow, 0,
+               w.loop_front[1].ptr, nullptr, &ctr->misc, w.ul_buf[2].ptr, cnts + 1, ctr,
+               (unsigned long long*)nullptr, &ctr->next_deg, dyn);
+    MGB_LAUNCH(dobfs_pull_group_kernel, kNumSMs * 8, 256, 0, s, gv, w.pull_rec.ptr,
+               w.ul_buf[2].ptr, cnts + 1, w.su32[0].ptr, w.su32[1].ptr, w.su32[2].ptr,
+               w.su32[3].ptr, 0u, mp, ow, 0, w.loop_front[1].ptr, nullptr, &ctr->misc, ctr,
+               (unsigned long long*)nullptr, &ctr->next_deg, dyn);
+    MGB_CUDA(cudaStreamEndCapture(s, &tmp));
+    const uint64_t l1 = g_launches.load();
+    // push branch: frontier list from the bitmap, prev = vis, edge-balanced advance
+    MGB_CUDA(cudaStreamBeginCaptureToGraph(s, bodies[1], nullptr, nullptr, 0,
+                                           cudaStreamCaptureModeRelaxed));
+    MGB_LAUNCH(bitmap_diff_list_kernel, grid_for(nw, 256, kNumSMs * 8), 256, 0, s, w.su32[2].ptr,
+               w.aux[4].ptr, (uint32_t)nw, w.loop_front[0].ptr, &st->in_count);
+    MGB_CUDA(cudaMemcpyAsync(w.aux[4].ptr, w.su32[2].ptr, 4 * nw, cudaMemcpyDeviceToDevice, s));
+    const uint32_t* nin = &st->in_count;
+    MGB_LAUNCH(lb_degree_kernel, kNumSMs * 8, kLbBlock, 0, s, w.off.ptr, w.loop_front[0].ptr, 0u,
+               w.loop_lb_row.ptr, w.loop_lb_pref.ptr, w.loop_lb_bsum.ptr, nin);
+    MGB_LAUNCH(lb_scan_kernel, 1, 1024, 0, s, w.loop_lb_bsum.ptr, 0u, w.loop_total.ptr,
+               &ctr->edges, nin);
+    const uint64_t max_tiles = (2 * w.ne + 1) / kTile + 2 + kMinTiles;
+    MGB_LAUNCH(lb_tiles_kernel, kNumSMs * 8, 256, 0, s, w.loop_lb_pref.ptr, w.loop_lb_bsum.ptr,
+               0u, w.loop_total.ptr, w.loop_tiles.ptr, (uint32_t)max_tiles, nin);
+    DobfsDev f{w.su32[0].ptr, w.su32[1].ptr, w.su32[2].ptr, w.su32[3].ptr, ow, 0u, mp, &st->iter};
+    MGB_LAUNCH((lb_expand_kernel<DobfsDev, true>), kNumSMs * 6, kExpBlock, 0, s, f, gv,
+               w.loop_front[0].ptr, 0u, w.loop_lb_row.ptr, w.loop_lb_pref.ptr, w.loop_lb_bsum.ptr,
+               w.loop_total.ptr, w.loop_tiles.ptr, w.loop_front[1].ptr, &ctr->out_cnt, nin);
+    MGB_LAUNCH(degsum_dev_kernel, kNumSMs * 4, 256, 0, s, gv, w.loop_front[1].ptr,
+               &ctr->out_cnt, &ctr->next_deg);
+    MGB_CUDA(cudaStreamEndCapture(s, &tmp));
+    const uint64_t l2 = g_launches.load();
+    // end (after both branches)
+    MGB_CUDA(cudaStreamBeginCaptureToGraph(s, body, ifs, nullptr, 2,
+                                           cudaStreamCaptureModeRelaxed));
+    MGB_LAUNCH(dobfs_loop_end_kernel, 1, 256, 0, s, st, ctr, hist, h_while);
+    MGB_CUDA(cudaStreamEndCapture(s, &tmp));
+    g_launches.store(l0);  // capture is not execution
+    MGB_CUDA(cudaGraphInstantiate(&w.loop_exec[gi], g, 0));
+    MGB_CUDA(cudaGraphDestroy(g));
+    w.loop_n_pull[gi] = (uint32_t)(l1 - l0);
+    w.loop_n_push[gi] = (uint32_t)(l2 - l1);
+    return {w.loop_exec[gi], w.loop_n_pull[gi], w.loop_n_push[gi]};
+  }
 };
 
 // ===========================================================================
@@ -2573,7 +2955,13 @@ int mg_bfs(mg_plan* plan, uint32_t source, int mark_preds, const mg_config* cfg,
     check_source(P, source, "bfs");
     mg_config c = cfg_or_default(cfg);
     P.last = mg_stats{};
-    if (c.dobfs_exact_cost && P.n == 1) {
+    bool done = false;
+    if (c.dobfs_exact_cost && DobfsGraphRunner::eligible(P, c))
+      done = DobfsGraphRunner::run(P, source, INFINITY, 0.1, mark_preds != 0, c, "bfs",
+                                   MG_COMM_SELECTIVE)
+                 .complete;
+    if (done) {
+    } else if (c.dobfs_exact_cost && P.n == 1) {
       // extension: the BFS schedule (every superstep logically forward: a
       // direction rule that never switches) on the DOBFS machinery, heavy
       // supersteps run physically as pulls; labels, S and W are BFS's
@@ -2621,18 +3009,31 @@ int mg_dobfs(mg_plan* plan, uint32_t source, double do_a, double do_b, int mark_
     Plan& P = *reinterpret_cast<Plan*>(plan);
     check_source(P, source, "dobfs");
     mg_config c = cfg_or_default(cfg);
-    DobfsPrim prim(source, do_a, do_b, mark_preds != 0, c.dobfs_exact_cost != 0, P.n);
-    P.last = mg_stats{};
-    run_primitive(P, prim, c);
+    std::vector<int> dir_log;
+    bool done = false;
+    if (DobfsGraphRunner::eligible(P, c)) {  // device-driven supersteps (one graph launch)
+      DobfsGraphRun r = DobfsGraphRunner::run(P, source, do_a, do_b, mark_preds != 0, c, "dobfs",
+                                              MG_COMM_BROADCAST);
+      if (r.complete) {
+        dir_log = r.dir_log;
+        done = true;
+      }
+    }
+    if (!done) {
+      DobfsPrim prim(source, do_a, do_b, mark_preds != 0, c.dobfs_exact_cost != 0, P.n);
+      P.last = mg_stats{};
+      run_primitive(P, prim, c);
+      dir_log = prim.dir_log;
+    }
     P.last_result_kind = 0;
     gather_labels_u32(P, pw(P, &Worker::su32, 0), labels, P.last.supersteps);
     if (mark_preds) gather_u32(P, pw(P, &Worker::su32, 1), preds);
-    if (len) *len = prim.dir_log.size();
-    for (uint64_t i = 0; direction_log && i < prim.dir_log.size() && i < cap; ++i)
-      direction_log[i] = prim.dir_log[i];
+    if (len) *len = dir_log.size();
+    for (uint64_t i = 0; direction_log && i < dir_log.size() && i < cap; ++i)
+      direction_log[i] = dir_log[i];
     uint64_t f = 0, b = 0;
-    for (size_t i = 0; i < prim.dir_log.size() && i < P.edges_per_iter.size(); ++i)
-      (prim.dir_log[i] ? b : f) += P.edges_per_iter[i];
+    for (size_t i = 0; i < dir_log.size() && i < P.edges_per_iter.size(); ++i)
+      (dir_log[i] ? b : f) += P.edges_per_iter[i];
     if (forward_edges) *forward_edges = f;
     if (backward_edges) *backward_edges = b;
     finish_stats(P, stats);

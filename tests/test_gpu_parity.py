@@ -427,3 +427,67 @@ def test_dobfs_exact_cost_several_partitions(n):
                 continue
             p = int(b.preds[v])
             assert b.labels[p] + 1 == b.labels[v] and v in col[off[p]:off[p + 1]]
+
+
+GRAPH_CFG = mg.EngineConfig(policy=mg.AllocPolicyKind.Maximum, fused=mg.FusedMode.On,
+                            dobfs_exact_cost=True)
+
+
+def _host_loop(fn):
+    import os
+    os.environ["MG_NO_GRAPH"] = "1"
+    try:
+        return fn()
+    finally:
+        del os.environ["MG_NO_GRAPH"]
+
+
+@pytest.mark.parametrize("scale,ef,seed", [(12, 16, 1), (14, 16, 3), (12, 32, 6)])
+def test_dobfs_graph_loop_equals_host_loop(scale, ef, seed):
+    """the device-driven superstep loop (one CUDA graph with WHILE/IF nodes)
+    reproduces the host-driven run: labels, direction log, S, W and the
+    per-superstep frontier sizes and edge counts"""
+    g = mg.Csr.rmat(scale, ef, seed)
+    off, col, _ = g.arrays()
+    plan = mg.PartitionPlan(g, None, 1)
+    for src in (0, 3, 77):
+        for do_a in (0.01, 0.001):
+            opt = mg.DobfsOptions(source=src, do_a=do_a, mark_preds=True)
+            a = mg.dobfs(plan, opt, GRAPH_CFG)
+            b = _host_loop(lambda: mg.dobfs(plan, opt, GRAPH_CFG))
+            assert np.array_equal(a.labels, seq.bfs_levels(off, col, src))
+            assert np.array_equal(a.labels, b.labels)
+            assert list(a.direction_log) == list(b.direction_log)
+            assert a.stats.supersteps == b.stats.supersteps
+            assert a.stats.edges_examined == b.stats.edges_examined
+            assert np.array_equal(a.stats.edges_per_iter, b.stats.edges_per_iter)
+            assert np.array_equal(a.stats.out_per_iter, b.stats.out_per_iter)
+            assert a.forward_edges == b.forward_edges and a.backward_edges == b.backward_edges
+            for v in np.nonzero(a.labels != mg.kInfLabel)[0][:300]:
+                if v == src:
+                    continue
+                p = int(a.preds[v])
+                assert a.labels[p] + 1 == a.labels[v] and v in col[off[p]:off[p + 1]]
+    # the BFS schedule through the same graph
+    a = mg.bfs(plan, mg.BfsOptions(source=0), GRAPH_CFG)
+    b = mg.bfs(plan, mg.BfsOptions(source=0))
+    assert np.array_equal(a.labels, b.labels)
+    assert a.stats.supersteps == b.stats.supersteps
+    assert a.stats.edges_examined == b.stats.edges_examined
+
+
+def test_dobfs_graph_loop_max_supersteps_and_isolated_source():
+    g = mg.Csr.rmat(12, 16, 1)
+    off, col, _ = g.arrays()
+    plan = mg.PartitionPlan(g, None, 1)
+    cfg = mg.EngineConfig(policy=mg.AllocPolicyKind.Maximum, fused=mg.FusedMode.On,
+                          dobfs_exact_cost=True, max_supersteps=2)
+    a = mg.dobfs(plan, mg.DobfsOptions(source=0), cfg)
+    b = _host_loop(lambda: mg.dobfs(plan, mg.DobfsOptions(source=0), cfg))
+    assert a.stats.supersteps == b.stats.supersteps == 2
+    assert np.array_equal(a.labels, b.labels)
+    assert a.stats.stop_reason == b.stats.stop_reason
+    iso = int(np.nonzero(np.diff(off) == 0)[0][0])
+    r = mg.dobfs(plan, mg.DobfsOptions(source=iso), GRAPH_CFG)
+    assert r.labels[iso] == 0 and int((r.labels != mg.kInfLabel).sum()) == 1
+    assert r.stats.supersteps == 1

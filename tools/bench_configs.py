@@ -63,6 +63,16 @@ def main():
         off, col, _ = g.arrays()
         deg = np.diff(off.astype(np.int64))
         plan = mg.PartitionPlan(g, None, 1)
+        exact = mg.EngineConfig(policy=mg.AllocPolicyKind.Maximum, fused=mg.FusedMode.On,
+                                dobfs_exact_cost=True)
+        # the exact-cost BFS (same labels) runs as one device-driven graph here
+        r = mg.bfs(plan, mg.BfsOptions(source=0), exact)
+        ar = reached(r.labels, deg, mg.kInfLabel)
+        mean, best = timeit(lambda: mg.bfs(plan, mg.BfsOptions(source=0), exact,
+                                          download=False).stats.device_ms, a.reps)
+        emit(config=1, primitive="bfs_exact_cost", graph="rmat18_ef16_seed1", reached_arcs=ar,
+             device_ms_mean=mean, device_ms_min=best, gteps=ar / (mean * 1e-3) / 1e9,
+             supersteps=int(r.stats.supersteps))
         r = mg.bfs(plan, mg.BfsOptions(source=0), MAXCFG)
         ar = reached(r.labels, deg, mg.kInfLabel)
         mean, best = timeit(lambda: mg.bfs(plan, mg.BfsOptions(source=0), MAXCFG,
