@@ -350,6 +350,14 @@ constexpr int kPullK = 2;      // arcs held in the record
 constexpr int kPullGroup = 8;  // lanes per vertex in the long-row pass
 constexpr int kPV = 8;         // records per thread per iteration (loads in flight)
 constexpr uint32_t kPullQ = 256 * kPV + 1024;  // CTA queue capacity (> one chunk of 256 * kPV)
+#ifndef MG_PULL_MID
+#define MG_PULL_MID 8
+#endif
+// arcs [kPullK, kPullK + kPullMid) of rows the record did not settle are tested
+// by the thread stage itself (one offset load + one or two col sectors per row);
+// only rows longer than kPullStart go on to the cooperative stage
+constexpr int kPullMid = MG_PULL_MID;
+constexpr uint32_t kPullStart = kPullK + kPullMid;
 
 __global__ void pull_records_kernel(GraphView g, const uint32_t* __restrict__ ni, uint32_t n,
                                     uint4* rec) {
@@ -419,14 +427,16 @@ __device__ __forceinline__ void warp_set_bits_smem(uint32_t* bits, uint32_t* win
 
 // pull step, stage 1 (primitives.cpp:230-251): one thread per unvisited record
 // tests the record's two arcs against the frontier bitmap; a hit labels the
-// vertex, a short row without a hit stays unvisited, a longer row goes to the
+// vertex, a short row without a hit stays unvisited, a longer row is tested on
+// up to kPullStart arcs by stage 1b below and only then goes to the
 // cooperative stage.  CTA queues with one shared atomic per warp and one
 // global atomic per queue per 256*kPV records.  With emit_found == 0 (single
 // partition) the discovered vertices are only counted (and their degrees
 // summed into deg_out when non-null): the next superstep rebuilds the frontier
 // list from the visited bitmap only if it pushes.
 __global__ void __launch_bounds__(256, 4)
-    dobfs_pull_thread_kernel(const uint4* __restrict__ rec, const uint32_t* __restrict__ ul,
+    dobfs_pull_thread_kernel(GraphView g, const uint4* __restrict__ rec,
+                             const uint32_t* __restrict__ ul,
                              uint32_t nul, uint32_t* labels, uint32_t* preds, uint32_t* vis,
                              const uint32_t* __restrict__ fb, uint32_t next_label, int mark_preds,
                              OwnerView ow, int emit_found, uint32_t* out, uint32_t* ul_out,
@@ -448,6 +458,7 @@ __global__ void __launch_bounds__(256, 4)
   __shared__ BlockQueue<kPullQ> q_found, q_keep, q_long;
   __shared__ uint32_t s_found;
   __shared__ uint32_t s_win[256 / 32][kBitSlots];  // visited-bit merge windows
+  __shared__ uint32_t s_mid[kPullMid > 0 ? 256 / 32 : 1][kPullMid > 0 ? 32 * kPV : 1];
   for (uint32_t i = threadIdx.x; i < 8 * kBitSlots; i += blockDim.x) (&s_win[0][0])[i] = 0u;
   q_found.reset();
   q_keep.reset();
@@ -497,7 +508,68 @@ __global__ void __launch_bounds__(256, 4)
 
     if (emit_found) warp_queue_append<kPV>(q_found, found, vv);
     warp_queue_append<kPV>(q_keep, keep, pos);
-    warp_queue_append<kPV>(q_long, lng, pos);
+    if constexpr (kPullMid == 0) {
+      warp_queue_append<kPV>(q_long, lng, pos);
+    } else {
+      // stage 1b: the warp compacts its unsettled rows and spreads them over
+      // all 32 lanes; each lane tests arcs [kPullK, kPullStart) of one row
+      // with independent loads, first hit in arc order wins (exact W)
+      uint32_t* lst = s_mid[threadIdx.x >> 5];
+      const unsigned lt = (1u << lane_id()) - 1u;
+      uint32_t cnt = 0;
+#pragma unroll
+      for (int j = 0; j < kPV; ++j) {
+        const unsigned m = __ballot_sync(0xffffffffu, lng[j]);
+        if (lng[j]) lst[cnt + __popc(m & lt)] = pos[j];
+        cnt += __popc(m);
+      }
+      __syncwarp();
+      for (uint32_t t0 = 0; t0 < cnt; t0 += 32) {
+        const uint32_t t = t0 + lane_id();
+        const bool act = t < cnt;
+        uint32_t p = act ? lst[t] : 0u;
+        const uint4 rr = act ? rec[p] : make_uint4(0, 0, 0, 0);
+        uint32_t v = rr.x;
+        const uint32_t d = rr.y;
+        const uint32_t o = act ? __ldg(&g.off[v]) : 0u;
+        const uint32_t e = d < kPullStart ? d : kPullStart;
+        uint32_t wv[kPullMid > 0 ? kPullMid : 1];
+        bool h[kPullMid > 0 ? kPullMid : 1];
+#pragma unroll
+        for (int k = 0; k < kPullMid; ++k) {
+          const bool ok = act && kPullK + k < e;
+          wv[k] = ok ? __ldg(&g.col[o + kPullK + k]) : 0u;
+          h[k] = ok;
+        }
+#pragma unroll
+        for (int k = 0; k < kPullMid; ++k) h[k] = h[k] && bit_set(fb, wv[k]);
+        int f = -1;
+        uint32_t pw = 0;
+#pragma unroll
+        for (int k = kPullMid - 1; k >= 0; --k)
+          if (h[k]) {
+            f = k;
+            pw = wv[k];
+          }
+        bool fnd = f >= 0;
+        bool kp = act && !fnd && d <= kPullStart;
+        bool lg = act && !fnd && d > kPullStart;
+        if (fnd) {
+          scanned += f + 1;
+          __stcs(&labels[v], next_label);
+          if (mark_preds) preds[v] = ow.to_global(pw);
+          ++found_n;
+          degs += d;
+        } else if (act) {
+          scanned += e - kPullK;
+        }
+        warp_set_bits_smem(vis, s_win[threadIdx.x >> 5], fnd, v);
+        if (emit_found) warp_queue_append<1>(q_found, &fnd, &v);
+        warp_queue_append<1>(q_keep, &kp, &p);
+        warp_queue_append<1>(q_long, &lg, &p);
+      }
+      __syncwarp();
+    }
     __syncthreads();
     const bool last = base + gridDim.x * chunk >= nul;
     if (last || q_found.n > kPullQ - chunk || q_keep.n > kPullQ - chunk ||
@@ -532,6 +604,10 @@ __global__ void __launch_bounds__(256, 4)
 // hit in arc order wins, so W equals the reference's sequential count.  Queue
 // appends are CTA-aggregated like stage 1.
 constexpr int kGroupIters = 4;  // vertices per group between CTA flushes
+#ifndef MG_GROUP_SECTORS
+#define MG_GROUP_SECTORS 4
+#endif
+constexpr int kGroupSectors = MG_GROUP_SECTORS;  // 8-arc sectors per group per round
 
 __global__ void __launch_bounds__(256)
     dobfs_pull_group_kernel(GraphView g, const uint4* __restrict__ rec,
@@ -574,18 +650,43 @@ __global__ void __launch_bounds__(256)
         r = rec[pos];
         v = r.x;
         const uint32_t row = g.off[v];
-        const uint32_t b = row + kPullK, e = row + r.y;
+        const uint32_t b = row + kPullStart, e = row + r.y;
         keep = true;
-        for (uint32_t k = b; k < e; k += kPullGroup) {
-          uint32_t idx = k + sub;
-          uint32_t w = idx < e ? __ldg(&g.col[idx]) : 0u;
-          bool hit = idx < e && bit_set(fb, w);
-          unsigned m = __ballot_sync(gmask, hit) & gmask;
-          if (m) {
-            unsigned first = __ffs(m) - 1 - gbase;
-            uint32_t pw = __shfl_sync(gmask, w, gbase + first);
+        // the first round tests one sector (most rows hit early); later rounds
+        // keep kGroupSectors sectors of the row in flight per group, since a
+        // row that got this far is likely to be scanned to its end
+        uint32_t span = kPullGroup;
+        for (uint32_t k = b; k < e; k += span, span = kPullGroup * kGroupSectors) {
+          uint32_t w[kGroupSectors];
+          bool hit[kGroupSectors];
+#pragma unroll
+          for (int j = 0; j < kGroupSectors; ++j) {
+            const uint32_t idx = k + j * kPullGroup + sub;
+            const bool ok = idx < e && (j == 0 || span > kPullGroup);
+            w[j] = ok ? __ldg(&g.col[idx]) : 0u;
+            hit[j] = ok;
+          }
+#pragma unroll
+          for (int j = 0; j < kGroupSectors; ++j) hit[j] = hit[j] && bit_set(fb, w[j]);
+          int fj = -1;
+          unsigned m = 0;
+#pragma unroll
+          for (int j = kGroupSectors - 1; j >= 0; --j) {  // lowest sector with a hit
+            const unsigned mj = __ballot_sync(gmask, hit[j]) & gmask;
+            if (mj) {
+              fj = j;
+              m = mj;
+            }
+          }
+          if (fj >= 0) {
+            const unsigned first = __ffs(m) - 1 - gbase;
+            uint32_t sel = w[0];
+#pragma unroll
+            for (int j = 1; j < kGroupSectors; ++j)
+              if (j == fj) sel = w[j];
+            const uint32_t pw = __shfl_sync(gmask, sel, gbase + first);
             if (sub == 0) {
-              scanned += k - b + first + 1;
+              scanned += k - b + fj * kPullGroup + first + 1;
               found = true;
               keep = false;
               labels[v] = next_label;
@@ -596,7 +697,7 @@ __global__ void __launch_bounds__(256)
             }
             break;
           }
-          if (sub == 0) scanned += (e - k < (uint32_t)kPullGroup) ? (e - k) : kPullGroup;
+          if (sub == 0) scanned += (e - k < span) ? (e - k) : span;
         }
         if (sub != 0) keep = false;
       }
@@ -931,7 +1032,7 @@ struct DobfsPrim : PrimBase {
         reports_deg && !c.want_deg && c.P->n == 1 ? &c.ctr()->next_deg : nullptr;
     if (nul) {
       MGB_LAUNCH(dobfs_pull_thread_kernel, grid_for(nul, 256 * kPV, kNumSMs * 4), 256, 0,
-                 w.stream, w.pull_rec.ptr, ul, nul, w.su32[0].ptr, w.su32[1].ptr, w.su32[2].ptr,
+                 w.stream, w.graph(), w.pull_rec.ptr, ul, nul, w.su32[0].ptr, w.su32[1].ptr, w.su32[2].ptr,
                  w.su32[3].ptr, next_label, mark_preds ? 1 : 0, c.owner_view(), emit ? 1 : 0,
                  w.output.ptr, w.ul_buf[dst].ptr, ulcnt, w.ul_buf[2].ptr, cnts + 1, c.ctr(),
                  scanned, deg_out, DobfsDyn{nullptr, nullptr, nullptr});
@@ -1208,7 +1309,7 @@ class DobfsGraphRunner {
     MGB_LAUNCH(frontier_diff_kernel, grid_for(nw, 256, kNumSMs * 8), 256, 0, s, w.su32[2].ptr,
                w.aux[4].ptr, w.su32[3].ptr, (uint32_t)nw, cnts, nullptr, 0ull,
                (const DobfsLoop*)st, &ctr->edges);
-    MGB_LAUNCH(dobfs_pull_thread_kernel, kNumSMs * 4, 256, 0, s, w.pull_rec.ptr, nullptr, 0u,
+    MGB_LAUNCH(dobfs_pull_thread_kernel, kNumSMs * 4, 256, 0, s, gv, w.pull_rec.ptr, nullptr, 0u,
                w.su32[0].ptr, w.su32[1].ptr, w.su32[2].ptr, w.su32[3].ptr, 0u, mp, ow, 0,
                w.loop_front[1].ptr, nullptr, &ctr->misc, w.ul_buf[2].ptr, cnts + 1, ctr,
                (unsigned long long*)nullptr, &ctr->next_deg, dyn);
