@@ -203,10 +203,20 @@ struct BfsPrim : PrimBase {
 // examined-edge count W are those of the reference's scan (first hit in arc
 // order), so labels, direction log and W match it exactly.
 
+// exact-cost physical direction: pull when Σdeg(Q) > ratio * |unvisited list|
+// (MG_PULL_RATIO overrides the default, for the sweep in DESIGN.md §7)
+static double pull_ratio() {
+  static const double r = [] {
+    const char* e = getenv("MG_PULL_RATIO");
+    return e ? atof(e) : 4.0;
+  }();
+  return r;
+}
+
 // ---- device-driven supersteps (see DobfsGraph below) ------------------------
 struct DobfsLoop {
   // per-run parameters, written by the host before the graph launch
-  double nv_d, ne_d, do_a, do_b;
+  double nv_d, ne_d, do_a, do_b, pull_ratio;
   uint32_t nv, source, max_supersteps, exact;
   // superstep state, owned by the device
   uint32_t iter, dir, switched, physical;
@@ -804,7 +814,9 @@ __global__ void dobfs_loop_decide_kernel(DobfsLoop* st, DobfsHist* hist,
     st->dir = next;
   }
   uint32_t phys = st->dir == 1;
-  if (!phys && st->exact && t > 0 && st->in_count && st->in_degsum > 4ull * st->ul_len) phys = 1;
+  if (!phys && st->exact && t > 0 && st->in_count &&
+      (double)st->in_degsum > st->pull_ratio * st->ul_len)
+    phys = 1;
   st->physical = phys;
   hist[t].dir = st->dir;
   hist[t].physical = phys;
@@ -968,7 +980,7 @@ struct DobfsPrim : PrimBase {
     uint64_t logical_w = 0;
     if (dir == 0 && exact_cost && c.P->n == 1 && c.in_count && c.iter > 0) {
       logical_w = c.degsum();
-      physical_pull = logical_w > 4ull * ul_len[w.p];
+      physical_pull = (double)logical_w > pull_ratio() * ul_len[w.p];
       if (physical_pull) ++physical_pull_steps;
     } else if (dir == 0 && exact_cost && c.P->n > 1 && c.iter > 0) {
       // several partitions: every worker must take the same physical direction
@@ -980,7 +992,7 @@ struct DobfsPrim : PrimBase {
         gw += r.u[1];
         gul += r.u[0];
       }
-      physical_pull = gw > 4ull * gul;
+      physical_pull = (double)gw > pull_ratio() * gul;
       logical_w = c.in_degsum == kUnknownDeg ? c.degsum() : c.in_degsum;
       if (physical_pull) ++physical_pull_steps;
     }
@@ -1146,6 +1158,7 @@ class DobfsGraphRunner {
     h.source = source;
     h.max_supersteps = (uint32_t)(cfg.max_supersteps < kLoopHist ? cfg.max_supersteps : kLoopHist);
     h.exact = 1;
+    h.pull_ratio = pull_ratio();
     h.n_nonisolated = w.n_nonisolated;
     DobfsLoop* lh = static_cast<DobfsLoop*>(w.loop_host);
     DobfsHist* hh = static_cast<DobfsHist*>(w.loop_hist_host);

@@ -36,7 +36,8 @@ if len(sys.argv) > 2 and sys.argv[1] == "--summarise":
         r = recs[k]
         b = r.get("dram__bytes_read.sum", 0) + r.get("dram__bytes_write.sum", 0)
         if "thread" in r["name"]:
-            cur = {"bytes": b, "ns": r.get("gpu__time_duration.sum", 0)}
+            cur = {"bytes": b, "ns": r.get("gpu__time_duration.sum", 0),
+                   "thread_bytes": b, "thread_ns": r.get("gpu__time_duration.sum", 0)}
             steps.append(cur)
         elif cur is not None:
             cur["bytes"] += b
@@ -45,7 +46,9 @@ if len(sys.argv) > 2 and sys.argv[1] == "--summarise":
     print(json.dumps({"pull_steps": len(steps), "dram_bytes_total": tot,
                       "dram_bytes_per_step": tot / max(len(steps), 1),
                       "largest_step_bytes": max(s["bytes"] for s in steps),
-                      "ncu_ns_total": sum(s["ns"] for s in steps)}))
+                      "ncu_ns_total": sum(s["ns"] for s in steps),
+                      "steps": [[int(s["bytes"]), int(s["ns"]), int(s["thread_bytes"]),
+                                 int(s["thread_ns"])] for s in steps]}))
     sys.exit(0)
 
 import bench  # noqa: E402
