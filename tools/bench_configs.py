@@ -101,6 +101,23 @@ def main():
             emit(config=2, primitive=name, graph="rmat26_ef16", reached_arcs=ar,
                  device_ms_mean=mean, device_ms_min=best, gteps=ar / (mean * 1e-3) / 1e9,
                  supersteps=int(r.stats.supersteps), edges_examined=int(r.stats.edges_examined))
+        # DOBFS over source 0 + 64 random non-isolated sources:
+        # per-source GTEPS and their harmonic mean, exact-cost and reference schedule
+        import bench
+        srcs = bench.pick_sources(off, 65)
+        for name, cfg in (("dobfs_exact_cost", exact), ("dobfs", MAXCFG)):
+            per = []
+            for s in srcs:
+                r = mg.dobfs(plan, mg.DobfsOptions(source=s), cfg)
+                ar = reached(r.labels, deg, mg.kInfLabel)
+                mean, _ = timeit(lambda: mg.dobfs(plan, mg.DobfsOptions(source=s), cfg,
+                                                 download=False).stats.device_ms, 3)
+                per.append((s, ar, mean))
+            g = [ar / (ms * 1e-3) / 1e9 for _, ar, ms in per]
+            emit(config=2, primitive=name + "_65_sources", graph="rmat26_ef16",
+                 sources="0 + 64 random non-isolated (bench.pick_sources seed 7)",
+                 hmean_gteps=len(g) / sum(1.0 / x for x in g), min_gteps=min(g), max_gteps=max(g),
+                 per_source=[[s, ar, round(ms, 4), round(x, 1)] for (s, ar, ms), x in zip(per, g)])
         del plan, off, deg
 
     if cfgs & {3, 5}:  # RMAT-24/16 (device hashed generator), weights U[1,64] seed+101

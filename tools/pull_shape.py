@@ -22,7 +22,8 @@ lab = r.labels
 deg = np.diff(off.astype(np.int64))
 front = first_pull  # frontier of superstep t = label t
 unv = np.nonzero((lab > front) & (deg > 0))[0]
-print(f"first pull at superstep {first_pull}: frontier {(lab == front).sum()}, unvisited {len(unv)}")
+print(f"first pull at superstep {first_pull}: frontier {(lab == front).sum()}, unvisited {len(unv)}, "
+      f"frontier degree sum {int(deg[lab == front].sum())}, unvisited degree sum {int(deg[unv].sum())}")
 isf = (lab == front)
 fh = np.empty(len(unv), np.int64)
 CH = 1 << 22
