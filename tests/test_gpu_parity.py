@@ -491,3 +491,54 @@ def test_dobfs_graph_loop_max_supersteps_and_isolated_source():
     r = mg.dobfs(plan, mg.DobfsOptions(source=iso), GRAPH_CFG)
     assert r.labels[iso] == 0 and int((r.labels != mg.kInfLabel).sum()) == 1
     assert r.stats.supersteps == 1
+
+
+def _first_hit_graph():
+    """source 0 -> hub 1 -> rows x whose first frontier neighbour (the hub) sits at
+    arc position k = 0..14, followed by 0/1/5/20 more arcs: the pull's record
+    arcs (0-1), its in-thread stage (arcs 2-9) and the cooperative stage (10+)"""
+    adj = [[1], [0]]
+    for k in range(15):
+        for t in (0, 1, 5, 20):
+            x = len(adj)
+            adj.append([])
+            adj[1].append(x)
+            fill = []
+            for _ in range(k):
+                f = len(adj)
+                adj.append([x])
+                fill.append(f)
+            tail = []
+            for _ in range(t):
+                f = len(adj)
+                adj.append([x])
+                tail.append(f)
+            adj[x] = fill + [1] + tail
+    off = np.zeros(len(adj) + 1, np.uint32)
+    off[1:] = np.cumsum([len(a) for a in adj])
+    col = np.array([v for a in adj for v in a], np.uint32)
+    return mg.Csr.from_csr(off, col)
+
+
+@pytest.mark.parametrize("n", [1, 2])
+@pytest.mark.parametrize("do_a", [1e-9, 0.01])
+def test_dobfs_pull_first_hit_positions(n, do_a):
+    """W (the first-hit scan count) and labels equal the reference's for first
+    hits at every arc position across the pull's three stages"""
+    g = _first_hit_graph()
+    off, col, _ = g.arrays()
+    plan, owner = plan_for(g, n, seed=5)
+    for exact in (False, True):
+        cfg = mg.EngineConfig(policy=mg.AllocPolicyKind.Maximum, fused=mg.FusedMode.On,
+                              dobfs_exact_cost=exact)
+        r = mg.dobfs(plan, mg.DobfsOptions(source=0, do_a=do_a, do_b=0.1, mark_preds=True), cfg)
+        assert np.array_equal(r.labels, seq.bfs_levels(off, col, 0))
+        x = np.nonzero(r.labels == 2)[0]
+        assert np.all(r.preds[x] == 1) and len(x) == 60
+        if do_a < 1e-6:
+            assert r.backward_edges > 0  # the rows were pulled
+        if ref.available():
+            rr = ref.RefPlan(ref.RefGraph.from_csr(off, col), owner, n).dobfs(0, do_a, 0.1)
+            assert list(r.direction_log) == list(rr.direction_log)
+            assert r.stats.edges_examined == rr.stats.edges_examined
+            assert r.stats.supersteps == rr.stats.supersteps
