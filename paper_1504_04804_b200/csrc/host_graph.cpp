@@ -2,6 +2,8 @@
 // See host_graph.hpp for the contract; reference lines cited per function.
 #include "host_graph.hpp"
 
+#include <immintrin.h>
+
 #include <algorithm>
 #include <numeric>
 #include <random>
@@ -447,6 +449,39 @@ __attribute__((target_clones("avx2", "default"))) void widen_labels_u8(const uin
     const uint32_t v = src[i];
     dst[i] = v == 255u ? kInvalid : v;
   }
+}
+
+// 4-bit levels (two per byte, 15 -> kInvalid) -> u32 labels [lo, hi)
+static inline uint32_t nib_at(const uint8_t* src, size_t i) {
+  const uint32_t v = (src[i >> 1] >> ((i & 1) * 4)) & 15u;
+  return v == 15u ? kInvalid : v;
+}
+
+__attribute__((target("avx2"))) static void widen_labels_u4_avx2(const uint8_t* src,
+                                                                  uint32_t* dst, size_t lo,
+                                                                  size_t hi) {
+  size_t i = lo;
+  for (; i < hi && (i & 31); ++i) dst[i] = nib_at(src, i);
+  const __m128i m4 = _mm_set1_epi8(0x0F);
+  const __m256i f = _mm256_set1_epi32(15);
+  for (; i + 32 <= hi; i += 32) {  // 16 bytes -> 32 labels
+    const __m128i b = _mm_loadu_si128(reinterpret_cast<const __m128i*>(src + (i >> 1)));
+    const __m128i l = _mm_and_si128(b, m4), h = _mm_and_si128(_mm_srli_epi16(b, 4), m4);
+    const __m128i p0 = _mm_unpacklo_epi8(l, h), p1 = _mm_unpackhi_epi8(l, h);
+    __m256i w[4] = {_mm256_cvtepu8_epi32(p0), _mm256_cvtepu8_epi32(_mm_srli_si128(p0, 8)),
+                    _mm256_cvtepu8_epi32(p1), _mm256_cvtepu8_epi32(_mm_srli_si128(p1, 8))};
+    for (int k = 0; k < 4; ++k) {
+      w[k] = _mm256_or_si256(w[k], _mm256_cmpeq_epi32(w[k], f));  // 15 -> 0xFFFFFFFF
+      _mm256_storeu_si256(reinterpret_cast<__m256i*>(dst + i + 8 * k), w[k]);
+    }
+  }
+  for (; i < hi; ++i) dst[i] = nib_at(src, i);
+}
+
+void widen_labels_u4(const uint8_t* src, uint32_t* dst, size_t lo, size_t hi) {
+  static const bool avx2 = __builtin_cpu_supports("avx2");
+  if (avx2) return widen_labels_u4_avx2(src, dst, lo, hi);
+  for (size_t i = lo; i < hi; ++i) dst[i] = nib_at(src, i);
 }
 
 }  // namespace mgb

@@ -80,6 +80,7 @@ HostPlan build_plan(const HostCsr& g, const std::vector<uint32_t>& owner, uint32
 
 // u8 levels (255 = unreached) -> u32 labels (split label download, plan.cu)
 void widen_labels_u8(const uint8_t* src, uint32_t* dst, size_t n);
+void widen_labels_u4(const uint8_t* src, uint32_t* dst, size_t lo, size_t hi);
 
 // FIFO-BFS (Cuthill-McKee order without degree sort) vertex order: perm[old] = new
 std::vector<uint32_t> bfs_locality_order(const uint32_t* off, const uint32_t* col, uint32_t nv);

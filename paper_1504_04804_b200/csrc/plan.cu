@@ -439,6 +439,16 @@ __global__ void narrow_labels_kernel(const uint32_t* __restrict__ lab, uint32_t 
   }
 }
 
+// two levels per byte (15 = unreached) when every level is below 15
+__global__ void narrow_labels_nib_kernel(const uint32_t* __restrict__ lab, uint32_t n,
+                                         uint8_t* out) {
+  const uint32_t np = (n + 1) / 2;
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < np; i += gridDim.x * blockDim.x) {
+    const uint32_t a = lab[2 * i], b = 2 * i + 1 < n ? lab[2 * i + 1] : kInfLabel;
+    out[i] = (uint8_t)((a == kInfLabel ? 15u : a) | ((b == kInfLabel ? 15u : b) << 4));
+  }
+}
+
 HostPool::HostPool(unsigned n) : n_(n ? n : 1) {
   for (unsigned t = 0; t < n_; ++t)
     threads_.emplace_back([this, t] {
@@ -508,9 +518,17 @@ void gather_labels_u32(Plan& P, const std::vector<const uint32_t*>& pw, uint32_t
                                                        ? 16
                                                        : std::thread::hardware_concurrency());
   const uint32_t* src = pw[w.p];
-  MGB_LAUNCH(narrow_labels_kernel, grid_for(nb, 256, kNumSMs * 8), 256, 0, w.stream, src + m, nb,
-             P.label_dev.ptr);
-  MGB_CUDA(cudaMemcpyAsync(P.label_stage, P.label_dev.ptr, nb, cudaMemcpyDeviceToHost, w.stream));
+  const char* ne = getenv("MG_D2H_NIBBLE");
+  const bool nib = max_label < 15 && !(ne && ne[0] == '0');  // 4-bit levels: half the bytes
+  const uint32_t nbytes = nib ? (nb + 1) / 2 : nb;
+  if (nib)
+    MGB_LAUNCH(narrow_labels_nib_kernel, grid_for(nbytes, 256, kNumSMs * 8), 256, 0, w.stream,
+               src + m, nb, P.label_dev.ptr);
+  else
+    MGB_LAUNCH(narrow_labels_kernel, grid_for(nb, 256, kNumSMs * 8), 256, 0, w.stream, src + m,
+               nb, P.label_dev.ptr);
+  MGB_CUDA(cudaMemcpyAsync(P.label_stage, P.label_dev.ptr, nbytes, cudaMemcpyDeviceToHost,
+                           w.stream));
   MGB_CUDA(cudaEventRecord(w.ev_k0, w.stream));
   if (m) MGB_CUDA(cudaMemcpyAsync(out, src, 4ull * m, cudaMemcpyDeviceToHost, w.stream));
   MGB_CUDA(cudaEventSynchronize(w.ev_k0));  // bytes landed: widen while the head streams in
@@ -518,7 +536,10 @@ void gather_labels_u32(Plan& P, const std::vector<const uint32_t*>& pw, uint32_t
   uint32_t* dst = out + m;
   P.pool->run([&](unsigned t, unsigned T) {
     const uint64_t lo = (uint64_t)nb * t / T, hi = (uint64_t)nb * (t + 1) / T;
-    widen_labels_u8(stage + lo, dst + lo, hi - lo);
+    if (nib)
+      widen_labels_u4(stage, dst, lo, hi);
+    else
+      widen_labels_u8(stage + lo, dst + lo, hi - lo);
   });
   MGB_CUDA(cudaStreamSynchronize(w.stream));
 }
