@@ -359,7 +359,10 @@ __global__ void select_nonisolated_kernel(const uint32_t* __restrict__ hosted, u
 constexpr int kPullK = 2;      // arcs held in the record
 constexpr int kPullGroup = 8;  // lanes per vertex in the long-row pass
 constexpr int kPV = 8;         // records per thread per iteration (loads in flight)
-constexpr uint32_t kPullQ = 256 * kPV + 1024;  // CTA queue capacity (> one chunk of 256 * kPV)
+#ifndef MG_PULL_QX
+#define MG_PULL_QX 0
+#endif
+constexpr uint32_t kPullQ = 256 * kPV + MG_PULL_QX;  // CTA queue capacity (>= one chunk of 256 * kPV)
 #ifndef MG_PULL_MID
 #define MG_PULL_MID 8
 #endif
@@ -368,6 +371,10 @@ constexpr uint32_t kPullQ = 256 * kPV + 1024;  // CTA queue capacity (> one chun
 // only rows longer than kPullStart go on to the cooperative stage
 constexpr int kPullMid = MG_PULL_MID;
 constexpr uint32_t kPullStart = kPullK + kPullMid;
+#ifndef MG_MID_PARTS
+#define MG_MID_PARTS 1
+#endif
+constexpr int kMidParts = MG_MID_PARTS;
 
 __global__ void pull_records_kernel(GraphView g, const uint32_t* __restrict__ ni, uint32_t n,
                                     uint4* rec) {
@@ -444,7 +451,13 @@ __device__ __forceinline__ void warp_set_bits_smem(uint32_t* bits, uint32_t* win
 // partition) the discovered vertices are only counted (and their degrees
 // summed into deg_out when non-null): the next superstep rebuilds the frontier
 // list from the visited bitmap only if it pushes.
-__global__ void __launch_bounds__(256, 4)
+#ifndef MG_PULL_OCC
+#define MG_PULL_OCC 4
+#endif
+// kEmit: discoveries listed (several partitions); otherwise only counted and
+// the found queue takes no shared memory
+template <bool kEmit>
+__global__ void __launch_bounds__(256, MG_PULL_OCC)
     dobfs_pull_thread_kernel(GraphView g, const uint4* __restrict__ rec,
                              const uint32_t* __restrict__ ul,
                              uint32_t nul, uint32_t* labels, uint32_t* preds, uint32_t* vis,
@@ -465,10 +478,11 @@ __global__ void __launch_bounds__(256, 4)
   uint32_t found_n = 0;
   // queues hold up to kPullQ entries and are flushed only when one could
   // overflow in the next chunk (one barrier per chunk otherwise)
-  __shared__ BlockQueue<kPullQ> q_found, q_keep, q_long;
+  __shared__ BlockQueue<kEmit ? kPullQ : 1> q_found;
+  __shared__ BlockQueue<kPullQ> q_keep, q_long;
   __shared__ uint32_t s_found;
   __shared__ uint32_t s_win[256 / 32][kBitSlots];  // visited-bit merge windows
-  __shared__ uint32_t s_mid[kPullMid > 0 ? 256 / 32 : 1][kPullMid > 0 ? 32 * kPV : 1];
+  __shared__ uint32_t s_mid[kPullMid > 0 ? 256 / 32 : 1][kPullMid > 0 ? 32 * kPV / kMidParts : 1];
   for (uint32_t i = threadIdx.x; i < 8 * kBitSlots; i += blockDim.x) (&s_win[0][0])[i] = 0u;
   q_found.reset();
   q_keep.reset();
@@ -516,7 +530,7 @@ __global__ void __launch_bounds__(256, 4)
       warp_set_bits_smem(vis, s_win[threadIdx.x >> 5], found[j], v);
     }
 
-    if (emit_found) warp_queue_append<kPV>(q_found, found, vv);
+    if constexpr (kEmit) warp_queue_append<kPV>(q_found, found, vv);
     warp_queue_append<kPV>(q_keep, keep, pos);
     if constexpr (kPullMid == 0) {
       warp_queue_append<kPV>(q_long, lng, pos);
@@ -524,11 +538,15 @@ __global__ void __launch_bounds__(256, 4)
       // stage 1b: the warp compacts its unsettled rows and spreads them over
       // all 32 lanes; each lane tests arcs [kPullK, kPullStart) of one row
       // with independent loads, first hit in arc order wins (exact W)
+      // (in kMidParts passes over the lane's records: a smaller shared list)
       uint32_t* lst = s_mid[threadIdx.x >> 5];
       const unsigned lt = (1u << lane_id()) - 1u;
+#pragma unroll
+      for (int part = 0; part < kMidParts; ++part) {
       uint32_t cnt = 0;
 #pragma unroll
-      for (int j = 0; j < kPV; ++j) {
+      for (int jj = 0; jj < kPV / kMidParts; ++jj) {
+        const int j = part * (kPV / kMidParts) + jj;
         const unsigned m = __ballot_sync(0xffffffffu, lng[j]);
         if (lng[j]) lst[cnt + __popc(m & lt)] = pos[j];
         cnt += __popc(m);
@@ -574,11 +592,12 @@ __global__ void __launch_bounds__(256, 4)
           scanned += e - kPullK;
         }
         warp_set_bits_smem(vis, s_win[threadIdx.x >> 5], fnd, v);
-        if (emit_found) warp_queue_append<1>(q_found, &fnd, &v);
+        if constexpr (kEmit) warp_queue_append<1>(q_found, &fnd, &v);
         warp_queue_append<1>(q_keep, &kp, &p);
         warp_queue_append<1>(q_long, &lg, &p);
       }
       __syncwarp();
+      }
     }
     __syncthreads();
     const bool last = base + gridDim.x * chunk >= nul;
@@ -598,7 +617,7 @@ __global__ void __launch_bounds__(256, 4)
       __syncthreads();
     }
   }
-  if (!emit_found) {
+  if constexpr (!kEmit) {
     unsigned m = __reduce_add_sync(0xffffffffu, found_n);
     if (lane_id() == 0 && m) atomicAdd(&s_found, m);
     __syncthreads();
@@ -1043,7 +1062,8 @@ struct DobfsPrim : PrimBase {
     unsigned long long* deg_out =
         reports_deg && !c.want_deg && c.P->n == 1 ? &c.ctr()->next_deg : nullptr;
     if (nul) {
-      MGB_LAUNCH(dobfs_pull_thread_kernel, grid_for(nul, 256 * kPV, kNumSMs * 4), 256, 0,
+      auto* kern = emit ? dobfs_pull_thread_kernel<true> : dobfs_pull_thread_kernel<false>;
+      MGB_LAUNCH(kern, grid_for(nul, 256 * kPV, kNumSMs * MG_PULL_OCC), 256, 0,
                  w.stream, w.graph(), w.pull_rec.ptr, ul, nul, w.su32[0].ptr, w.su32[1].ptr, w.su32[2].ptr,
                  w.su32[3].ptr, next_label, mark_preds ? 1 : 0, c.owner_view(), emit ? 1 : 0,
                  w.output.ptr, w.ul_buf[dst].ptr, ulcnt, w.ul_buf[2].ptr, cnts + 1, c.ctr(),
@@ -1322,7 +1342,7 @@ class DobfsGraphRunner {
     MGB_LAUNCH(frontier_diff_kernel, grid_for(nw, 256, kNumSMs * 8), 256, 0, s, w.su32[2].ptr,
                w.aux[4].ptr, w.su32[3].ptr, (uint32_t)nw, cnts, nullptr, 0ull,
                (const DobfsLoop*)st, &ctr->edges);
-    MGB_LAUNCH(dobfs_pull_thread_kernel, kNumSMs * 4, 256, 0, s, gv, w.pull_rec.ptr, nullptr, 0u,
+    MGB_LAUNCH(dobfs_pull_thread_kernel<false>, kNumSMs * MG_PULL_OCC, 256, 0, s, gv, w.pull_rec.ptr, nullptr, 0u,
                w.su32[0].ptr, w.su32[1].ptr, w.su32[2].ptr, w.su32[3].ptr, 0u, mp, ow, 0,
                w.loop_front[1].ptr, nullptr, &ctr->misc, w.ul_buf[2].ptr, cnts + 1, ctr,
                (unsigned long long*)nullptr, &ctr->next_deg, dyn);
