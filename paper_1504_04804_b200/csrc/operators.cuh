@@ -29,8 +29,14 @@ constexpr int kLbBlock = 256;     // degree pass: one vertex per thread
 constexpr int kExpBlock = 256;    // expansion CTA
 constexpr int kItems = 8;         // arcs per thread per batch (lane-strided)
 constexpr uint32_t kTile = 8192;  // arcs per tile for large advances
-constexpr int kWarpQ = 384;       // warp-private output staging entries
-constexpr int kStage = 1536;      // max tile vertices staged in shared memory
+#ifndef MG_WARPQ
+#define MG_WARPQ 384
+#endif
+#ifndef MG_KSTAGE
+#define MG_KSTAGE 1536
+#endif
+constexpr int kWarpQ = MG_WARPQ;   // warp-private output staging entries
+constexpr int kStage = MG_KSTAGE;  // max tile vertices staged in shared memory
 
 // lb 1: row starts + CTA-local exclusive prefix of degrees
 // (n_in_ptr: the frontier length read on the device — graph-captured
