@@ -358,7 +358,10 @@ __global__ void select_nonisolated_kernel(const uint32_t* __restrict__ hosted, u
 // positions; the first pull of a run walks all records without a list.
 constexpr int kPullK = 2;      // arcs held in the record
 constexpr int kPullGroup = 8;  // lanes per vertex in the long-row pass
-constexpr int kPV = 8;         // records per thread per iteration (loads in flight)
+#ifndef MG_PV
+#define MG_PV 8
+#endif
+constexpr int kPV = MG_PV;     // records per thread per iteration (loads in flight)
 #ifndef MG_PULL_QX
 #define MG_PULL_QX 0
 #endif
