@@ -11,8 +11,15 @@ CUDA-event time of the superstep loop including per-run init (the reference's
 wall_ms region, engine.hpp:951-964).  `e2e` repeats the steps through the same
 public call with the labels copied back into pinned host memory every step.
 
+--gpus N > 1 without torchrun re-launches itself under torch.distributed.run
+with N ranks (one process per GPU, partition_random(|V|, N, 7)); with
+MG_BENCH_DEVICE=0 every rank shares GPU 0 (the path, not its speed).
+
 --impl reference times the reference's own CPU engine (oracle/_ref, compiled
-from the reference sources) on the same graph and sources.
+from the reference sources) on the same graph and sources.  That process never
+loads the product library: its graph comes from the oracle's own generator
+(oracle/gen_oracle.cpp), bit-identical to the device generator
+(tests/test_oracle.py, tests/test_gpu_parity.py).
 """
 import argparse
 import json
@@ -29,6 +36,8 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 HBM_FALLBACK = 6650.0
+NVLINK_GBS = 900.0  # NVLink 5, per direction per GPU (nominal)
+METRIC = "DOBFS GTEPS (A_r / t) on RMAT"
 
 
 def peaks():
@@ -49,6 +58,19 @@ def ncu_traffic(kind):
         return d.get(f"dobfs_{kind}_bytes_per_launch"), d.get(f"dobfs_{kind}_launch")
     except Exception:
         return None, None
+
+
+def host_info():
+    model = "unknown"
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    model = line.split(":", 1)[1].strip()
+                    break
+    except Exception:
+        pass
+    return {"cpu_model": model, "nproc": os.cpu_count()}
 
 
 class Clocks:
@@ -99,6 +121,25 @@ def pick_sources(off, count, seed=7):
     return [0] + [int(x) for x in extra]
 
 
+def reached_arcs(labels, deg):
+    return int(deg[labels != 0xFFFFFFFF].sum())
+
+
+def workload_config(args, n, sources, nv, ne):
+    """the config dict both arms print (identical for the same arguments)"""
+    return {
+        "workload": f"dobfs_rmat{args.scale}_ef{args.edge_factor}",
+        "scale": args.scale, "edge_factor": args.edge_factor, "seed": args.seed,
+        "generator": f"counter-based R-MAT (a,b,c,d)=(.57,.19,.19,.05) seed {args.seed},"
+                     " symmetrized + deduplicated",
+        "num_vertices": int(nv), "num_arcs": int(ne),
+        "partitions": n,
+        "partitioner": "partition_random(|V|, N, 7)" if n > 1 else "single partition",
+        "sources": sources, "do_a": 0.01, "do_b": 0.1,
+        "l2": "inputs larger than L2 (CSR %.1f GB vs 126 MB L2)" % (4 * (nv + ne) / 1e9),
+    }
+
+
 def allreduce(x, op):
     """scalar all-reduce over ranks (device tensor under NCCL, host under gloo)"""
     import torch
@@ -107,10 +148,6 @@ def allreduce(x, op):
     t = torch.tensor([x], dtype=torch.float64, device=dev)
     dist.all_reduce(t, op=dist.ReduceOp.MAX if op == "max" else dist.ReduceOp.SUM)
     return float(t.item())
-
-
-def reached_arcs(labels, deg):
-    return int(deg[labels != 0xFFFFFFFF].sum())
 
 
 def dist_env():
@@ -123,26 +160,15 @@ def dist_env():
     return rank, world, local
 
 
-def cpu_reference(graph_arrays, sources, arcs, max_s, label):
-    """time the reference engine (oracle/_ref) on the same graph; n = 1 partition"""
-    from oracle import ref
-    off, col, _ = graph_arrays
-    t0 = time.time()
-    g = ref.RefGraph.from_csr(off, col)
-    plan = ref.RefPlan(g, np.zeros(len(off) - 1, np.uint32), 1)
-    prep = time.time() - t0
-    done, ms, a = [], 0.0, 0
-    t1 = time.time()
-    for s in sources:
-        r = plan.dobfs(s)
-        ms += r.stats.wall_ms
-        a += arcs[s]
-        done.append(s)
-        if time.time() - t1 > max_s:
-            break
-    return {"value": a / (ms * 1e-3) / 1e9, "unit": "GTEPS", "cores": 1, "kind": "reference",
-            "sample": f"{label}: reference dobfs (n=1 partition, 1 thread) from sources {done}, "
-                      f"{ms:.0f} ms engine wall_ms (plan build {prep:.1f} s excluded)"}
+def spawn(argv, n):
+    """--gpus N without a launcher: run this script under torch.distributed.run"""
+    import socket
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__)]
+    return subprocess.call(cmd + argv)
 
 
 def main():
@@ -159,7 +185,15 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
 
+    if args.impl == "ours" and args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        return spawn(sys.argv[1:], args.gpus)
     rank, world, local = dist_env()
+    if args.impl == "reference":
+        # CPU reference: rank 0 alone runs and prints; other ranks exit at once
+        return run_reference(args, rank, max(world, args.gpus)) if rank == 0 else 0
+    if world != args.gpus:
+        print(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}", file=sys.stderr)
+        return 2
     if world > 1:
         import torch
         import torch.distributed as dist
@@ -168,215 +202,12 @@ def main():
         # rank is pinned to one GPU (NCCL refuses duplicate devices)
         backend = "gloo" if "MG_BENCH_DEVICE" in os.environ else "nccl"
         dist.init_process_group(backend, init_method="env://")
-    workload = f"dobfs_rmat{args.scale}_ef{args.edge_factor}"
-    if args.impl == "reference":
-        return run_reference(args, rank, world, workload)
-    return run_ours(args, rank, world, local, workload)
+    return run_ours(args, rank, world, local)
 
 
-def build_plan(args, n, owner=None, devices=None):
-    import paper_1504_04804_b200 as mg
-    t0 = time.time()
-    plan = mg.PartitionPlan.rmat_device(args.scale, args.edge_factor, args.seed, owner=owner, n=n,
-                                        devices=devices)
-    return plan, time.time() - t0
-
-
-def run_ours(args, rank, world, local, workload):
-    import torch
-
-    import paper_1504_04804_b200 as mg
-    torch.cuda.set_device(local)
-    hbm, hbm_kind = peaks()
-    # one partition per GPU: N = 1 is the single-partition plan; N > 1 is one
-    # process per GPU, partition_random(|V|, N, 7) (partition.cpp:31-40), ranks
-    # exchanging records through CUDA-IPC-mapped inboxes over NVLink
-    if world > 1:
-        import uuid
-        owner = mg.partition_random(1 << args.scale, world, 7)
-        key = [uuid.uuid4().hex if rank == 0 else None]
-        torch.distributed.broadcast_object_list(key, src=0)
-        t0 = time.time()
-        plan = mg.PartitionPlan.rmat_device_multiprocess(args.scale, args.edge_factor, args.seed,
-                                                         owner, world, rank, local, key[0])
-        prep_s = time.time() - t0
-        hosted = owner == rank
-    else:
-        plan, prep_s = build_plan(args, 1, devices=[local])
-        hosted = None
-    g = plan.download_graph()
-    off, col, _ = g.arrays()
-    del g
-    deg = np.diff(off.astype(np.int64))
-    sources = pick_sources(off, args.num_sources)
-    cfg = mg.EngineConfig(policy=mg.AllocPolicyKind.Maximum, fused=mg.FusedMode.On)
-    opt = lambda s: mg.DobfsOptions(source=s)  # noqa: E731
-    # warm-up: every source once with labels downloaded (A_r per source), >= W runs
-    arcs = {}
-    for i in range(max(args.warmup, len(sources))):
-        s = sources[i % len(sources)]
-        r = mg.dobfs(plan, opt(s), cfg)
-        if s not in arcs:
-            lab = r.labels if hosted is None else np.where(hosted, r.labels, 0xFFFFFFFF)
-            a = reached_arcs(lab, deg)
-            if world > 1:  # each rank holds its hosted labels only
-                a = int(allreduce(a, "sum"))
-            arcs[s] = a
-    steps = [sources[i % len(sources)] for i in range(args.steps)]
-    total_arcs = sum(arcs[s] for s in steps)
-
-    def timed(do_a, do_b, cfg=cfg):
-        """K device-resident steps; CUDA-event times from the library stream"""
-        mg.lib().mg_plan_set_profiling(plan._h, 1)
-        for s in sources[:2]:  # warm this parameter set
-            dobfs_stats(mg, plan, s, cfg, do_a, do_b)
-        if world > 1:
-            torch.distributed.barrier()
-        torch.cuda.synchronize()
-        acc = {"dev_ms": 0.0, "pull": [0.0, 0.0, 0], "push": [0.0, 0.0, 0], "xms": 0.0,
-               "xbytes": 0}
-        l0 = mg.kernel_launch_count()
-        clocks = Clocks(local)
-        w0 = time.perf_counter()
-        for s in steps:
-            st = dobfs_stats(mg, plan, s, cfg, do_a, do_b)
-            acc["dev_ms"] += st.device_ms
-            acc["xms"] += st.exchange_ms  # pack + publish kernels (records into peer HBM)
-            acc["xbytes"] += st.exchange_bytes
-            for key, ms, b, n in (("pull", st.kernel_ms, st.kernel_bytes, st.kernel_launches),
-                                  ("push", st.kernel2_ms, st.kernel2_bytes,
-                                   st.kernel2_launches)):
-                acc[key][0] += ms
-                acc[key][1] += b
-                acc[key][2] += n
-        torch.cuda.synchronize()
-        acc["wall"] = time.perf_counter() - w0
-        acc["clocks"] = clocks.stop()
-        acc["launches"] = mg.kernel_launch_count() - l0
-        mg.lib().mg_plan_set_profiling(plan._h, 0)
-        dev = acc["dev_ms"]
-        if world > 1:
-            dev = allreduce(dev, "max")
-        acc["dev_max_ms"] = dev
-        acc["value"] = total_arcs / (dev * 1e-3) / 1e9
-        # end to end: same calls, labels copied into pinned host memory each step
-        e2e_t = 0.0
-        for s in steps:
-            t0 = time.perf_counter()
-            e2e_call(mg, plan, s, cfg, labels, do_a, do_b)
-            e2e_t += time.perf_counter() - t0
-        if world > 1:
-            e2e_t = allreduce(e2e_t, "max")
-        acc["e2e"] = total_arcs / e2e_t / 1e9
-        return acc
-
-    host = torch.empty(plan.num_global_vertices, dtype=torch.int32, pin_memory=True)
-    labels = host.numpy().view(np.uint32)
-    # headline: the reference's direction rule and defaults (primitives.hpp:69-70);
-    # on one partition a logically-forward superstep whose exact edge count
-    # dwarfs the unvisited list runs on the pull kernel (mg_config.dobfs_exact_cost).
-    # Labels, direction log, S and W are the reference's (tests/test_gpu_parity.py).
-    exact_cfg = mg.EngineConfig(policy=mg.AllocPolicyKind.Maximum, fused=mg.FusedMode.On,
-                                dobfs_exact_cost=True)
-    main = timed(0.01, 0.1, exact_cfg)
-    # the same rule executed physically as the reference schedules it
-    refsched = timed(0.01, 0.1)
-    tuned = timed(0.001, 0.1)      # do_a tuned for RMAT (PAPER.md:744-749: per graph type)
-    dev_ms, value, e2e, clk, launches, wall = (main["dev_max_ms"], main["value"], main["e2e"],
-                                              main["clocks"], main["launches"], main["wall"])
-    kind = "push" if main["push"][0] >= main["pull"][0] else "pull"
-    prof = {"ms": main[kind][0], "bytes": main[kind][1], "launches": main[kind][2],
-            "dev_ms": main["dev_ms"]}
-    other = "pull" if kind == "push" else "push"
-
-    if rank != 0:
-        return 0
-    cpu = None
-    if not args.no_cpu_baseline and world == 1:
-        try:
-            cpu = cpu_reference((off, col, None), sources, arcs, args.cpu_seconds, workload)
-        except Exception as ex:  # the baseline is reported, never required
-            cpu = {"value": None, "unit": "GTEPS", "cores": 1, "kind": "reference",
-                   "sample": f"unavailable: {ex}"}
-    achieved = prof["bytes"] / (prof["ms"] * 1e-3) / 1e9 if prof["ms"] else None
-    traffic, traffic_src = ncu_traffic(kind)
-    line = {
-        "metric": "DOBFS GTEPS (A_r / t) on RMAT",
-        "value": round(value, 3),
-        "unit": "GTEPS",
-        "n_gpus": world,
-        "steps": args.steps,
-        "warmup": args.warmup,
-        "ms_per_step": round(dev_ms / args.steps, 4),
-        "higher_is_better": True,
-        "scaling": "strong",
-        "vs_baseline": None,
-        "dtype": "u32",
-        "data": "synthetic (hashed R-MAT generated on the GPU)",
-        "config": {
-            "workload": workload, "scale": args.scale, "edge_factor": args.edge_factor,
-            "generator": f"counter-based R-MAT (a,b,c,d)=(.57,.19,.19,.05) seed {args.seed},"
-                         " symmetrized + deduplicated",
-            "num_vertices": plan.num_global_vertices, "num_arcs": plan.num_global_edges,
-            "partitions_per_gpu": 1,
-            "parallelism": f"partitioned x{world} (random, seed 7), CUDA IPC P2P exchange"
-            if world > 1 else "single partition",
-            "sources": sources, "mean_reached_arcs": total_arcs // len(steps),
-            "policy": "max + fused", "do_a": 0.01, "do_b": 0.1,
-            "physical_direction": "exact cost (pull when sum deg(Q) > 4 |unvisited|, "
-                                  "summed over all partitions)",
-            "l2": "inputs larger than L2 (CSR %.1f GB vs 126 MB L2)" % (
-                (4 * (plan.num_global_vertices + plan.num_global_edges)) / 1e9),
-            "graph_prep_s": round(prep_s, 2),
-            "host_wall_s": round(wall, 4),
-            "timing": "CUDA events on the library stream around init + superstep loop, "
-                      "summed over the K steps (max over ranks)",
-        },
-        "e2e": {"value": round(e2e, 3), "unit": "GTEPS", "h2d_bytes_per_step": 4,
-                "d2h_bytes_per_step": 4 * plan.num_global_vertices},
-        "roofline": {"bound": "hbm",
-                     "kernel": "lb_expand (push advance)" if kind == "push"
-                     else "dobfs_pull (thread + group stages)",
-                     "achieved": round(achieved, 1) if achieved else None, "peak": hbm,
-                     "peak_kind": hbm_kind, "unit": "GB/s",
-                     "frac": round(achieved / hbm, 4) if achieved else None,
-                     "traffic": traffic, "traffic_source": traffic_src,
-                     "algorithmic_bytes_per_launch": prof["bytes"] / max(prof["launches"], 1),
-                     "avg_launch_ms": prof["ms"] / max(prof["launches"], 1),
-                     "share_of_step": round(prof["ms"] / prof["dev_ms"], 4) if prof["dev_ms"]
-                     else None,
-                     "other_kernel": {"kernel": other,
-                                      "achieved": round(main[other][1] / (main[other][0] * 1e-3)
-                                                        / 1e9, 1) if main[other][0] else None,
-                                      "share_of_step": round(main[other][0] / main["dev_ms"], 4)}},
-        "tuned": {"do_a": 0.001, "do_b": 0.1, "value": round(tuned["value"], 3),
-                  "ms_per_step": round(tuned["dev_max_ms"] / args.steps, 4),
-                  "e2e": round(tuned["e2e"], 3),
-                  "note": "same graph and sources; the reference with the same do_a takes the "
-                          "same direction decisions (direction log checked in tests)"},
-        "reference_schedule": {
-            "do_a": 0.01, "do_b": 0.1, "value": round(refsched["value"], 3),
-            "ms_per_step": round(refsched["dev_max_ms"] / args.steps, 4),
-            "e2e": round(refsched["e2e"], 3),
-            "note": "dobfs_exact_cost off: every superstep runs in the direction the reference "
-                    "rule picks (push advance for forward steps)"},
-        "exchange": None if world == 1 else {
-            "bytes_per_step": main["xbytes"] / args.steps,
-            "pack_ms_per_step": round(main["xms"] / args.steps, 4),
-            "achieved": round(main["xbytes"] / (main["xms"] * 1e-3) / 1e9, 1) if main["xms"] else None,
-            "peak": 900.0, "unit": "GB/s",
-            "peak_kind": "NVLink 5 nominal per direction per GPU",
-            "note": "rank 0: record bytes its pack kernels stored into peer inboxes / their "
-                    "CUDA-event time (with every rank on one GPU this is HBM, not NVLink)"},
-        "cpu_baseline": cpu,
-        "clocks": clk,
-        "gpu_launches": launches,
-    }
-    print(json.dumps(line))
-    return 0
-
-
+# ------------------------------------------------------------------------------ our arm
 def e2e_call(mg, plan, s, cfg, labels, do_a=0.01, do_b=0.1):
+    """one DOBFS through the C-ABI (mg_dobfs); labels=None keeps them on the device"""
     import ctypes as C
 
     from paper_1504_04804_b200 import abi
@@ -392,35 +223,321 @@ def e2e_call(mg, plan, s, cfg, labels, do_a=0.01, do_b=0.1):
     return st
 
 
-def dobfs_stats(mg, plan, s, cfg, do_a=0.01, do_b=0.1):
-    """one device-resident DOBFS through the C-ABI (no result download)"""
-    return e2e_call(mg, plan, s, cfg, None, do_a, do_b)
+def d2h_bytes(mg, plan):
+    import ctypes as C
+    b = C.c_uint64()
+    mg.lib().mg_plan_last_d2h_bytes(plan._h, C.byref(b))
+    return b.value
 
 
-def run_reference(args, rank, world, workload):
+def run_ours(args, rank, world, local):
+    import torch
+
+    import paper_1504_04804_b200 as mg
+    torch.cuda.set_device(local)
+    hbm, hbm_kind = peaks()
+    # one partition per GPU: N = 1 is the single-partition plan; N > 1 is one
+    # process per GPU, partition_random(|V|, N, 7) (partition.cpp:31-40), ranks
+    # exchanging through CUDA-IPC-mapped inboxes over NVLink
+    t0 = time.time()
+    if world > 1:
+        import uuid
+        owner = mg.partition_random(1 << args.scale, world, 7)
+        key = [uuid.uuid4().hex if rank == 0 else None]
+        torch.distributed.broadcast_object_list(key, src=0)
+        plan = mg.PartitionPlan.rmat_device_multiprocess(args.scale, args.edge_factor, args.seed,
+                                                         owner, world, rank, local, key[0])
+        hosted = owner == rank
+    else:
+        plan = mg.PartitionPlan.rmat_device(args.scale, args.edge_factor, args.seed,
+                                            devices=[local])
+        hosted = None
+    torch.cuda.synchronize()
+    prep_s = time.time() - t0
+    g = plan.download_graph()
+    off, col, _ = g.arrays()
+    del g
+    deg = np.diff(off.astype(np.int64))
+    sources = pick_sources(off, args.num_sources)
+    base = dict(policy=mg.AllocPolicyKind.Maximum, fused=mg.FusedMode.On)
+    exact_cfg = mg.EngineConfig(dobfs_exact_cost=True, **base)
+    ref_cfg = mg.EngineConfig(**base)
+    # plan-lifetime precomputation (non-isolated list + its host sort, pull
+    # records, CUDA-graph capture): paid by the first call on a plan, outside
+    # `value`; measured here as first call minus a warm call of the same source
+    t1 = time.perf_counter()
+    e2e_call(mg, plan, sources[0], exact_cfg, None)
+    first = time.perf_counter() - t1
+    t1 = time.perf_counter()
+    e2e_call(mg, plan, sources[0], exact_cfg, None)
+    precompute_s = max(first - (time.perf_counter() - t1), 0.0)
+    # warm-up: every source once with labels downloaded (A_r per source), >= W runs
+    arcs = {}
+    for i in range(max(args.warmup, len(sources))):
+        s = sources[i % len(sources)]
+        r = mg.dobfs(plan, mg.DobfsOptions(source=s), exact_cfg)
+        if s not in arcs:
+            lab = r.labels if hosted is None else np.where(hosted, r.labels, 0xFFFFFFFF)
+            a = reached_arcs(lab, deg)
+            if world > 1:  # each rank holds its hosted labels only
+                a = int(allreduce(a, "sum"))
+            arcs[s] = a
+    steps = [sources[i % len(sources)] for i in range(args.steps)]
+    total_arcs = sum(arcs[s] for s in steps)
+    host = torch.empty(plan.num_global_vertices, dtype=torch.int32, pin_memory=True)
+    labels = host.numpy().view(np.uint32)
+
+    def barrier():
+        if world > 1:
+            torch.distributed.barrier()
+        torch.cuda.synchronize()
+
+    def timed(do_a, do_b, cfg):
+        """K device-resident steps, profiling off: the library's CUDA-event time of
+        every run (init + superstep loop), summed; then the same K steps through the
+        public call with the labels downloaded (e2e)"""
+        for s in sources[:2]:  # warm this parameter set
+            e2e_call(mg, plan, s, cfg, None, do_a, do_b)
+        barrier()
+        acc = {"dev_ms": 0.0, "xms": 0.0, "xbytes": 0, "device_loop": 0}
+        l0 = mg.kernel_launch_count()
+        clocks = Clocks(local)
+        w0 = time.perf_counter()
+        for s in steps:
+            st = e2e_call(mg, plan, s, cfg, None, do_a, do_b)
+            acc["dev_ms"] += st.device_ms
+            acc["xms"] += st.exchange_ms  # pack + publish kernels (records into peer HBM)
+            acc["xbytes"] += st.exchange_bytes
+            acc["device_loop"] += st.device_loop
+        barrier()
+        acc["wall"] = time.perf_counter() - w0
+        acc["clocks"] = clocks.stop()
+        acc["launches"] = mg.kernel_launch_count() - l0
+        acc["dev_max_ms"] = allreduce(acc["dev_ms"], "max") if world > 1 else acc["dev_ms"]
+        acc["value"] = total_arcs / (acc["dev_max_ms"] * 1e-3) / 1e9
+        # end to end: same calls, labels copied into pinned host memory each step
+        barrier()
+        e2e_t, d2h = 0.0, 0
+        for s in steps:
+            t = time.perf_counter()
+            e2e_call(mg, plan, s, cfg, labels, do_a, do_b)
+            e2e_t += time.perf_counter() - t
+            d2h += d2h_bytes(mg, plan)
+        if world > 1:
+            e2e_t = allreduce(e2e_t, "max")
+        acc["e2e"] = total_arcs / e2e_t / 1e9
+        acc["d2h_per_step"] = d2h // len(steps)
+        return acc
+
+    def profiled(do_a, do_b, cfg):
+        """the same K steps with per-kernel CUDA events on the library stream
+        (host-driven loop): the roofline of the dominant kernel classes"""
+        mg.lib().mg_plan_set_profiling(plan._h, 1)
+        e2e_call(mg, plan, sources[0], cfg, None, do_a, do_b)
+        barrier()
+        acc = {"pull": [0.0, 0.0, 0], "push": [0.0, 0.0, 0], "dev_ms": 0.0}
+        for s in steps:
+            st = e2e_call(mg, plan, s, cfg, None, do_a, do_b)
+            acc["dev_ms"] += st.device_ms
+            for key, ms, b, n in (("pull", st.kernel_ms, st.kernel_bytes, st.kernel_launches),
+                                  ("push", st.kernel2_ms, st.kernel2_bytes,
+                                   st.kernel2_launches)):
+                acc[key][0] += ms
+                acc[key][1] += b
+                acc[key][2] += n
+        barrier()
+        mg.lib().mg_plan_set_profiling(plan._h, 0)
+        return acc
+
+    # headline: the reference's direction rule and defaults (primitives.hpp:69-70);
+    # a logically-forward superstep whose exact edge count dwarfs the unvisited
+    # list runs on the pull kernels (mg_config.dobfs_exact_cost).  Labels,
+    # direction log, S and W are the reference's (tests/test_gpu_parity.py).
+    main = timed(0.01, 0.1, exact_cfg)
+    prof = profiled(0.01, 0.1, exact_cfg)
+    # the same rule executed physically as the reference schedules it
+    refsched = timed(0.01, 0.1, ref_cfg)
+    tuned = timed(0.001, 0.1, exact_cfg)  # do_a tuned for RMAT (PAPER.md:744-749)
+    kind = "push" if prof["push"][0] >= prof["pull"][0] else "pull"
+    other = "pull" if kind == "push" else "push"
+    k_ms, k_bytes, k_n = prof[kind]
+
     if rank != 0:
         return 0
+    cpu = None
+    if not args.no_cpu_baseline and world == 1:
+        try:
+            cpu = cpu_reference((off, col), sources, arcs, args.cpu_seconds)
+        except Exception as ex:  # the baseline is reported, never required
+            cpu = {"value": None, "unit": "GTEPS", "cores": 1, "kind": "reference",
+                   "sample": f"unavailable: {ex}"}
+    achieved = k_bytes / (k_ms * 1e-3) / 1e9 if k_ms else None
+    traffic, traffic_src = ncu_traffic(kind)
+    hbm_roof = {
+        "bound": "hbm",
+        "kernel": "lb_expand (push advance)" if kind == "push"
+        else "dobfs_pull (thread + group stages)",
+        "achieved": round(achieved, 1) if achieved else None, "peak": hbm,
+        "peak_kind": hbm_kind, "unit": "GB/s",
+        "frac": round(achieved / hbm, 4) if achieved else None,
+        "traffic": traffic, "traffic_source": traffic_src,
+        "algorithmic_bytes_per_launch": k_bytes / max(k_n, 1),
+        "avg_launch_ms": k_ms / max(k_n, 1),
+        "share_of_step": round(k_ms / prof["dev_ms"], 4) if prof["dev_ms"] else None,
+        "timing": "CUDA events around each launch pair on the library stream (profiled pass, "
+                  "host-driven loop)",
+        "other_kernel": {"kernel": other,
+                         "achieved": round(prof[other][1] / (prof[other][0] * 1e-3) / 1e9, 1)
+                         if prof[other][0] else None,
+                         "share_of_step": round(prof[other][0] / prof["dev_ms"], 4)
+                         if prof["dev_ms"] else None}}
+    xchg = None
+    if world > 1:
+        xa = main["xbytes"] / (main["xms"] * 1e-3) / 1e9 if main["xms"] else None
+        xchg = {"bound": "nvlink", "kernel": "dobfs exchange pack + publish (P2P stores into "
+                                             "peer inboxes)",
+                "achieved": round(xa, 1) if xa else None, "peak": NVLINK_GBS,
+                "peak_kind": "NVLink 5 nominal per direction per GPU", "unit": "GB/s",
+                "frac": round(xa / NVLINK_GBS, 4) if xa else None, "traffic": None,
+                "bytes_per_step": main["xbytes"] / args.steps,
+                "ms_per_step": round(main["xms"] / args.steps, 4),
+                "share_of_step": round(main["xms"] / main["dev_ms"], 4) if main["dev_ms"] else None,
+                "note": "rank 0: bytes its pack kernels stored into peer inboxes / their "
+                        "CUDA-event time" + (" (every rank on one GPU: HBM, not NVLink)"
+                                             if "MG_BENCH_DEVICE" in os.environ else "")}
+    roofline = dict(xchg, hbm_kernel=hbm_roof) if xchg else hbm_roof
+    dev_ms = main["dev_max_ms"]
+    loop = "device (CUDA-graph loop)" if main["device_loop"] == len(steps) else \
+        "host-driven enactor loop" if main["device_loop"] == 0 else "mixed"
+    line = {
+        "metric": METRIC,
+        "value": round(main["value"], 3),
+        "unit": "GTEPS",
+        "n_gpus": world,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "ms_per_step": round(dev_ms / args.steps, 4),
+        "higher_is_better": True,
+        "scaling": "strong",
+        "vs_baseline": None,
+        "dtype": "u32",
+        "data": "synthetic (hashed R-MAT generated on the GPU)",
+        "config": workload_config(args, world, sources, plan.num_global_vertices,
+                                  plan.num_global_edges),
+        "run": {
+            "policy": "max + fused",
+            "physical_direction": "exact cost (pull when sum deg(Q) > 4 |unvisited|, "
+                                  "summed over all partitions)",
+            "loop": loop,
+            "mean_reached_arcs": total_arcs // len(steps),
+            "graph_prep_s": round(prep_s, 2),
+            "plan_precompute_s": round(precompute_s, 3),
+            "precompute_note": "first call on a plan builds the non-isolated vertex list "
+                               "(device select + host sort), the 16-byte pull records and, "
+                               "under 2^30 arcs, the CUDA-graph loop; excluded from value",
+            "host_wall_s": round(main["wall"], 4),
+            "timing": "CUDA events on the library stream around init + superstep loop, "
+                      "summed over the K steps (max over ranks), profiling off",
+        },
+        "e2e": {"value": round(main["e2e"], 3), "unit": "GTEPS", "h2d_bytes_per_step": 4,
+                "d2h_bytes_per_step": int(main["d2h_per_step"]),
+                "note": "mg_dobfs with the labels into pinned host memory every step; h2d = the "
+                        "4-byte source (a kernel argument); d2h = bytes the library copied "
+                        "(u32 head + 4/8-bit tail of the level array, widened on the host)"},
+        "roofline": roofline,
+        "tuned": {"do_a": 0.001, "do_b": 0.1, "value": round(tuned["value"], 3),
+                  "ms_per_step": round(tuned["dev_max_ms"] / args.steps, 4),
+                  "e2e": round(tuned["e2e"], 3),
+                  "note": "same graph and sources; the reference with the same do_a takes the "
+                          "same direction decisions (direction log checked in tests)"},
+        "reference_schedule": {
+            "do_a": 0.01, "do_b": 0.1, "value": round(refsched["value"], 3),
+            "ms_per_step": round(refsched["dev_max_ms"] / args.steps, 4),
+            "e2e": round(refsched["e2e"], 3),
+            "note": "dobfs_exact_cost off: every superstep runs in the direction the reference "
+                    "rule picks (push advance for forward steps)"},
+        "cpu_baseline": cpu,
+        "clocks": main["clocks"],
+        "gpu_launches": main["launches"],
+    }
+    print(json.dumps(line))
+    return 0
+
+
+def cpu_reference(graph_arrays, sources, arcs, max_s):
+    """time the reference engine (oracle/_ref) on the same graph; n = 1 partition"""
+    from oracle import ref
+    off, col = graph_arrays
+    t0 = time.time()
+    g = ref.RefGraph.from_csr(off, col)
+    plan = ref.RefPlan(g, np.zeros(len(off) - 1, np.uint32), 1)
+    prep = time.time() - t0
+    done, ms, a = [], 0.0, 0
+    t1 = time.time()
+    for s in sources:
+        r = plan.dobfs(s)
+        ms += r.stats.wall_ms
+        a += arcs[s]
+        done.append(s)
+        if time.time() - t1 > max_s:
+            break
+    return dict({"value": a / (ms * 1e-3) / 1e9, "unit": "GTEPS", "cores": 1,
+                 "kind": "reference",
+                 "sample": f"reference dobfs (n=1 partition, 1 thread) from sources {done}, "
+                           f"{ms:.0f} ms engine wall_ms (plan build {prep:.1f} s excluded)"},
+                **host_info())
+
+
+# ------------------------------------------------------------------------------ reference arm
+def reference_sweep(args, budget_s=60.0):
+    """best partition count of the reference engine (one std::thread per partition,
+    engine.hpp:951-959), chosen on a bounded sample: the same generator at scale - 4,
+    two sources per n, n in {1, 2, 4, 8, 16} up to the host's cores"""
+    from oracle import ref
+    sc = max(args.scale - 4, 10)
+    g = ref.RefGraph.rmat_hashed(sc, args.edge_factor, args.seed)
+    off = g.offsets()
+    deg = np.diff(off.astype(np.int64))
+    nv = len(off) - 1
+    srcs = pick_sources(off, 2)
+    out, t0 = {}, time.time()
+    for n in (1, 2, 4, 8, 16):
+        if n > (os.cpu_count() or 1) or time.time() - t0 > budget_s:
+            break
+        own = ref.partition_random(nv, n, 7) if n > 1 else np.zeros(nv, np.uint32)
+        p = ref.RefPlan(g, own, n)
+        ms, a = 0.0, 0
+        for s in srcs:
+            r = p.dobfs(s)
+            ms += r.stats.wall_ms
+            a += reached_arcs(r.labels, deg)
+        out[n] = a / (ms * 1e-3) / 1e9
+        del p
+    return sc, out
+
+
+def run_reference(args, rank, n_gpus):
     from oracle import ref
     if not ref.available():
         print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref not built"}))
         return 0
-    import paper_1504_04804_b200 as mg
-    # input synthesis only (not timed): the same hashed R-MAT graph
-    try:
-        plan, _ = build_plan(args, 1)
-        g = plan.download_graph()
-        del plan
-    except Exception:
-        g = mg.Csr.rmat_hashed(args.scale, args.edge_factor, args.seed)
-    off, col, _ = g.arrays()
+    sweep_scale, sweep = reference_sweep(args)
+    best_n = max(sweep, key=sweep.get) if sweep else 1
+    # input synthesis (not timed): the oracle's own counter-based R-MAT builder,
+    # bit-identical to the product's device generator, so this process never
+    # maps libmgraph_b200.so
+    t0 = time.time()
+    rg = ref.RefGraph.rmat_hashed(args.scale, args.edge_factor, args.seed)
+    gen_s = time.time() - t0
+    nv, ne, _ = rg.info()
+    off = rg.offsets()
     deg = np.diff(off.astype(np.int64))
     sources = pick_sources(off, args.num_sources)
-    rg = ref.RefGraph.from_csr(off, col)
-    del g, col
-    # same partitioning as our arm: one reference worker thread per GPU rank
-    owner = (mg.partition_random(len(off) - 1, world, 7) if world > 1
-             else np.zeros(len(off) - 1, np.uint32))
-    rplan = ref.RefPlan(rg, owner, world)
+    del off
+    owner = ref.partition_random(nv, best_n, 7) if best_n > 1 else np.zeros(nv, np.uint32)
+    t0 = time.time()
+    rplan = ref.RefPlan(rg, owner, best_n)
+    plan_s = time.time() - t0
     arcs = {}
     for i in range(args.warmup):
         s = sources[i % len(sources)]
@@ -435,17 +552,28 @@ def run_reference(args, rank, world, workload):
         ms += r.stats.wall_ms
         a += arcs[s]
     v = a / (ms * 1e-3) / 1e9
+    info = host_info()
     print(json.dumps({
-        "impl": "reference", "metric": "DOBFS GTEPS (A_r / t) on RMAT", "value": round(v, 4),
-        "unit": "GTEPS", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "impl": "reference", "metric": METRIC, "value": round(v, 4),
+        "unit": "GTEPS", "n_gpus": n_gpus, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": round(ms / args.steps, 3), "higher_is_better": True, "scaling": "strong",
-        "vs_baseline": None, "dtype": "u32", "data": "synthetic (hashed R-MAT)",
-        "config": {"workload": workload, "scale": args.scale, "edge_factor": args.edge_factor,
-                   "sources": sources, "partitions": world},
-        "cpu_baseline": {"value": round(v, 4), "unit": "GTEPS", "cores": world,
-                         "kind": "reference",
-                         "sample": f"{args.steps} reference dobfs runs (engine wall_ms), "
-                                   f"n={world} partitions = {world} worker threads"},
+        "vs_baseline": None, "dtype": "u32",
+        "data": "synthetic (the same hashed R-MAT, built by the oracle's host generator)",
+        "config": workload_config(args, n_gpus, sources, nv, ne),
+        "cpu_baseline": dict({"value": round(v, 4), "unit": "GTEPS", "cores": best_n,
+                              "kind": "reference",
+                              "sample": f"{args.steps} reference dobfs runs (engine wall_ms, "
+                                        f"engine.hpp:951-964) with n={best_n} partitions = "
+                                        f"{best_n} worker threads (the engine runs one thread "
+                                        f"per partition)"}, **info),
+        "reference_engine": {
+            "partitions": best_n,
+            "sweep": {"scale": sweep_scale, "gteps_by_partitions": {str(k): round(x, 4)
+                                                                   for k, x in sweep.items()},
+                      "note": "best partition count picked on the scale-4 sample (2 sources "
+                              "each), then used at full size"},
+            "graph_gen_s": round(gen_s, 1), "plan_build_s": round(plan_s, 1),
+            "graph_source": "oracle/gen_oracle.cpp (no product library in this process)"},
         "e2e": {"value": round(v, 4), "unit": "GTEPS", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
     }))

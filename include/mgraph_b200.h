@@ -122,6 +122,9 @@ int mg_plan_border_metrics(const mg_plan* plan, uint64_t* pair_border, uint64_t*
 /* copy the global CSR of a device-built plan back to the host (for the CPU
  * baseline / oracle on the same graph) */
 int mg_plan_download_graph(const mg_plan* plan, mg_graph** out);
+/* device->host bytes the last primitive call / fetch actually copied for its
+ * results (e.g. the split u32 / 8-bit / 4-bit label download) */
+int mg_plan_last_d2h_bytes(const mg_plan* plan, uint64_t* bytes);
 /* time the primitive's dominant kernel with CUDA events on its stream */
 int mg_plan_set_profiling(mg_plan* plan, int enable);
 
@@ -197,18 +200,23 @@ typedef struct mg_stats {
   double kernel2_ms;
   uint64_t kernel2_launches;
   double kernel2_bytes;
+  /* 1 when the supersteps ran as one CUDA-graph launch (device-driven loop,
+   * DobfsGraphRunner), 0 for the host-driven enactor loop */
+  int device_loop;
 } mg_stats;
 
 /* per-run arrays of the last run on this plan:
  *   MG_ARR_H_MATRIX n*n, MG_ARR_H_PER_ITER S*n ([iter][src]),
- *   MG_ARR_OUT_PER_ITER S, MG_ARR_EDGES_PER_ITER S, MG_ARR_COMBINE_PER_ITER S.
+ *   MG_ARR_OUT_PER_ITER S, MG_ARR_EDGES_PER_ITER S, MG_ARR_COMBINE_PER_ITER S,
+ *   MG_ARR_DIRECTION_LOG S (DOBFS: 0 forward / 1 backward per superstep).
  * Returns the full length in *len; copies min(len, cap) values. */
 enum {
   MG_ARR_H_MATRIX = 0,
   MG_ARR_H_PER_ITER = 1,
   MG_ARR_OUT_PER_ITER = 2,
   MG_ARR_EDGES_PER_ITER = 3,
-  MG_ARR_COMBINE_PER_ITER = 4
+  MG_ARR_COMBINE_PER_ITER = 4,
+  MG_ARR_DIRECTION_LOG = 5
 };
 int mg_plan_last_array(const mg_plan* plan, int which, uint64_t* buf, uint64_t cap,
                        uint64_t* len);

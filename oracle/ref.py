@@ -67,6 +67,9 @@ def lib():
             "ref_seq_cc": (None, [P, P]),
             "ref_seq_bc": (None, [P, u32, P]),
             "ref_seq_pagerank": (u64, [P, dbl, dbl, u64, P, P, u64]),
+            "ref_gen_last_error": (C.c_char_p, []),
+            "ref_rmat_hashed_edges": (i32, [i32, i32, u64, P, P]),
+            "ref_graph_rmat_hashed": (i32, [i32, i32, u64, i32, PP]),
         }
         for name, (res, args) in protos.items():
             f = getattr(L, name)
@@ -113,6 +116,17 @@ class RefGraph:
         return cls._make(lib().ref_graph_rmat, scale, ef, seed, int(symmetrize))
 
     @classmethod
+    def rmat_hashed(cls, scale, ef, seed, threads=0):
+        """counter-based R-MAT, symmetrized + deduplicated by the oracle's parallel
+        builder (gen_oracle.cpp) into a reference Csr: the reference side's copy of
+        the benchmark graph, made without the product library"""
+        out = C.c_void_p()
+        rc = lib().ref_graph_rmat_hashed(scale, ef, seed, threads, C.byref(out))
+        if rc != 0:
+            raise RefError(rc, lib().ref_gen_last_error().decode())
+        return cls(out.value)
+
+    @classmethod
     def from_csr(cls, off, col, w=None):
         off = np.ascontiguousarray(off, np.uint32)
         col = np.ascontiguousarray(col, np.uint32)
@@ -144,6 +158,13 @@ class RefGraph:
         nv, ne, w = C.c_uint32(), C.c_uint64(), C.c_int()
         lib().ref_graph_info(self.h, C.byref(nv), C.byref(ne), C.byref(w))
         return nv.value, ne.value, bool(w.value)
+
+    def offsets(self):
+        """row offsets only (no copy of the columns)"""
+        nv = self.info()[0]
+        off = np.empty(nv + 1, np.uint32)
+        lib().ref_graph_copy(self.h, _p(off), None, None)
+        return off
 
     def arrays(self):
         nv, ne, has_w = self.info()
@@ -181,6 +202,17 @@ class RefGraph:
         sums = np.empty(max(cap, 1), np.float64)
         it = lib().ref_seq_pagerank(self.h, d, eps, max_iter, _p(ranks), _p(sums), cap)
         return ranks, int(it), sums[:it].copy()
+
+
+def rmat_hashed_edges(scale, ef, seed):
+    """the raw counter-based R-MAT draws (src, dst), 2^scale * ef of them"""
+    m = (1 << scale) * ef
+    src = np.empty(m, np.uint32)
+    dst = np.empty(m, np.uint32)
+    rc = lib().ref_rmat_hashed_edges(scale, ef, seed, _p(src), _p(dst))
+    if rc != 0:
+        raise RefError(rc, lib().ref_gen_last_error().decode())
+    return src, dst
 
 
 def partition_random(nv, n, seed):

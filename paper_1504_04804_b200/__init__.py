@@ -479,7 +479,14 @@ def dobfs(plan: PartitionPlan, opt: DobfsOptions = DobfsOptions(), cfg: EngineCo
                           C.byref(fw), C.byref(bw), C.byref(st)))
     r = Result()
     r.labels, r.preds, r.stats = labels, preds, RunStats(plan, st, "dobfs")
-    r.direction_log = dl[:ln.value].copy()
+    if ln.value > len(dl):  # longer than the buffer: the library keeps the whole log
+        full = np.zeros(ln.value, np.uint64)
+        got = C.c_uint64()
+        _check(lib().mg_plan_last_array(plan._h, abi.MG_ARR_DIRECTION_LOG, _p(full), ln.value,
+                                        C.byref(got)))
+        r.direction_log = full.astype(np.int32)
+    else:
+        r.direction_log = dl[:ln.value].copy()
     r.forward_edges, r.backward_edges = fw.value, bw.value
     return r
 

@@ -18,7 +18,7 @@ ROLES = ("advance_output", "filter_output", "input_frontier", "outbox", "inbox")
 MG_NUM_ROLES = 5
 STOP_REASONS = ("frontiers_empty", "stop_condition", "max_supersteps", "worker_error")
 (MG_ARR_H_MATRIX, MG_ARR_H_PER_ITER, MG_ARR_OUT_PER_ITER, MG_ARR_EDGES_PER_ITER,
- MG_ARR_COMBINE_PER_ITER) = range(5)
+ MG_ARR_COMBINE_PER_ITER, MG_ARR_DIRECTION_LOG) = range(6)
 (MG_RES_LABELS, MG_RES_PREDS, MG_RES_DISTS, MG_RES_COMPONENTS, MG_RES_BC, MG_RES_SIGMA,
  MG_RES_RANKS) = range(7)
 
@@ -74,6 +74,7 @@ class mg_stats(C.Structure):
         ("kernel2_ms", C.c_double),
         ("kernel2_launches", C.c_uint64),
         ("kernel2_bytes", C.c_double),
+        ("device_loop", C.c_int),
     ]
 
 
@@ -120,6 +121,7 @@ PROTOTYPES = {
     "mg_plan_border_metrics": (i32, [P, P, C.POINTER(u64)]),
     "mg_plan_download_graph": (i32, [P, PP]),
     "mg_plan_set_profiling": (i32, [P, i32]),
+    "mg_plan_last_d2h_bytes": (i32, [P, C.POINTER(u64)]),
     "mg_config_default": (None, [C.POINTER(mg_config)]),
     "mg_plan_last_array": (i32, [P, i32, P, u64, C.POINTER(u64)]),
     "mg_plan_last_buffer_stats": (i32, [P, u32, i32, C.POINTER(u64), C.POINTER(u64),

@@ -205,6 +205,10 @@ int mg_plan_download_graph(const mg_plan* p, mg_graph** out) {
   });
 }
 
+int mg_plan_last_d2h_bytes(const mg_plan* p, uint64_t* bytes) {
+  return wrap([&] { *bytes = plan_of(p).last_d2h_bytes; });
+}
+
 int mg_plan_set_profiling(mg_plan* p, int enable) {
   return wrap([&] { plan_of(p).profile = enable != 0; });
 }
@@ -223,6 +227,7 @@ int mg_plan_last_array(const mg_plan* p, int which, uint64_t* buf, uint64_t cap,
       case MG_ARR_OUT_PER_ITER: flat = P.out_per_iter; break;
       case MG_ARR_EDGES_PER_ITER: flat = P.edges_per_iter; break;
       case MG_ARR_COMBINE_PER_ITER: flat = P.combine_per_iter; break;
+      case MG_ARR_DIRECTION_LOG: flat.assign(P.last_dir_log.begin(), P.last_dir_log.end()); break;
       default: throw Error(MG_EINVAL, "mg_plan_last_array: unknown array");
     }
     if (len) *len = flat.size();

@@ -391,6 +391,7 @@ void gather_result_t(Plan& P, const std::vector<const T*>& per_worker, T* host_o
     DeviceGuard dg(w.dev);
     const T* src = per_worker[p];
     if (P.n == 1 && P.dup == MG_DUP_ALL) {
+      P.last_d2h_bytes += sizeof(T) * (uint64_t)w.nv;
       MGB_CUDA(cudaMemcpyAsync(host_out, src, sizeof(T) * w.nv, cudaMemcpyDeviceToHost, w.stream));
       MGB_CUDA(cudaStreamSynchronize(w.stream));
       continue;
@@ -402,6 +403,7 @@ void gather_result_t(Plan& P, const std::vector<const T*>& per_worker, T* host_o
     MGB_LAUNCH(compact_hosted_kernel<T>, grid_for(nh, 256, 4096), 256, 0, w.stream, src,
                w.hosted.ptr, nh, tmp);
     std::vector<T> h(nh);
+    P.last_d2h_bytes += sizeof(T) * (uint64_t)nh;
     MGB_CUDA(cudaMemcpyAsync(h.data(), tmp, sizeof(T) * nh, cudaMemcpyDeviceToHost, w.stream));
     MGB_CUDA(cudaFreeAsync(tmp, w.stream));
     MGB_CUDA(cudaStreamSynchronize(w.stream));
@@ -527,6 +529,7 @@ void gather_labels_u32(Plan& P, const std::vector<const uint32_t*>& pw, uint32_t
   else
     MGB_LAUNCH(narrow_labels_kernel, grid_for(nb, 256, kNumSMs * 8), 256, 0, w.stream, src + m,
                nb, P.label_dev.ptr);
+  P.last_d2h_bytes += nbytes + 4ull * m;  // what actually crosses PCIe
   MGB_CUDA(cudaMemcpyAsync(P.label_stage, P.label_dev.ptr, nbytes, cudaMemcpyDeviceToHost,
                            w.stream));
   MGB_CUDA(cudaEventRecord(w.ev_k0, w.stream));

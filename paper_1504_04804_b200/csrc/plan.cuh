@@ -227,6 +227,10 @@ struct Plan {
   std::vector<std::vector<BufferStats>> last_buffers;  // [worker][role]
   // device-resident results of the last run (global ID space, on workers[0].dev)
   int last_result_kind = -1;
+  // bytes the last primitive call moved host<->device for its arguments /
+  // results (reset at the start of every call; the e2e bench line reports them)
+  uint64_t last_h2d_bytes = 0, last_d2h_bytes = 0;
+  std::vector<int> last_dir_log;  // DOBFS direction per superstep of the last run
 
   // live timing of the primitive's dominant kernel (bench roofline)
   bool profile = false;

@@ -1231,6 +1231,7 @@ class DobfsGraphRunner {
         std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
     st.device_ms = ms;
     st.gpu_launches = launches;
+    st.device_loop = 1;
     P.h_matrix.assign(1, std::vector<uint64_t>(1, 0));
     P.h_per_iter.assign(S, std::vector<uint64_t>(1, 0));
     P.out_per_iter = r.out;
@@ -3089,6 +3090,7 @@ int mg_bfs(mg_plan* plan, uint32_t source, int mark_preds, const mg_config* cfg,
            uint32_t* preds, mg_stats* stats) {
   return guarded([&] {
     Plan& P = *reinterpret_cast<Plan*>(plan);
+    P.last_d2h_bytes = 0;
     check_source(P, source, "bfs");
     mg_config c = cfg_or_default(cfg);
     P.last = mg_stats{};
@@ -3144,6 +3146,7 @@ int mg_dobfs(mg_plan* plan, uint32_t source, double do_a, double do_b, int mark_
              mg_stats* stats) {
   return guarded([&] {
     Plan& P = *reinterpret_cast<Plan*>(plan);
+    P.last_d2h_bytes = 0;
     check_source(P, source, "dobfs");
     mg_config c = cfg_or_default(cfg);
     std::vector<int> dir_log;
@@ -3165,6 +3168,7 @@ int mg_dobfs(mg_plan* plan, uint32_t source, double do_a, double do_b, int mark_
     P.last_result_kind = 0;
     gather_labels_u32(P, pw(P, &Worker::su32, 0), labels, P.last.supersteps);
     if (mark_preds) gather_u32(P, pw(P, &Worker::su32, 1), preds);
+    P.last_dir_log = dir_log;  // full log (mg_plan_last_array) when `cap` is short
     if (len) *len = dir_log.size();
     for (uint64_t i = 0; direction_log && i < dir_log.size() && i < cap; ++i)
       direction_log[i] = dir_log[i];
@@ -3181,6 +3185,7 @@ int mg_sssp(mg_plan* plan, uint32_t source, int mark_preds, const mg_config* cfg
             uint32_t* preds, mg_stats* stats) {
   return guarded([&] {
     Plan& P = *reinterpret_cast<Plan*>(plan);
+    P.last_d2h_bytes = 0;
     check_source(P, source, "sssp");
     if (!P.weighted && P.ne > 0) throw Error(MG_EINVAL, "sssp: graph has no edge weights");
     mg_config c = cfg_or_default(cfg);
@@ -3197,6 +3202,7 @@ int mg_sssp(mg_plan* plan, uint32_t source, int mark_preds, const mg_config* cfg
 int mg_cc(mg_plan* plan, const mg_config* cfg, uint32_t* components, mg_stats* stats) {
   return guarded([&] {
     Plan& P = *reinterpret_cast<Plan*>(plan);
+    P.last_d2h_bytes = 0;
     mg_config c = cfg_or_default(cfg);
     CcPrim prim;
     P.last = mg_stats{};
@@ -3211,6 +3217,7 @@ int mg_bc(mg_plan* plan, uint32_t source, const mg_config* cfg, double* bc, doub
           uint32_t* labels, mg_stats* stats) {
   return guarded([&] {
     Plan& P = *reinterpret_cast<Plan*>(plan);
+    P.last_d2h_bytes = 0;
     check_source(P, source, "bc");
     mg_config c = cfg_or_default(cfg);
     BcPrim prim(source);
@@ -3229,6 +3236,7 @@ int mg_pagerank(mg_plan* plan, double damping, double epsilon, uint64_t max_iter
                 uint64_t cap, uint64_t* len, mg_stats* stats) {
   return guarded([&] {
     Plan& P = *reinterpret_cast<Plan*>(plan);
+    P.last_d2h_bytes = 0;
     if (!(damping > 0.0 && damping < 1.0))
       throw Error(MG_EINVAL, "pagerank: damping must lie in (0,1)");
     if (!(epsilon > 0.0)) throw Error(MG_EINVAL, "pagerank: epsilon must be positive");
@@ -3258,6 +3266,7 @@ int mg_pagerank(mg_plan* plan, double damping, double epsilon, uint64_t max_iter
 int mg_plan_fetch(mg_plan* plan, int which, void* host_out) {
   return guarded([&] {
     Plan& P = *reinterpret_cast<Plan*>(plan);
+    P.last_d2h_bytes = 0;
     switch (which) {
       case MG_RES_LABELS: gather_u32(P, pw(P, &Worker::su32, 0), (uint32_t*)host_out); break;
       case MG_RES_PREDS: gather_u32(P, pw(P, &Worker::su32, 1), (uint32_t*)host_out); break;
