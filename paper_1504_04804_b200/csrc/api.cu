@@ -17,6 +17,56 @@ using namespace mgb;
 
 namespace {
 int wrap(const std::function<void()>& f) { return run_guarded(f); }
+
+// undirected cut of a device-resident graph (border_metrics, partition.cpp:
+// 224-240): arcs (u,v) with different owners, each pair once — from the
+// smaller endpoint, or from u when the reverse arc is absent (rows sorted:
+// binary search).  One warp per row.
+__global__ void edge_cut_kernel(const uint32_t* __restrict__ off, const uint32_t* __restrict__ col,
+                                const uint8_t* __restrict__ owner, uint32_t nv,
+                                unsigned long long* out) {
+  unsigned long long c = 0;
+  const uint32_t warps = gridDim.x * blockDim.x / 32;
+  for (uint32_t u = (blockIdx.x * blockDim.x + threadIdx.x) / 32; u < nv; u += warps) {
+    const uint8_t ou = owner[u];
+    for (uint32_t e = off[u] + lane_id(); e < off[u + 1]; e += 32) {
+      const uint32_t v = col[e];
+      if (owner[v] == ou) continue;
+      if (v > u) {
+        ++c;
+        continue;
+      }
+      uint32_t lo = off[v], hi = off[v + 1];
+      while (lo < hi) {
+        const uint32_t m = (lo + hi) >> 1;
+        if (col[m] < u) lo = m + 1;
+        else hi = m;
+      }
+      if (lo == off[v + 1] || col[lo] != u) ++c;
+    }
+  }
+  warp_add_u64(out, c);
+}
+
+uint64_t device_edge_cut(Plan& P) {
+  if (P.n == 1) return 0;
+  const uint32_t me = P.local_workers.front();
+  Worker& w = *P.workers[me];
+  const bool single = !P.g_off.ptr && P.n == 1;
+  if (!P.g_off.ptr && !single) throw Error(MG_EINVAL, "plan holds no global graph");
+  const uint32_t* d_off = single ? w.off.ptr : P.g_off.ptr;
+  const uint32_t* d_col = single ? w.col.ptr : P.g_col.ptr;
+  DeviceGuard dg(w.dev);
+  DevArray<unsigned long long> out;
+  out.alloc(1);
+  MGB_CUDA(cudaMemsetAsync(out.ptr, 0, 8, w.stream));
+  MGB_LAUNCH(edge_cut_kernel, grid_for((uint64_t)P.nv * 32, 256, num_sms() * 16), 256, 0, w.stream,
+             d_off, d_col, w.owner.ptr, P.nv, out.ptr);
+  unsigned long long c = 0;
+  MGB_CUDA(cudaMemcpyAsync(&c, out.ptr, 8, cudaMemcpyDeviceToHost, w.stream));
+  MGB_CUDA(cudaStreamSynchronize(w.stream));
+  return c;
+}
 mg_graph* box(HostCsr&& g) { return new mg_graph{std::make_shared<HostCsr>(std::move(g))}; }
 Plan& plan_of(const mg_plan* p) {
   if (!p) throw Error(MG_EINVAL, "null plan");
@@ -150,8 +200,11 @@ int mg_plan_border_metrics(const mg_plan* p, uint64_t* pair, uint64_t* cut) {
     if (pair)
       for (uint32_t i = 0; i < P.n; ++i)
         for (uint32_t j = 0; j < P.n; ++j) pair[i * P.n + j] = P.pair_border[i][j];
+    if (cut && !P.host_graph) {  // device-built plan: count on the GPU
+      *cut = device_edge_cut(P);
+      return;
+    }
     if (cut) {
-      if (!P.host_graph) throw Error(MG_EINVAL, "edge cut needs the host graph");
       const HostCsr& g = *P.host_graph;
       uint64_t c = 0;  // undirected edges {u,v} with different owners, counted once
       for (uint32_t u = 0; u < g.nv; ++u)

@@ -19,8 +19,12 @@ namespace mgb {
 constexpr uint32_t kInfLabel = 0xFFFFFFFFu;
 constexpr uint64_t kInfDist = 0xFFFFFFFFFFFFFFFFull;
 constexpr int kMaxWorkers = 64;
-constexpr int kMaxAssoc = 2;  // vertex / value associates per record (reference allows 8)
-constexpr int kNumSMs = 148;
+constexpr int kMaxAssoc = 8;  // vertex / value associates per record (engine.hpp:645-646)
+// B200 (sm_100a) has 148 SMs.  Device-side tiling heuristics use this design
+// constant (kMinTiles, the BC bucket CTA count: layout, not correctness);
+// host-side launch sizing asks the device (num_sms()), so grids stay
+// multiples of the SM count on any part the library runs on.
+constexpr int kB200SMs = 148;
 
 extern std::atomic<uint64_t> g_launches;
 
@@ -39,7 +43,22 @@ extern std::atomic<uint64_t> g_launches;
     MGB_CUDA(cudaGetLastError());                                                         \
   } while (0)
 
-inline unsigned grid_for(uint64_t items, unsigned per_block, unsigned cap = kNumSMs * 8) {
+// SM count of the current device (cached per ordinal)
+inline unsigned num_sms() {
+  static unsigned cache[64] = {};
+  int d = 0;
+  cudaGetDevice(&d);
+  if (d < 0 || d >= 64) return kB200SMs;
+  if (!cache[d]) {
+    int v = 0;
+    cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, d);
+    cache[d] = v > 0 ? static_cast<unsigned>(v) : kB200SMs;
+  }
+  return cache[d];
+}
+
+inline unsigned grid_for(uint64_t items, unsigned per_block, unsigned cap = 0) {
+  if (!cap) cap = num_sms() * 8;
   uint64_t g = (items + per_block - 1) / per_block;
   if (g < 1) g = 1;
   if (g > cap) g = cap;

@@ -23,6 +23,7 @@
 #include <cstring>
 #include <functional>
 #include <optional>
+#include <type_traits>
 
 #include "operators.cuh"
 
@@ -65,63 +66,160 @@ void fabric_exchange_reports(Plan& P, const WorkerReport& r, const Counters& c,
                              std::vector<WorkerReport>& reports,
                              std::vector<std::vector<uint32_t>>& sends, bool& overflow);
 
+// Associates a functor set may ship per record: the slot tables hold
+// kMaxAssoc (8, as the reference's fixed arrays, engine.hpp:645-646); the
+// per-thread staging in split/merge is sized by the functor's kAssocCap
+// (default 2, what the built-in primitives need) so their registers do not pay
+// for the general case.
+template <class F, class = void>
+struct AssocCap {
+  static constexpr int value = 2;
+};
+template <class F>
+struct AssocCap<F, std::void_t<decltype(F::kAssocCap)>> {
+  static constexpr int value = F::kAssocCap;
+};
+
+// ---------------------------------------------------------------------------
+// Dense exchange (broadcast primitives).  A broadcast superstep ships every
+// output vertex to every peer (E:880-890).  When a worker's output is large,
+// the same information is smaller as a dense array over its local ID space:
+//   kind 1  DOBFS: the discovery bitmap vis & ~vis_prev (|V|/8 bytes instead of
+//           4 bytes per record once the output holds >= |V|/32 vertices);
+//   kind 2  CC: the whole comp[] array (4 B/vertex instead of 8 B/record once
+//           more than half the vertices changed) — with min-combine this is an
+//           all-gather + local MIN reduction, and vertices outside the sender's
+//           delta are no-ops at the receiver (their value was broadcast before).
+// The sender decides on the device from its output length; the slot count
+// carries kDenseFlag, so each receiver merges each source in the format it was
+// sent.  H, C and wire records are counted in records, as the reference does.
+constexpr uint32_t kDenseFlag = 0x80000000u;
+
+struct DenseView {
+  int kind = 0;                      // 0: records only, 1: bitmap, 2: u32 values
+  const uint32_t* cur = nullptr;     // 1: visited bitmap now; 2: the value array
+  const uint32_t* prev = nullptr;    // 1: visited bitmap before this superstep's body
+  uint32_t* vis = nullptr;           // 1: the receiver's visited bitmap (merge pre-test)
+  uint32_t words = 0;                // bitmap words / values
+  uint32_t threshold = 0xFFFFFFFFu;  // dense once the output holds >= threshold vertices
+};
+
 // ---------------------------------------------------------------------------
 // split + pack: route every output vertex (engine.hpp:880-909) and store the
-// remote records directly into the destination inbox slot
+// remote records directly into the destination inbox slot.  Slot positions are
+// reserved once per warp and destination (broadcast: one ballot; selective:
+// lanes grouped by destination with match.any), not once per record: a single
+// per-destination counter hit by every record serialises at its L2 slice.
 
 template <class F>
 __global__ void __launch_bounds__(256)
     split_pack_kernel(F f, OwnerView ow, GraphView g, const uint32_t* __restrict__ out,
                       Counters* ctr, uint32_t* __restrict__ next, const SlotView* __restrict__ table,
                       uint32_t n, int broadcast, unsigned long long drop_mask, int nva, int nvv,
-                      int want_deg) {
+                      int want_deg, DenseView dv) {
+  constexpr int A = AssocCap<F>::value;
   const uint32_t cnt = ctr->out_cnt;
+  const bool dense = broadcast && dv.kind != 0 && cnt >= dv.threshold;
+  const unsigned lane = lane_id(), lt = (1u << lane) - 1u;
   unsigned long long my_deg = 0;
   for (uint32_t base = blockIdx.x * blockDim.x; base < cnt; base += gridDim.x * blockDim.x) {
-    uint32_t i = base + threadIdx.x;
-    bool local = false;
+    const uint32_t i = base + threadIdx.x;
+    const bool valid = i < cnt;
     uint32_t v = 0, q = ow.p;
-    if (i < cnt) {
+    if (valid) {
       v = out[i];
       q = broadcast ? ow.p : ow.owner_of_local(v);
-      local = (q == ow.p);
     }
-    uint32_t slot = warp_append(&ctr->next_cnt, local);
+    const bool local = valid && q == ow.p;
+    const uint32_t slot = warp_append(&ctr->next_cnt, local);
     if (local) {
       next[slot] = v;
       if (want_deg) my_deg += g.off[v + 1] - g.off[v];
     }
-    if (i >= cnt) continue;
+    uint32_t va[A];
+    double vv[A];
     if (broadcast) {
-      uint32_t va[kMaxAssoc];
-      double vv[kMaxAssoc];
-      f.gather(v, va, vv);
+      if (dense) continue;
+      if (valid) f.gather(v, va, vv);
+      const unsigned m = __ballot_sync(0xffffffffu, valid);
+      if (!m) continue;
+      const unsigned leader = __ffs(m) - 1;
       for (uint32_t d = 0; d < n; ++d) {
         if (d == ow.p || ((drop_mask >> d) & 1ull)) continue;
-        uint32_t pos = atomicAdd(&ctr->send_cnt[d], 1u);
+        uint32_t b = 0;
+        if (lane == leader) b = atomicAdd(&ctr->send_cnt[d], (uint32_t)__popc(m));
+        b = __shfl_sync(0xffffffffu, b, leader);
+        if (!valid) continue;
+        const uint32_t pos = b + __popc(m & lt);
         const SlotView& s = table[d];
         if (pos >= s.cap) {
           atomicExch(&ctr->overflow, 1u);
           continue;
         }
         s.ids[pos] = v;
-        for (int a = 0; a < nva; ++a) s.va[a][pos] = va[a];
-        for (int a = 0; a < nvv; ++a) s.vv[a][pos] = vv[a];
+#pragma unroll
+        for (int a = 0; a < A; ++a)
+          if (a < nva) s.va[a][pos] = va[a];
+#pragma unroll
+        for (int a = 0; a < A; ++a)
+          if (a < nvv) s.vv[a][pos] = vv[a];
       }
-    } else if (!local && f.send_filter(q, v)) {
-      uint32_t va[kMaxAssoc];
-      double vv[kMaxAssoc];
-      f.gather(v, va, vv);
-      if ((drop_mask >> q) & 1ull) continue;
-      uint32_t pos = atomicAdd(&ctr->send_cnt[q], 1u);
+    } else {
+      // send_filter before the drop test: its side effects (SSSP last_sent)
+      // happen for a dropped package too, as in the reference (E:424-432)
+      bool send = valid && !local && f.send_filter(q, v);
+      if (send && ((drop_mask >> q) & 1ull)) send = false;
+      if (send) f.gather(v, va, vv);
+      const unsigned m = __ballot_sync(0xffffffffu, send);
+      if (!send) continue;
+      const unsigned grp = __match_any_sync(m, q);
+      const unsigned leader = __ffs(grp) - 1;
+      uint32_t b = 0;
+      if (lane == leader) b = atomicAdd(&ctr->send_cnt[q], (uint32_t)__popc(grp));
+      b = __shfl_sync(grp, b, leader);
+      const uint32_t pos = b + __popc(grp & lt);
       const SlotView& s = table[q];
       if (pos >= s.cap) {
         atomicExch(&ctr->overflow, 1u);
         continue;
       }
       s.ids[pos] = f.peer_id(v, q, i);
-      for (int a = 0; a < nva; ++a) s.va[a][pos] = va[a];
-      for (int a = 0; a < nvv; ++a) s.vv[a][pos] = vv[a];
+#pragma unroll
+      for (int a = 0; a < A; ++a)
+        if (a < nva) s.va[a][pos] = va[a];
+#pragma unroll
+      for (int a = 0; a < A; ++a)
+        if (a < nvv) s.vv[a][pos] = vv[a];
+    }
+  }
+  if (dense) {
+    // the whole array, 16 bytes per store, into every peer's slot
+    if (blockIdx.x == 0 && threadIdx.x == 0)
+      for (uint32_t d = 0; d < n; ++d)
+        if (d != ow.p && !((drop_mask >> d) & 1ull)) ctr->send_cnt[d] = cnt | kDenseFlag;
+    const uint32_t n4 = dv.words / 4;
+    const uint32_t items = n4 + (dv.words - 4 * n4);  // uint4 stores, then the tail words
+    const uint32_t stride = gridDim.x * blockDim.x;
+    for (uint32_t k = blockIdx.x * blockDim.x + threadIdx.x; k < items; k += stride) {
+      const bool vec = k < n4;
+      uint4 w4 = make_uint4(0u, 0u, 0u, 0u);
+      uint32_t w1 = 0;
+      if (vec) {
+        w4 = reinterpret_cast<const uint4*>(dv.cur)[k];
+        if (dv.kind == 1) {
+          const uint4 p4 = reinterpret_cast<const uint4*>(dv.prev)[k];
+          w4 = make_uint4(w4.x & ~p4.x, w4.y & ~p4.y, w4.z & ~p4.z, w4.w & ~p4.w);
+        }
+      } else {
+        const uint32_t j = n4 * 4 + (k - n4);
+        w1 = dv.kind == 1 ? (dv.cur[j] & ~dv.prev[j]) : dv.cur[j];
+      }
+      for (uint32_t d = 0; d < n; ++d) {
+        if (d == ow.p || ((drop_mask >> d) & 1ull)) continue;
+        uint32_t* dst = table[d].ids;
+        if (vec) reinterpret_cast<uint4*>(dst)[k] = w4;
+        else dst[n4 * 4 + (k - n4)] = w1;
+      }
     }
   }
   if (want_deg) warp_add_u64(&ctr->next_deg, my_deg);
@@ -244,6 +342,7 @@ __global__ void __launch_bounds__(256)
   const uint32_t src = blockIdx.y;
   if (src == p) return;
   const uint32_t cnt = inbox_cnt[src];
+  if (cnt & kDenseFlag) return;  // merge_dense_kernel
   const SlotView s = slots[src];
   if (threadIdx.x == 0 && blockIdx.x == 0) ctr->recv_cnt[src] = cnt;
   unsigned long long my_deg = 0, my_comb = 0;
@@ -253,10 +352,13 @@ __global__ void __launch_bounds__(256)
     uint32_t v = 0;
     if (i < cnt) {
       v = s.ids[i];
-      uint32_t va[kMaxAssoc];
-      double vv[kMaxAssoc];
-      for (int a = 0; a < nva; ++a) va[a] = s.va[a][i];
-      for (int a = 0; a < nvv; ++a) vv[a] = s.vv[a][i];
+      constexpr int A = AssocCap<F>::value;
+      uint32_t va[A];
+      double vv[A];
+#pragma unroll
+      for (int a = 0; a < A; ++a) va[a] = a < nva ? s.va[a][i] : 0u;
+#pragma unroll
+      for (int a = 0; a < A; ++a) vv[a] = a < nvv ? s.vv[a][i] : 0.0;
       ++my_comb;
       bool accepted = f.combine(v, va, vv, iteration);
       if (accepted && enqueue) push = atomicExch(&merge_stamp[v], stamp) != stamp;
@@ -269,6 +371,72 @@ __global__ void __launch_bounds__(256)
   }
   if (want_deg) warp_add_u64(&ctr->next_deg, my_deg);
   warp_add_u64(&ctr->combine, my_comb);
+}
+
+// merge of a dense slot (see DenseView): kind 1 combines every bit the
+// receiver has not visited yet (a visited vertex cannot take an equal-or-later
+// label, so combine() on it would be a no-op); kind 2 combines every value
+// (no-ops outside the sender's delta).  C counts the sender's records.
+template <class F>
+__global__ void __launch_bounds__(256)
+    merge_dense_kernel(F f, DenseView dv, const SlotView* __restrict__ slots,
+                       const uint32_t* __restrict__ inbox_cnt, uint32_t p, uint32_t stamp,
+                       uint32_t iteration, uint32_t* merge_stamp, uint32_t* __restrict__ next,
+                       Counters* ctr, GraphView g, int want_deg) {
+  constexpr int A = AssocCap<F>::value;
+  const uint32_t src = blockIdx.y;
+  if (src == p) return;
+  const uint32_t c = inbox_cnt[src];
+  if (!(c & kDenseFlag)) return;
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    ctr->recv_cnt[src] = c & ~kDenseFlag;
+    atomicAdd(&ctr->combine, (unsigned long long)(c & ~kDenseFlag));
+  }
+  const uint32_t* __restrict__ words = slots[src].ids;
+  uint32_t va[A];
+  double vv[A];
+#pragma unroll
+  for (int a = 0; a < A; ++a) {
+    va[a] = 0u;
+    vv[a] = 0.0;
+  }
+  unsigned long long my_deg = 0;
+  for (uint32_t base = blockIdx.x * blockDim.x; base < dv.words; base += gridDim.x * blockDim.x) {
+    const uint32_t k = base + threadIdx.x;
+    if (dv.kind == 1) {
+      uint32_t cand = 0;
+      if (k < dv.words) {
+        cand = words[k];
+        if (cand) cand &= ~__ldcg(&dv.vis[k]);
+      }
+      while (__any_sync(0xffffffffu, cand != 0)) {
+        bool push = false;
+        uint32_t v = 0;
+        if (cand) {
+          v = k * 32 + (__ffs(cand) - 1);
+          cand &= cand - 1;
+          if (f.combine(v, va, vv, iteration)) push = atomicExch(&merge_stamp[v], stamp) != stamp;
+        }
+        const uint32_t slot = warp_append(&ctr->next_cnt, push);
+        if (push) {
+          next[slot] = v;
+          if (want_deg) my_deg += g.off[v + 1] - g.off[v];
+        }
+      }
+    } else {
+      bool push = false;
+      if (k < dv.words) {
+        va[0] = words[k];
+        if (f.combine(k, va, vv, iteration)) push = atomicExch(&merge_stamp[k], stamp) != stamp;
+      }
+      const uint32_t slot = warp_append(&ctr->next_cnt, push);
+      if (push) {
+        next[slot] = k;
+        if (want_deg) my_deg += g.off[k + 1] - g.off[k];
+      }
+    }
+  }
+  if (want_deg) warp_add_u64(&ctr->next_deg, my_deg);
 }
 
 // degree sum of a frontier (init: the advance bound of superstep 0)
@@ -356,10 +524,10 @@ struct Ctx {
     const uint64_t max_deg = in_degsum == kUnknownDeg ? 2 * w->ne + 1 : in_degsum;
     const uint64_t max_tiles = max_deg / kTile + 2 + kMinTiles;
     if (w->lb_tile.n < max_tiles + 1) w->lb_tile.alloc(max_tiles + 1);
-    MGB_LAUNCH(lb_tiles_kernel, grid_for(max_tiles + 1, 256, kNumSMs * 8), 256, 0, w->stream,
+    MGB_LAUNCH(lb_tiles_kernel, grid_for(max_tiles + 1, 256, num_sms() * 8), 256, 0, w->stream,
                w->lb_pref.ptr, w->lb_bsum.ptr, in_count, w->lb_bsum.ptr + nb, w->lb_tile.ptr,
                (uint32_t)max_tiles);
-    const unsigned resident = kNumSMs * 6;  // 32 KB smem + 256 threads per CTA
+    const unsigned resident = num_sms() * 6;  // 32 KB smem + 256 threads per CTA
     unsigned grid = in_degsum == kUnknownDeg ? resident
                                              : grid_for(in_degsum, lb_tile_size(in_degsum), resident);
     MGB_LAUNCH((lb_expand_kernel<F, kFused>), grid, kExpBlock, 0, w->stream, f, graph(),
@@ -378,7 +546,7 @@ struct Ctx {
     unsigned long long* tmp = &ctr()->next_deg;  // free until split/merge of this superstep
     MGB_CUDA(cudaMemsetAsync(tmp, 0, 8, w->stream));
     if (in_count)
-      MGB_LAUNCH(degsum_kernel, grid_for(in_count, 256, kNumSMs * 8), 256, 0, w->stream, graph(),
+      MGB_LAUNCH(degsum_kernel, grid_for(in_count, 256, num_sms() * 8), 256, 0, w->stream, graph(),
                  w->input.ptr, in_count, tmp);
     unsigned long long h = 0;
     MGB_CUDA(cudaMemcpyAsync(&h, tmp, 8, cudaMemcpyDeviceToHost, w->stream));
@@ -406,7 +574,7 @@ struct Ctx {
       MGB_CUDA(cudaStreamSynchronize(w->stream));
       ensure_output(adv < dedup_bound ? adv : dedup_bound);
       if (adv == 0) return;
-      MGB_LAUNCH(filter_kernel<F>, grid_for(adv, 256, kNumSMs * 8), 256, 0, w->stream, f,
+      MGB_LAUNCH(filter_kernel<F>, grid_for(adv, 256, num_sms() * 8), 256, 0, w->stream, f,
                  w->advance_out.ptr, &ctr()->adv_cnt, w->output.ptr, &ctr()->out_cnt);
     }
   }
@@ -418,6 +586,7 @@ struct RunState {
   std::vector<uint32_t> in_count, next_count;
   std::vector<uint64_t> in_deg, next_deg;
   std::vector<cudaEvent_t> packed;  // per worker, recorded after publish
+  std::vector<uint32_t> dense_words;  // per worker: words of its dense view this superstep
 };
 
 struct SmallList {
@@ -481,6 +650,9 @@ void run_primitive(Plan& P, Prim& prim, const mg_config& cfg) {
   HostTrace trace;
   trace("enter");
   const uint32_t n = P.n;
+  if (prim.nva < 0 || prim.nva > kMaxAssoc || prim.nvv < 0 || prim.nvv > kMaxAssoc)
+    throw Error(MG_EINVAL, std::string(prim.name) + ": at most " + std::to_string(kMaxAssoc) +
+                               " vertex and value associates per record");
   if (prim.dup_required >= 0 && P.dup != prim.dup_required)
     throw Error(MG_EINVAL, std::string(prim.name) + ": requires --dup " +
                                (prim.dup_required == MG_DUP_ALL ? "all" : "onehop"));
@@ -509,6 +681,16 @@ void run_primitive(Plan& P, Prim& prim, const mg_config& cfg) {
   rs.in_deg.assign(n, 0);
   rs.next_deg.assign(n, 0);
   rs.packed.assign(n, nullptr);
+  rs.dense_words.assign(n, 0);
+  // a hook or kernel that throws mid-run (a worker failure, E:773-782) must not
+  // leak the per-run events: the plan stays usable for the next call
+  struct EventGuard {
+    std::vector<cudaEvent_t>& ev;
+    ~EventGuard() {
+      for (auto& e : ev)
+        if (e) cudaEventDestroy(e), e = nullptr;
+    }
+  } event_guard{rs.packed};
 
   std::vector<Ctx> ctx(n);
   for (uint32_t p : P.local_workers) {
@@ -613,14 +795,18 @@ void run_primitive(Plan& P, Prim& prim, const mg_config& cfg) {
         w.output.cap = w.next_input.cap;
         w.next_input.cap = oc;
         if (want_deg)
-          MGB_LAUNCH(degsum_dev_kernel, kNumSMs * 4, 256, 0, w.stream, w.graph(),
+          MGB_LAUNCH(degsum_dev_kernel, num_sms() * 4, 256, 0, w.stream, w.graph(),
                      w.next_input.ptr, &w.ctr.ptr->out_cnt, &w.ctr.ptr->next_deg);
         MGB_CUDA(cudaEventRecord(rs.packed[p], w.stream));
         continue;
       }
       // next_input holds the local part plus everything merged this superstep
+      // (a dense slot can merge any vertex; merged vertices are unique)
+      const DenseView dv = step_comm[p] == MG_COMM_BROADCAST ? prim.dense_view(c) : DenseView{};
+      rs.dense_words[p] = dv.kind ? dv.words : 0;
       uint64_t incoming = 0;
       for (uint32_t s = 0; s < n; ++s) incoming += (s == p) ? 0 : w.slot_cap[s];
+      if (prim.dense_view(c).kind && incoming < w.nv) incoming = w.nv;
       w.next_input.ensure(w.output.cap + incoming, w.stream);
       unsigned long long drop = 0;
       if (cfg.drop_enabled && cfg.drop_src == p && cfg.drop_iteration == iter &&
@@ -628,11 +814,12 @@ void run_primitive(Plan& P, Prim& prim, const mg_config& cfg) {
         drop = 1ull << cfg.drop_dst;
       if (n > 1) MGB_CUDA(cudaEventRecord(w.ev_x0, w.stream));
       with_dev(prim, c, [&](auto dev) {
-        MGB_LAUNCH(split_pack_kernel<decltype(dev)>, grid_for(w.output.cap, 256, kNumSMs * 8),
-                   256, 0, w.stream, dev, c.owner_view(), w.graph(), w.output.ptr, w.ctr.ptr,
+        const uint64_t items = w.output.cap > dv.words ? w.output.cap : dv.words;
+        MGB_LAUNCH(split_pack_kernel<decltype(dev)>, grid_for(items, 256, num_sms() * 8), 256, 0,
+                   w.stream, dev, c.owner_view(), w.graph(), w.output.ptr, w.ctr.ptr,
                    w.next_input.ptr, w.send_table.ptr + parity * n, n,
                    step_comm[p] == MG_COMM_BROADCAST ? 1 : 0, drop, prim.nva, prim.nvv,
-                   (want_deg || prim.reports_deg) ? 1 : 0);
+                   (want_deg || prim.reports_deg) ? 1 : 0, dv);
       });
       if (n > 1) {
         MGB_LAUNCH(publish_kernel, 1, 64, 0, w.stream, w.ctr.ptr, w.send_cnt_ptr.ptr + parity * n,
@@ -664,13 +851,21 @@ void run_primitive(Plan& P, Prim& prim, const mg_config& cfg) {
         uint64_t maxcap = 0;
         for (uint32_t s = 0; s < n; ++s)
           if (s != p && w.slot_cap[s] > maxcap) maxcap = w.slot_cap[s];
-        dim3 grid(grid_for(maxcap, 256, kNumSMs * 2), n);
+        dim3 grid(grid_for(maxcap, 256, num_sms() * 2), n);
+        const DenseView dv = prim.dense_view(c);
         with_dev(prim, c, [&](auto dev) {
           MGB_LAUNCH(merge_kernel<decltype(dev)>, grid, 256, 0, w.stream, dev,
                      w.recv_table.ptr + parity * n, w.inbox_cnt.ptr + parity * kMaxWorkers, p,
                      (uint32_t)(iter + 1), (uint32_t)iter, w.merge_stamp.ptr, w.next_input.ptr,
                      w.ctr.ptr, w.graph(), prim.nva, prim.nvv, 1,
                      (want_deg || prim.reports_deg) ? 1 : 0);
+          if (dv.kind)
+            MGB_LAUNCH(merge_dense_kernel<decltype(dev)>,
+                       dim3(grid_for(dv.words, 256, num_sms() * 2), n), 256, 0, w.stream, dev, dv,
+                       w.recv_table.ptr + parity * n, w.inbox_cnt.ptr + parity * kMaxWorkers, p,
+                       (uint32_t)(iter + 1), (uint32_t)iter, w.merge_stamp.ptr,
+                       w.next_input.ptr, w.ctr.ptr, w.graph(),
+                       (want_deg || prim.reports_deg) ? 1 : 0);
         });
       }
       prim.after_merge(c);
@@ -716,11 +911,12 @@ void run_primitive(Plan& P, Prim& prim, const mg_config& cfg) {
       if (n > 1) {
         for (uint32_t q = 0; q < n; ++q) {
           if (q == p) continue;
-          uint64_t len = hc.send_cnt[q];
+          const uint64_t len = hc.send_cnt[q] & ~kDenseFlag;  // records (E:391-393)
           P.h_matrix[p][q] += len;
           h_src[p] += len;
           wire += len * inflation;
-          xbytes += len * (4ull + 4ull * prim.nva + 8ull * prim.nvv);
+          xbytes += (hc.send_cnt[q] & kDenseFlag) ? 4ull * rs.dense_words[p]
+                                                  : len * (4ull + 4ull * prim.nva + 8ull * prim.nvv);
         }
         float xms = 0;
         cudaEventElapsedTime(&xms, w.ev_x0, w.ev_x1);
@@ -753,7 +949,7 @@ void run_primitive(Plan& P, Prim& prim, const mg_config& cfg) {
             x.f[k] = d.f[k];
             x.u[k] = d.u[k];
           }
-          for (uint32_t e = 0; e < n; ++e) sends[q][e] = d.send_cnt[e];
+          for (uint32_t e = 0; e < n; ++e) sends[q][e] = d.send_cnt[e] & ~kDenseFlag;
           overflow |= d.overflow != 0;
         }
       } else {
@@ -815,7 +1011,6 @@ void run_primitive(Plan& P, Prim& prim, const mg_config& cfg) {
     float ms = 0;
     cudaEventElapsedTime(&ms, w.ev_start, w.ev_end);
     if (ms > dev_ms) dev_ms = ms;
-    cudaEventDestroy(rs.packed[p]);
   }
   auto t1 = std::chrono::steady_clock::now();
   mg_stats& st = P.last;

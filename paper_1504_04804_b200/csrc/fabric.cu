@@ -177,7 +177,7 @@ void fabric_exchange_reports(Plan& P, const WorkerReport& r, const Counters& c,
       x.f[k] = all[q].f[k];
       x.u[k] = all[q].u[k];
     }
-    for (uint32_t d = 0; d < n; ++d) sends[q][d] = all[q].send_cnt[d];
+    for (uint32_t d = 0; d < n; ++d) sends[q][d] = all[q].send_cnt[d] & ~kDenseFlag;
     overflow |= all[q].overflow != 0;
   }
 }

@@ -97,7 +97,7 @@ static __global__ void __launch_bounds__(1024)
 
 // Arcs per expansion tile: kTile for large advances; small advances are cut
 // into at least kMinTiles tiles (multiples of 256 arcs) so every SM gets work.
-constexpr uint32_t kMinTiles = 2 * kNumSMs;
+constexpr uint32_t kMinTiles = 2 * kB200SMs;
 __host__ __device__ __forceinline__ unsigned long long lb_tile_size(unsigned long long total) {
   if (total >= (unsigned long long)kTile * kMinTiles) return kTile;
   unsigned long long t = (total + kMinTiles - 1) / kMinTiles;

@@ -21,7 +21,7 @@ uint32_t device_max_u32(const uint32_t* a, uint64_t n) {
   DevArray<uint32_t> o;
   o.alloc(1);
   MGB_CUDA(cudaMemset(o.ptr, 0, 4));
-  if (n) MGB_LAUNCH(max_u32_kernel, kNumSMs * 8, 256, 0, 0, a, n, o.ptr);
+  if (n) MGB_LAUNCH(max_u32_kernel, num_sms() * 8, 256, 0, 0, a, n, o.ptr);
   uint32_t h = 0;
   MGB_CUDA(cudaMemcpy(&h, o.ptr, 4, cudaMemcpyDeviceToHost));
   return h;
@@ -524,10 +524,10 @@ void gather_labels_u32(Plan& P, const std::vector<const uint32_t*>& pw, uint32_t
   const bool nib = max_label < 15 && !(ne && ne[0] == '0');  // 4-bit levels: half the bytes
   const uint32_t nbytes = nib ? (nb + 1) / 2 : nb;
   if (nib)
-    MGB_LAUNCH(narrow_labels_nib_kernel, grid_for(nbytes, 256, kNumSMs * 8), 256, 0, w.stream,
+    MGB_LAUNCH(narrow_labels_nib_kernel, grid_for(nbytes, 256, num_sms() * 8), 256, 0, w.stream,
                src + m, nb, P.label_dev.ptr);
   else
-    MGB_LAUNCH(narrow_labels_kernel, grid_for(nb, 256, kNumSMs * 8), 256, 0, w.stream, src + m,
+    MGB_LAUNCH(narrow_labels_kernel, grid_for(nb, 256, num_sms() * 8), 256, 0, w.stream, src + m,
                nb, P.label_dev.ptr);
   P.last_d2h_bytes += nbytes + 4ull * m;  // what actually crosses PCIe
   MGB_CUDA(cudaMemcpyAsync(P.label_stage, P.label_dev.ptr, nbytes, cudaMemcpyDeviceToHost,

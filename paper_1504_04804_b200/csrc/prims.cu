@@ -41,6 +41,7 @@ struct PrimBase {
                                      : P.pair_border[src][dst];
   }
   int comm_selector(Ctx&, int comm) { return comm; }
+  DenseView dense_view(Ctx&) const { return {}; }  // records only
   bool stop_condition(const GlobalView&) { return false; }
   void after_merge(Ctx&) {}
   void finalize(Ctx&, const GlobalView&) {}
@@ -895,6 +896,26 @@ struct DobfsPrim : PrimBase {
     communication = MG_COMM_BROADCAST;
   }
   static uint64_t words(uint32_t nv) { return (nv + 31) / 32 + 1; }
+  // several partitions: a superstep's discoveries go to the peers as IDs, or as
+  // the discovery bitmap vis & ~vis_prev once they number >= |V|/32 (engine.cuh
+  // DenseView); the inbox then needs room for only |V|/32 records.  Predecessors
+  // travel as associates, so mark_preds keeps the record form.
+  uint64_t inbox_bound(Plan& P, uint32_t src, uint32_t dst, int comm) const {
+    if (!mark_preds && comm == MG_COMM_BROADCAST) return words(P.nv);
+    return PrimBase::inbox_bound(P, src, dst, comm);
+  }
+  DenseView dense_view(Ctx& c) const {
+    if (mark_preds) return {};
+    Worker& w = *c.w;
+    DenseView d;
+    d.kind = 1;
+    d.cur = w.su32[2].ptr;
+    d.prev = w.aux[4].ptr;
+    d.vis = w.su32[2].ptr;
+    d.words = (uint32_t)words(w.nv);
+    d.threshold = d.words;
+    return d;
+  }
   static void ensure_nonisolated(Worker& w) {
     if (w.nonisolated_ready) return;
     uint32_t nh = (uint32_t)w.hosted_host.size();
@@ -917,7 +938,7 @@ struct DobfsPrim : PrimBase {
     w.n_nonisolated = k;
     w.pull_rec.alloc(k ? k : 1);
     if (k)
-      MGB_LAUNCH(pull_records_kernel, grid_for(k, 256, kNumSMs * 16), 256, 0, w.stream, w.graph(),
+      MGB_LAUNCH(pull_records_kernel, grid_for(k, 256, num_sms() * 16), 256, 0, w.stream, w.graph(),
                  w.nonisolated.ptr, k, w.pull_rec.ptr);
     MGB_CUDA(cudaStreamSynchronize(w.stream));
     w.nonisolated_ready = true;
@@ -989,7 +1010,7 @@ struct DobfsPrim : PrimBase {
         uint32_t* cnt = w.aux[2].ptr + 2;
         MGB_CUDA(cudaMemsetAsync(cnt, 0, 4, w.stream));
         w.input.ensure(c.in_count, w.stream);
-        MGB_LAUNCH(bitmap_diff_list_kernel, grid_for(nw, 256, kNumSMs * 8), 256, 0, w.stream,
+        MGB_LAUNCH(bitmap_diff_list_kernel, grid_for(nw, 256, num_sms() * 8), 256, 0, w.stream,
                    w.su32[2].ptr, w.aux[4].ptr, (uint32_t)nw, w.input.ptr, cnt);
       }
     }
@@ -1030,7 +1051,7 @@ struct DobfsPrim : PrimBase {
         prof_nul_[w.p] = c.in_count;
       }
       if (reports_deg && !c.want_deg && c.P->n == 1)
-        MGB_LAUNCH(degsum_dev_kernel, kNumSMs * 4, 256, 0, w.stream, w.graph(), w.output.ptr,
+        MGB_LAUNCH(degsum_dev_kernel, num_sms() * 4, 256, 0, w.stream, w.graph(), w.output.ptr,
                    &c.ctr()->out_cnt, &c.ctr()->next_deg);
       return;
     }
@@ -1039,7 +1060,7 @@ struct DobfsPrim : PrimBase {
     // the previous superstep, so its bitmap is vis & ~vis_prev — one streaming
     // pass over |V|/32 words instead of an atomic per frontier vertex
     uint32_t* cnts = w.aux[2].ptr;     // [1] long-row queue length (zeroed below)
-    MGB_LAUNCH(frontier_diff_kernel, grid_for(nw, 256, kNumSMs * 8), 256, 0, w.stream,
+    MGB_LAUNCH(frontier_diff_kernel, grid_for(nw, 256, num_sms() * 8), 256, 0, w.stream,
                w.su32[2].ptr, w.aux[4].ptr, w.su32[3].ptr, (uint32_t)nw, cnts,
                dir == 0 ? &c.ctr()->edges : nullptr, (unsigned long long)logical_w);
     const int src = ul_src[w.p];
@@ -1066,12 +1087,12 @@ struct DobfsPrim : PrimBase {
         reports_deg && !c.want_deg && c.P->n == 1 ? &c.ctr()->next_deg : nullptr;
     if (nul) {
       auto* kern = emit ? dobfs_pull_thread_kernel<true> : dobfs_pull_thread_kernel<false>;
-      MGB_LAUNCH(kern, grid_for(nul, 256 * kPV, kNumSMs * MG_PULL_OCC), 256, 0,
+      MGB_LAUNCH(kern, grid_for(nul, 256 * kPV, num_sms() * MG_PULL_OCC), 256, 0,
                  w.stream, w.graph(), w.pull_rec.ptr, ul, nul, w.su32[0].ptr, w.su32[1].ptr, w.su32[2].ptr,
                  w.su32[3].ptr, next_label, mark_preds ? 1 : 0, c.owner_view(), emit ? 1 : 0,
                  w.output.ptr, w.ul_buf[dst].ptr, ulcnt, w.ul_buf[2].ptr, cnts + 1, c.ctr(),
                  scanned, deg_out, DobfsDyn{nullptr, nullptr, nullptr});
-      MGB_LAUNCH(dobfs_pull_group_kernel, kNumSMs * 8, 256, 0, w.stream, w.graph(),
+      MGB_LAUNCH(dobfs_pull_group_kernel, num_sms() * 8, 256, 0, w.stream, w.graph(),
                  w.pull_rec.ptr, w.ul_buf[2].ptr, cnts + 1, w.su32[0].ptr, w.su32[1].ptr,
                  w.su32[2].ptr, w.su32[3].ptr, next_label, mark_preds ? 1 : 0, c.owner_view(),
                  emit ? 1 : 0, w.output.ptr, w.ul_buf[dst].ptr, ulcnt, c.ctr(), scanned, deg_out,
@@ -1343,14 +1364,14 @@ class DobfsGraphRunner {
     // pull branch
     MGB_CUDA(cudaStreamBeginCaptureToGraph(s, bodies[0], nullptr, nullptr, 0,
                                            cudaStreamCaptureModeRelaxed));
-    MGB_LAUNCH(frontier_diff_kernel, grid_for(nw, 256, kNumSMs * 8), 256, 0, s, w.su32[2].ptr,
+    MGB_LAUNCH(frontier_diff_kernel, grid_for(nw, 256, num_sms() * 8), 256, 0, s, w.su32[2].ptr,
                w.aux[4].ptr, w.su32[3].ptr, (uint32_t)nw, cnts, nullptr, 0ull,
                (const DobfsLoop*)st, &ctr->edges);
-    MGB_LAUNCH(dobfs_pull_thread_kernel<false>, kNumSMs * MG_PULL_OCC, 256, 0, s, gv, w.pull_rec.ptr, nullptr, 0u,
+    MGB_LAUNCH(dobfs_pull_thread_kernel<false>, num_sms() * MG_PULL_OCC, 256, 0, s, gv, w.pull_rec.ptr, nullptr, 0u,
                w.su32[0].ptr, w.su32[1].ptr, w.su32[2].ptr, w.su32[3].ptr, 0u, mp, ow, 0,
                w.loop_front[1].ptr, nullptr, &ctr->misc, w.ul_buf[2].ptr, cnts + 1, ctr,
                (unsigned long long*)nullptr, &ctr->next_deg, dyn);
-    MGB_LAUNCH(dobfs_pull_group_kernel, kNumSMs * 8, 256, 0, s, gv, w.pull_rec.ptr,
+    MGB_LAUNCH(dobfs_pull_group_kernel, num_sms() * 8, 256, 0, s, gv, w.pull_rec.ptr,
                w.ul_buf[2].ptr, cnts + 1, w.su32[0].ptr, w.su32[1].ptr, w.su32[2].ptr,
                w.su32[3].ptr, 0u, mp, ow, 0, w.loop_front[1].ptr, nullptr, &ctr->misc, ctr,
                (unsigned long long*)nullptr, &ctr->next_deg, dyn);
@@ -1359,22 +1380,22 @@ class DobfsGraphRunner {
     // push branch: frontier list from the bitmap, prev = vis, edge-balanced advance
     MGB_CUDA(cudaStreamBeginCaptureToGraph(s, bodies[1], nullptr, nullptr, 0,
                                            cudaStreamCaptureModeRelaxed));
-    MGB_LAUNCH(bitmap_diff_list_kernel, grid_for(nw, 256, kNumSMs * 8), 256, 0, s, w.su32[2].ptr,
+    MGB_LAUNCH(bitmap_diff_list_kernel, grid_for(nw, 256, num_sms() * 8), 256, 0, s, w.su32[2].ptr,
                w.aux[4].ptr, (uint32_t)nw, w.loop_front[0].ptr, &st->in_count);
     MGB_CUDA(cudaMemcpyAsync(w.aux[4].ptr, w.su32[2].ptr, 4 * nw, cudaMemcpyDeviceToDevice, s));
     const uint32_t* nin = &st->in_count;
-    MGB_LAUNCH(lb_degree_kernel, kNumSMs * 8, kLbBlock, 0, s, w.off.ptr, w.loop_front[0].ptr, 0u,
+    MGB_LAUNCH(lb_degree_kernel, num_sms() * 8, kLbBlock, 0, s, w.off.ptr, w.loop_front[0].ptr, 0u,
                w.loop_lb_row.ptr, w.loop_lb_pref.ptr, w.loop_lb_bsum.ptr, nin);
     MGB_LAUNCH(lb_scan_kernel, 1, 1024, 0, s, w.loop_lb_bsum.ptr, 0u, w.loop_total.ptr,
                &ctr->edges, nin);
     const uint64_t max_tiles = (2 * w.ne + 1) / kTile + 2 + kMinTiles;
-    MGB_LAUNCH(lb_tiles_kernel, kNumSMs * 8, 256, 0, s, w.loop_lb_pref.ptr, w.loop_lb_bsum.ptr,
+    MGB_LAUNCH(lb_tiles_kernel, num_sms() * 8, 256, 0, s, w.loop_lb_pref.ptr, w.loop_lb_bsum.ptr,
                0u, w.loop_total.ptr, w.loop_tiles.ptr, (uint32_t)max_tiles, nin);
     DobfsDev f{w.su32[0].ptr, w.su32[1].ptr, w.su32[2].ptr, w.su32[3].ptr, ow, 0u, mp, &st->iter};
-    MGB_LAUNCH((lb_expand_kernel<DobfsDev, true>), kNumSMs * 6, kExpBlock, 0, s, f, gv,
+    MGB_LAUNCH((lb_expand_kernel<DobfsDev, true>), num_sms() * 6, kExpBlock, 0, s, f, gv,
                w.loop_front[0].ptr, 0u, w.loop_lb_row.ptr, w.loop_lb_pref.ptr, w.loop_lb_bsum.ptr,
                w.loop_total.ptr, w.loop_tiles.ptr, w.loop_front[1].ptr, &ctr->out_cnt, nin);
-    MGB_LAUNCH(degsum_dev_kernel, kNumSMs * 4, 256, 0, s, gv, w.loop_front[1].ptr,
+    MGB_LAUNCH(degsum_dev_kernel, num_sms() * 4, 256, 0, s, gv, w.loop_front[1].ptr,
                &ctr->out_cnt, &ctr->next_deg);
     MGB_CUDA(cudaStreamEndCapture(s, &tmp));
     const uint64_t l2 = g_launches.load();
@@ -1548,7 +1569,7 @@ struct SsspPrim : PrimBase {
     if (!narrow) return;
     if (w.su64[0].n < w.nv || !w.su64[0].ptr) w.su64[0].alloc(w.nv ? w.nv : 1);
     if (w.nv)
-      MGB_LAUNCH(widen_dist_kernel, grid_for(w.nv, 256, kNumSMs * 8), 256, 0, w.stream,
+      MGB_LAUNCH(widen_dist_kernel, grid_for(w.nv, 256, num_sms() * 8), 256, 0, w.stream,
                  w.su32[0].ptr, w.nv, w.su64[0].ptr);
   }
 };
@@ -1564,6 +1585,7 @@ struct CcDev {
   __device__ bool prefilter(uint32_t) const { return true; }
   __device__ bool combine(uint32_t v, const uint32_t* va, const double*, uint32_t) const {
     uint32_t c = va[0];
+    if (c >= __ldcg(&comp[v])) return false;  // comp only falls: no atomic for a no-op
     uint32_t old = atomicMin(&comp[v], c);
     if (c < old) {
       atomicMin(&snapshot[v], c);  // the sender already broadcast it to everyone
@@ -1725,7 +1747,7 @@ __global__ void __launch_bounds__(256)
     }
   }
   if (__any_sync(0xffffffffu, any) && lane_id() == 0) *hooked = 1;
-  warp_add_u64(scanned_out, scanned);
+  if (scanned_out) warp_add_u64(scanned_out, scanned);
 }
 
 // is the (ordered) transpose symmetric?  every arc (u <- v) needs (v <- u):
@@ -1827,6 +1849,19 @@ struct CcPrim : PrimBase {
     nc = nh;
   }
   CcDev dev(Ctx& c) { return {c.w->su32[0].ptr, c.w->su32[1].ptr}; }
+  // several partitions: a delta of more than half the vertices goes to the
+  // peers as the whole comp[] array (4 B/vertex instead of 8 B/record); the
+  // receivers' min-combine turns the exchange into an all-gather + MIN
+  // reduction (engine.cuh DenseView)
+  DenseView dense_view(Ctx& c) const {
+    if (ordered) return {};
+    DenseView d;
+    d.kind = 2;
+    d.cur = c.w->su32[0].ptr;
+    d.words = c.w->nv;
+    d.threshold = c.w->nv / 2 + 1;
+    return d;
+  }
   void body(Ctx& c) {  // primitives.cpp:436-472: local fixpoint, then delta
     Worker& w = *c.w;
     uint32_t nh = (uint32_t)w.hosted_host.size();
@@ -1836,26 +1871,31 @@ struct CcPrim : PrimBase {
     const uint64_t local_edges = w.ne;  // every hosted arc once per hook pass
     uint32_t* comp = comp_arr(w);
     if (ordered && c.P->n == 1) {
-      // one partition receives nothing, so superstep 0's fixpoint is final
+      // one partition receives nothing, so superstep 0's fixpoint is final.
+      // W keeps the reference's unit, |E_i| per hook sweep (primitives.cpp:
+      // 441-457): the sampled fixpoint counts its link pass plus its rest
+      // sweeps; a later superstep counts the one confirming sweep the
+      // reference runs on its own output (it can hook nothing, so it is not run)
       if (c.iter == 0) {
         if (symmetric(w)) {
-          sampled_fixpoint(c, comp);
+          scanned = sampled_fixpoint(c, comp) * local_edges;
           h = 0;
         }
       } else {
+        scanned = local_edges;
         h = 0;
       }
     }
     while (h) {
       MGB_CUDA(cudaMemsetAsync(hooked, 0, 4, w.stream));
       if (ordered)
-        MGB_LAUNCH(cc_hook_rows_kernel, grid_for((uint64_t)w.nv * kCcGroup, 256, kNumSMs * 16),
+        MGB_LAUNCH(cc_hook_rows_kernel, grid_for((uint64_t)w.nv * kCcGroup, 256, num_sms() * 16),
                    256, 0, w.stream, w.toff.ptr, w.tcol.ptr, w.nv, comp, hooked);
       else if (nh)
-        MGB_LAUNCH(cc_hook_kernel, grid_for((uint64_t)nh * 32, 256, kNumSMs * 16), 256, 0,
+        MGB_LAUNCH(cc_hook_kernel, grid_for((uint64_t)nh * 32, 256, num_sms() * 16), 256, 0,
                    w.stream, w.graph(), w.hosted.ptr, nh, comp, hooked);
       if (w.nv)
-        MGB_LAUNCH(cc_jump_kernel, grid_for(w.nv, 256, kNumSMs * 16), 256, 0, w.stream, comp,
+        MGB_LAUNCH(cc_jump_kernel, grid_for(w.nv, 256, num_sms() * 16), 256, 0, w.stream, comp,
                    w.nv);
       MGB_CUDA(cudaMemcpyAsync(&h, hooked, 4, cudaMemcpyDeviceToHost, w.stream));
       MGB_CUDA(cudaStreamSynchronize(w.stream));
@@ -1863,7 +1903,7 @@ struct CcPrim : PrimBase {
     }
     c.ensure_output(w.nv);
     if (w.nv)
-      MGB_LAUNCH(cc_delta_kernel, grid_for(w.nv, 256, kNumSMs * 8), 256, 0, w.stream, comp,
+      MGB_LAUNCH(cc_delta_kernel, grid_for(w.nv, 256, num_sms() * 8), 256, 0, w.stream, comp,
                  w.su32[1].ptr, w.nv, w.output.ptr, c.ctr(),
                  (c.P->n > 1 || c.want_deg) ? 1 : 0);  // one partition: only the count is read
     add_edges(c, scanned);
@@ -1872,9 +1912,9 @@ struct CcPrim : PrimBase {
     Worker& w = *c.w;
     if (!ordered) return;
     MGB_CUDA(cudaMemsetAsync(w.su32[1].ptr, 0xFF, 4ull * w.nv, w.stream));  // min vertex ID
-    MGB_LAUNCH(cc_min_id_kernel, grid_for(w.nv, 256, kNumSMs * 4), 256, 0, w.stream,
+    MGB_LAUNCH(cc_min_id_kernel, grid_for(w.nv, 256, num_sms() * 4), 256, 0, w.stream,
                w.aux[5].ptr, w.pr_iperm.ptr, w.nv, w.su32[1].ptr);
-    MGB_LAUNCH(cc_labels_kernel, grid_for(w.nv, 256, kNumSMs * 8), 256, 0, w.stream,
+    MGB_LAUNCH(cc_labels_kernel, grid_for(w.nv, 256, num_sms() * 8), 256, 0, w.stream,
                w.aux[5].ptr, w.pr_perm.ptr, w.su32[1].ptr, w.nv, w.su32[0].ptr);
   }
   static void add_edges(Ctx& c, uint64_t k);
@@ -1885,7 +1925,7 @@ struct CcPrim : PrimBase {
       f.alloc(1);
       uint32_t one = 1;
       MGB_CUDA(cudaMemcpy(f.ptr, &one, 4, cudaMemcpyHostToDevice));
-      MGB_LAUNCH(cc_symmetric_kernel, grid_for((uint64_t)w.nv * 32, 256, kNumSMs * 16), 256, 0,
+      MGB_LAUNCH(cc_symmetric_kernel, grid_for((uint64_t)w.nv * 32, 256, num_sms() * 16), 256, 0,
                  w.stream, w.toff.ptr, w.tcol.ptr, w.nv, f.ptr);
       MGB_CUDA(cudaMemcpyAsync(&one, f.ptr, 4, cudaMemcpyDeviceToHost, w.stream));
       MGB_CUDA(cudaStreamSynchronize(w.stream));
@@ -1893,9 +1933,10 @@ struct CcPrim : PrimBase {
     }
     return w.cc_symmetric == 1;
   }
-  void sampled_fixpoint(Ctx& c, uint32_t* comp) {
+  // returns the number of sweeps (link pass + rest sweeps, the last finding no hook)
+  uint64_t sampled_fixpoint(Ctx& c, uint32_t* comp) {
     Worker& w = *c.w;
-    const unsigned g = grid_for(w.nv, 256, kNumSMs * 16);
+    const unsigned g = grid_for(w.nv, 256, num_sms() * 16);
     MGB_LAUNCH(cc_link_kernel, g, 256, 0, w.stream, w.toff.ptr, w.tcol.ptr, w.nv, comp);
     MGB_LAUNCH(cc_jump_kernel, g, 256, 0, w.stream, comp, w.nv);
     if (w.aux[4].n < w.nv || !w.aux[4].ptr) w.aux[4].alloc(w.nv);  // roots after linking
@@ -1919,17 +1960,17 @@ struct CcPrim : PrimBase {
       i = j;
     }
     uint32_t* hooked = w.su32[3].ptr;
-    // arcs examined: kCcLink per vertex in the link pass, then the rest passes
-    CcPrim::add_edges(c, (uint64_t)w.nv * kCcLink < w.ne ? (uint64_t)w.nv * kCcLink : w.ne);
-    for (uint32_t h = 1; h;) {
+    uint64_t sweeps = 1;  // the link pass
+    for (uint32_t h = 1; h; ++sweeps) {
       MGB_CUDA(cudaMemsetAsync(hooked, 0, 4, w.stream));
-      MGB_LAUNCH(cc_hook_rest_kernel, grid_for((uint64_t)w.nv * kCcGroup, 256, kNumSMs * 16),
+      MGB_LAUNCH(cc_hook_rest_kernel, grid_for((uint64_t)w.nv * kCcGroup, 256, num_sms() * 16),
                  256, 0, w.stream, w.toff.ptr, w.tcol.ptr, w.nv, w.aux[4].ptr, giant, comp,
-                 hooked, &c.ctr()->edges);
+                 hooked, (unsigned long long*)nullptr);
       MGB_LAUNCH(cc_jump_kernel, g, 256, 0, w.stream, comp, w.nv);
       MGB_CUDA(cudaMemcpyAsync(&h, hooked, 4, cudaMemcpyDeviceToHost, w.stream));
       MGB_CUDA(cudaStreamSynchronize(w.stream));
     }
+    return sweeps;
   }
 };
 
@@ -2213,7 +2254,7 @@ __global__ void bc_huge_finish_kernel(GraphView g, const uint32_t* __restrict__ 
   }
   warp_add_u64(&ctr->edges, scanned);
 }
-constexpr uint32_t kBcBucketCtas = kNumSMs * 4;
+constexpr uint32_t kBcBucketCtas = kB200SMs * 4;
 
 __global__ void __launch_bounds__(256)
     bc_bucket_count_kernel(const uint32_t* __restrict__ hosted, uint32_t nh,
@@ -2352,7 +2393,7 @@ struct BcPrim : PrimBase {
     if (phase == kFwd) {
       c.pipeline(dev(c), w.nv);
       if (nh && c.P->n > 1)  // the global max hosted label; n = 1 derives it
-        MGB_LAUNCH(max_hosted_label_kernel, grid_for(nh, 256, kNumSMs * 4), 256, 0, w.stream,
+        MGB_LAUNCH(max_hosted_label_kernel, grid_for(nh, 256, num_sms() * 4), 256, 0, w.stream,
                    w.su32[0].ptr, w.hosted.ptr, nh, c.ctr());
       c.report.u[1] = kFwd;
       c.report.u[0] = 0;  // filled from the device counter
@@ -2387,16 +2428,16 @@ struct BcPrim : PrimBase {
       const uint32_t c0 = deepest ? 0 : bucket_start[K * (level + 1)];
       const uint32_t c1 = deepest ? 0 : bucket_start[K * (level + 2)];
       const uint32_t work = (s3 - s0) > (c1 - c0) ? (s3 - s0) : (c1 - c0);
-      MGB_LAUNCH(bc_level_prep_kernel, grid_for(work, 256, kNumSMs * 8), 256, 0, w.stream, list,
+      MGB_LAUNCH(bc_level_prep_kernel, grid_for(work, 256, num_sms() * 8), 256, 0, w.stream, list,
                  s0, s3, c0, c1, deepest ? 1 : 0, w.sf64[0].ptr, w.sf64[1].ptr, w.sf64[3].ptr,
                  w.output.ptr, c.ctr());
       if (!deepest) {  // the deepest level only broadcasts
         if (s1 > s0)
-          MGB_LAUNCH(bc_backward_thread_kernel, grid_for(s1 - s0, 256, kNumSMs * 8), 256, 0,
+          MGB_LAUNCH(bc_backward_thread_kernel, grid_for(s1 - s0, 256, num_sms() * 8), 256, 0,
                      w.stream, w.graph(), list + s0, nullptr, s1 - s0, w.sf64[0].ptr,
                      w.sf64[1].ptr, w.sf64[2].ptr, w.sf64[3].ptr, source, c.ctr());
         if (s2 > s1)
-          MGB_LAUNCH(bc_backward_warp_kernel, grid_for((uint64_t)(s2 - s1) * 32, 256, kNumSMs * 8),
+          MGB_LAUNCH(bc_backward_warp_kernel, grid_for((uint64_t)(s2 - s1) * 32, 256, num_sms() * 8),
                      256, 0, w.stream, w.graph(), list + s1, nullptr, s2 - s1, w.sf64[0].ptr,
                      w.sf64[1].ptr, w.sf64[2].ptr, w.sf64[3].ptr, source, c.ctr());
         if (s3 > s2) {  // huge rows: chunks over many CTAs
@@ -2405,9 +2446,9 @@ struct BcPrim : PrimBase {
           if (w.bc_acc.n < nh_) w.bc_acc.alloc(nh_);
           MGB_LAUNCH(bc_huge_prefix_kernel, 1, 1024, 0, w.stream, list + s2, nh_, w.off.ptr,
                      w.aux[3].ptr, w.bc_acc.ptr);
-          MGB_LAUNCH(bc_huge_chunks_kernel, kNumSMs * 8, 256, 0, w.stream, w.graph(), list + s2,
+          MGB_LAUNCH(bc_huge_chunks_kernel, num_sms() * 8, 256, 0, w.stream, w.graph(), list + s2,
                      nh_, w.aux[3].ptr, w.sf64[3].ptr, w.bc_acc.ptr);
-          MGB_LAUNCH(bc_huge_finish_kernel, grid_for(nh_, 256, kNumSMs), 256, 0, w.stream,
+          MGB_LAUNCH(bc_huge_finish_kernel, grid_for(nh_, 256, num_sms()), 256, 0, w.stream,
                      w.graph(), list + s2, nh_, w.bc_acc.ptr, w.sf64[0].ptr, w.sf64[1].ptr,
                      w.sf64[2].ptr, source, c.ctr());
         }
@@ -2425,15 +2466,15 @@ struct BcPrim : PrimBase {
       uint32_t* cnts = w.aux[2].ptr;
       MGB_CUDA(cudaMemsetAsync(cnts, 0, 8, w.stream));
       if (nh) {
-        MGB_LAUNCH(bc_level_select_kernel, grid_for(nh, 256, kNumSMs * 16), 256, 0, w.stream,
+        MGB_LAUNCH(bc_level_select_kernel, grid_for(nh, 256, num_sms() * 16), 256, 0, w.stream,
                    w.hosted.ptr, nh, w.su32[0].ptr, w.off.ptr, level, w.output.ptr, c.ctr(),
                    w.aux[0].ptr, cnts, w.aux[1].ptr, cnts + 1, level == max_level ? 1 : 0,
                    w.sf64[0].ptr, w.sf64[1].ptr, w.sf64[3].ptr);
         if (level < max_level) {  // the deepest level only broadcasts
-          MGB_LAUNCH(bc_backward_thread_kernel, kNumSMs * 8, 256, 0, w.stream, w.graph(),
+          MGB_LAUNCH(bc_backward_thread_kernel, num_sms() * 8, 256, 0, w.stream, w.graph(),
                      w.aux[0].ptr, cnts, 0u, w.sf64[0].ptr, w.sf64[1].ptr, w.sf64[2].ptr,
                      w.sf64[3].ptr, source, c.ctr());
-          MGB_LAUNCH(bc_backward_warp_kernel, kNumSMs * 8, 256, 0, w.stream, w.graph(),
+          MGB_LAUNCH(bc_backward_warp_kernel, num_sms() * 8, 256, 0, w.stream, w.graph(),
                      w.aux[1].ptr, cnts + 1, 0u, w.sf64[0].ptr, w.sf64[1].ptr, w.sf64[2].ptr,
                      w.sf64[3].ptr, source, c.ctr());
         }
@@ -2829,13 +2870,13 @@ void ensure_transpose(Plan& P, Worker& w) {
     w.pr_perm.upload(perm.data(), w.nv, w.stream);
     w.pr_pdeg.alloc(w.nv);
   w.pr_iperm.alloc(w.nv);
-  MGB_LAUNCH(iperm_kernel, grid_for(w.nv, 256, kNumSMs * 8), 256, 0, w.stream, w.pr_perm.ptr,
+  MGB_LAUNCH(iperm_kernel, grid_for(w.nv, 256, num_sms() * 8), 256, 0, w.stream, w.pr_perm.ptr,
              w.nv, w.pr_iperm.ptr);
-    MGB_LAUNCH(transpose_keys_perm_kernel, grid_for((uint64_t)w.nv * 32, 256, kNumSMs * 16),
+    MGB_LAUNCH(transpose_keys_perm_kernel, grid_for((uint64_t)w.nv * 32, 256, num_sms() * 16),
                256, 0, w.stream, w.graph(), w.pr_perm.ptr, k0.ptr, w.pr_pdeg.ptr);
     MGB_CUDA(cudaStreamSynchronize(w.stream));
   } else if (nh && ne) {
-    MGB_LAUNCH(transpose_keys_kernel, grid_for((uint64_t)nh * 32, 256, kNumSMs * 16), 256, 0,
+    MGB_LAUNCH(transpose_keys_kernel, grid_for((uint64_t)nh * 32, 256, num_sms() * 16), 256, 0,
                w.stream, w.graph(), w.hosted.ptr, nh, k0.ptr);
   }
   cub::DoubleBuffer<unsigned long long> db(k0.ptr, k1.ptr);
@@ -2844,14 +2885,14 @@ void ensure_transpose(Plan& P, Worker& w) {
   void* tmp = nullptr;
   MGB_CUDA(cudaMalloc(&tmp, tb + 16));
   cub::DeviceRadixSort::SortKeys(tmp, tb, db, (int64_t)ne, 0, 64, w.stream);
-  MGB_LAUNCH(transpose_csr_kernel, kNumSMs * 16, 256, 0, w.stream, db.Current(), ne, w.nv,
+  MGB_LAUNCH(transpose_csr_kernel, num_sms() * 16, 256, 0, w.stream, db.Current(), ne, w.nv,
              w.toff.ptr, w.tcol.ptr);
   DevArray<uint32_t> cnt;
   cnt.alloc(1);
   MGB_CUDA(cudaMemsetAsync(cnt.ptr, 0, 4, w.stream));
   w.tlong.alloc(w.nv ? w.nv : 1);
   if (w.nv)
-    MGB_LAUNCH(select_long_rows_kernel, grid_for(w.nv, 256, kNumSMs * 8), 256, 0, w.stream,
+    MGB_LAUNCH(select_long_rows_kernel, grid_for(w.nv, 256, num_sms() * 8), 256, 0, w.stream,
                w.toff.ptr, w.nv, w.tlong.ptr, cnt.ptr);
   MGB_CUDA(cudaMemcpyAsync(&w.n_tlong, cnt.ptr, 4, cudaMemcpyDeviceToHost, w.stream));
   MGB_CUDA(cudaStreamSynchronize(w.stream));
@@ -2882,7 +2923,7 @@ struct PrPrim : PrimBase {
     if (w.pr_reordered) {
       for (int k : {0, 1, 2, 3})
         if (w.sf64[k].n < w.nv || !w.sf64[k].ptr) w.sf64[k].alloc(w.nv);
-      MGB_LAUNCH(fill_f64_kernel, grid_for(w.nv, 256, kNumSMs * 8), 256, 0, w.stream,
+      MGB_LAUNCH(fill_f64_kernel, grid_for(w.nv, 256, num_sms() * 8), 256, 0, w.stream,
                  w.sf64[3].ptr, w.nv, 1.0 / (double)c.P->nv);
       return;
     }
@@ -2899,7 +2940,7 @@ struct PrPrim : PrimBase {
     const double n = (double)c.P->nv;
     uint32_t nh = (uint32_t)w.hosted_host.size();
     if (nh)
-      MGB_LAUNCH(pr_update_kernel, grid_for(nh, 256, kNumSMs * 8), 256, 0, w.stream, w.hosted.ptr,
+      MGB_LAUNCH(pr_update_kernel, grid_for(nh, 256, num_sms() * 8), 256, 0, w.stream, w.hosted.ptr,
                  nh, w.sf64[0].ptr, w.sf64[1].ptr, (1.0 - damping) / n, damping,
                  dangling_prev / n, do_update ? 1 : 0, c.ctr());
   }
@@ -2909,16 +2950,16 @@ struct PrPrim : PrimBase {
   void update_contrib(Ctx& c, double dangling_prev, bool do_update) {
     Worker& w = *c.w;
     const double n = (double)c.P->nv;
-    MGB_LAUNCH(pr_update_contrib_kernel, grid_for(w.nv, 256, kNumSMs * 8), 256, 0, w.stream,
+    MGB_LAUNCH(pr_update_contrib_kernel, grid_for(w.nv, 256, num_sms() * 8), 256, 0, w.stream,
                w.nv, w.pr_pdeg.ptr, w.sf64[3].ptr, w.sf64[1].ptr, w.sf64[2].ptr,
                (1.0 - damping) / n, damping, dangling_prev / n, do_update ? 1 : 0, c.ctr());
   }
   void pull(Worker& w) {
     if (w.nv)
-      MGB_LAUNCH(pr_pull_kernel, grid_for(w.nv, 256, kNumSMs * 16), 256, 0, w.stream,
+      MGB_LAUNCH(pr_pull_kernel, grid_for(w.nv, 256, num_sms() * 16), 256, 0, w.stream,
                  w.toff.ptr, w.tcol.ptr, w.nv, w.sf64[2].ptr, w.sf64[1].ptr);
     if (w.n_tlong)
-      MGB_LAUNCH(pr_pull_warp_kernel, grid_for((uint64_t)w.n_tlong * 32, 256, kNumSMs * 8), 256,
+      MGB_LAUNCH(pr_pull_warp_kernel, grid_for((uint64_t)w.n_tlong * 32, 256, num_sms() * 8), 256,
                  0, w.stream, w.toff.ptr, w.tcol.ptr, w.tlong.ptr, w.n_tlong, w.sf64[2].ptr,
                  w.sf64[1].ptr);
   }
@@ -2960,10 +3001,10 @@ struct PrPrim : PrimBase {
     PrFuse f{w.pr_pdeg.ptr, w.sf64[3].ptr, nxt, (1.0 - damping) / n, damping,
              next_dangling / n, c.iter == 0 ? &c.ctr()->f[0] : nullptr, n, c.iter == 0 ? 0 : 1};
     if (w.nv)
-      MGB_LAUNCH(pr_pull_update_kernel, grid_for(w.nv, 256, kNumSMs * 16), 256, 0, w.stream,
+      MGB_LAUNCH(pr_pull_update_kernel, grid_for(w.nv, 256, num_sms() * 16), 256, 0, w.stream,
                  w.toff.ptr, w.tcol.ptr, w.nv, cur, f, c.ctr());
     if (w.n_tlong)
-      MGB_LAUNCH(pr_pull_update_warp_kernel, grid_for((uint64_t)w.n_tlong * 32, 256, kNumSMs * 8),
+      MGB_LAUNCH(pr_pull_update_warp_kernel, grid_for((uint64_t)w.n_tlong * 32, 256, num_sms() * 8),
                  256, 0, w.stream, w.toff.ptr, w.tcol.ptr, w.tlong.ptr, w.n_tlong, cur, f, c.ctr());
   }
   void body(Ctx& c) {  // primitives.cpp:747-782
@@ -2984,13 +3025,13 @@ struct PrPrim : PrimBase {
     // gathered per destination (pull) in a fixed order
     if (w.sf64[2].n < w.nv || !w.sf64[2].ptr) w.sf64[2].alloc(w.nv ? w.nv : 1);
     if (nh)
-      MGB_LAUNCH(pr_contrib_kernel, grid_for(nh, 256, kNumSMs * 8), 256, 0, w.stream, w.graph(),
+      MGB_LAUNCH(pr_contrib_kernel, grid_for(nh, 256, num_sms() * 8), 256, 0, w.stream, w.graph(),
                  w.hosted.ptr, nh, w.sf64[0].ptr, w.sf64[2].ptr, c.ctr());
     if (w.nv)
-      MGB_LAUNCH(pr_pull_kernel, grid_for(w.nv, 256, kNumSMs * 16), 256, 0, w.stream,
+      MGB_LAUNCH(pr_pull_kernel, grid_for(w.nv, 256, num_sms() * 16), 256, 0, w.stream,
                  w.toff.ptr, w.tcol.ptr, w.nv, w.sf64[2].ptr, w.sf64[1].ptr);
     if (w.n_tlong)
-      MGB_LAUNCH(pr_pull_warp_kernel, grid_for((uint64_t)w.n_tlong * 32, 256, kNumSMs * 8), 256,
+      MGB_LAUNCH(pr_pull_warp_kernel, grid_for((uint64_t)w.n_tlong * 32, 256, num_sms() * 8), 256,
                  0, w.stream, w.toff.ptr, w.tcol.ptr, w.tlong.ptr, w.n_tlong, w.sf64[2].ptr,
                  w.sf64[1].ptr);
     uint32_t nb = (uint32_t)w.border.n;
@@ -3017,7 +3058,7 @@ struct PrPrim : PrimBase {
       if (first) ++updates;
     }
     if (w.pr_reordered && w.nv)  // ranks back to vertex IDs
-      MGB_LAUNCH(unpermute_f64_kernel, grid_for(w.nv, 256, kNumSMs * 8), 256, 0, w.stream,
+      MGB_LAUNCH(unpermute_f64_kernel, grid_for(w.nv, 256, num_sms() * 8), 256, 0, w.stream,
                  w.sf64[3].ptr, w.pr_perm.ptr, w.nv, w.sf64[0].ptr);
   }
 };

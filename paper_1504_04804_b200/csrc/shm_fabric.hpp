@@ -18,7 +18,7 @@ namespace mgb {
 class ShmFabric {
  public:
   static constexpr uint32_t kMaxRanks = 64;
-  static constexpr uint32_t kBlobBytes = 4096;
+  static constexpr uint32_t kBlobBytes = 16384;
 
   // key: unique per job (all ranks must pass the same string)
   ShmFabric(const std::string& key, uint32_t rank, uint32_t world, double timeout_s = 300.0);

@@ -241,6 +241,14 @@ def test_cc_equals_union_find(G, name, n):
     plan, owner = plan_for(g, n, 5 * n + 2)
     r = mg.cc(plan)
     assert np.array_equal(r.components, seq.connected_components(off, col))
+    # W in the reference's unit (primitives.cpp:441-457): |E_i| per hook sweep, at
+    # least one sweep per worker per superstep (the sweep count of a parallel
+    # hook is its own, so W is not compared with the sequential loop's)
+    E = len(col)
+    assert all(int(e) >= E for e in r.stats.edges_per_iter)
+    if n == 1:
+        assert r.stats.edges_examined % max(E, 1) == 0
+        assert r.stats.edges_examined >= r.stats.supersteps * E
     if ref.available():
         rr = ref.RefPlan(ref.RefGraph.from_csr(off, col), owner, n).cc()
         assert r.stats.supersteps == rr.stats.supersteps
