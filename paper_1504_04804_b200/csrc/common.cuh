@@ -155,12 +155,43 @@ struct WarpQueue {
   }
 };
 
+// Sums are skipped when zero: a kernel that found no work must not end with
+// one same-address atomic per warp (~10^4 of them serialise at one L2 slice
+// for ~15 us — measured on the empty DOBFS long-row stage).
 __device__ __forceinline__ void warp_add_u64(unsigned long long* counter, uint64_t v) {
   unsigned active = __activemask();
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(active, v, o);
   // lanes outside `active` contributed nothing; the lowest active lane adds
-  if (lane_id() == (unsigned)(__ffs(active) - 1)) atomicAdd(counter, (unsigned long long)v);
+  if (v && lane_id() == (unsigned)(__ffs(active) - 1)) atomicAdd(counter, (unsigned long long)v);
+}
+
+// CTA-wide sums of N counters with ONE atomic per counter per CTA (zero sums
+// and null counters skipped), for the totals a kernel reports at its end.
+// Every thread of the CTA must call it, once per kernel.
+template <int N>
+__device__ __forceinline__ void block_add_u64(unsigned long long* const (&dst)[N],
+                                              const uint64_t (&v)[N]) {
+  __shared__ unsigned long long s_part[32][N];
+  const unsigned warp = threadIdx.x >> 5, lane = lane_id(), nwarps = (blockDim.x + 31) >> 5;
+  uint64_t x[N];
+#pragma unroll
+  for (int i = 0; i < N; ++i) {
+    x[i] = v[i];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) x[i] += __shfl_xor_sync(0xffffffffu, x[i], o);
+    if (lane == 0) s_part[warp][i] = x[i];
+  }
+  __syncthreads();
+  if (warp == 0) {
+#pragma unroll
+    for (int i = 0; i < N; ++i) {
+      uint64_t y = lane < nwarps ? s_part[lane][i] : 0ull;
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) y += __shfl_xor_sync(0xffffffffu, y, o);
+      if (lane == 0 && y && dst[i]) atomicAdd(dst[i], (unsigned long long)y);
+    }
+  }
 }
 
 // ---------------------------------------------------------------------------

@@ -375,6 +375,10 @@ constexpr uint32_t kPullQ = 256 * kPV + MG_PULL_QX;  // CTA queue capacity (>= o
 // only rows longer than kPullStart go on to the cooperative stage
 constexpr int kPullMid = MG_PULL_MID;
 constexpr uint32_t kPullStart = kPullK + kPullMid;
+// (measured: stage 1b as its own kernel over the long-row queue, one row per
+// thread and no CTA barrier, is slower — 8.93 -> 10.61 ms over the bench
+// sources — the inline stage reuses the record already in registers)
+constexpr bool kInline1b = kPullMid > 0;
 #ifndef MG_MID_PARTS
 #define MG_MID_PARTS 1
 #endif
@@ -458,6 +462,9 @@ __device__ __forceinline__ void warp_set_bits_smem(uint32_t* bits, uint32_t* win
 #ifndef MG_PULL_OCC
 #define MG_PULL_OCC 4
 #endif
+#ifndef MG_PULL_PF
+#define MG_PULL_PF 1
+#endif
 // kEmit: discoveries listed (several partitions); otherwise only counted and
 // the found queue takes no shared memory
 template <bool kEmit>
@@ -486,7 +493,7 @@ __global__ void __launch_bounds__(256, MG_PULL_OCC)
   __shared__ BlockQueue<kPullQ> q_keep, q_long;
   __shared__ uint32_t s_found;
   __shared__ uint32_t s_win[256 / 32][kBitSlots];  // visited-bit merge windows
-  __shared__ uint32_t s_mid[kPullMid > 0 ? 256 / 32 : 1][kPullMid > 0 ? 32 * kPV / kMidParts : 1];
+  __shared__ uint32_t s_mid[kInline1b ? 256 / 32 : 1][kInline1b ? 32 * kPV / kMidParts : 1];
   for (uint32_t i = threadIdx.x; i < 8 * kBitSlots; i += blockDim.x) (&s_win[0][0])[i] = 0u;
   q_found.reset();
   q_keep.reset();
@@ -495,6 +502,23 @@ __global__ void __launch_bounds__(256, MG_PULL_OCC)
   __syncthreads();
   const uint32_t chunk = 256 * kPV;
   for (uint32_t base = blockIdx.x * chunk; base < nul; base += gridDim.x * chunk) {
+#if MG_PULL_PF
+    // bulk-prefetch the CTA's next chunk into L2 (one TMA prefetch per CTA):
+    // the records themselves without a list (contiguous), the list otherwise
+    if (threadIdx.x == 0) {
+      const uint32_t nx = base + gridDim.x * chunk;
+      if (nx < nul) {
+        const uint32_t n = nul - nx < chunk ? nul - nx : chunk;
+        if (!ul)
+          asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(rec + nx), "r"(n * 16u)
+                       : "memory");
+        else if ((((uintptr_t)(ul + nx)) & 15u) == 0)
+          asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(ul + nx),
+                       "r"((n * 4u + 15u) & ~15u)
+                       : "memory");
+      }
+    }
+#endif
     uint32_t pos[kPV];
     uint4 r[kPV];
 #pragma unroll
@@ -536,7 +560,7 @@ __global__ void __launch_bounds__(256, MG_PULL_OCC)
 
     if constexpr (kEmit) warp_queue_append<kPV>(q_found, found, vv);
     warp_queue_append<kPV>(q_keep, keep, pos);
-    if constexpr (kPullMid == 0) {
+    if constexpr (!kInline1b) {
       warp_queue_append<kPV>(q_long, lng, pos);
     } else {
       // stage 1b: the warp compacts its unsettled rows and spreads them over
@@ -627,9 +651,9 @@ __global__ void __launch_bounds__(256, MG_PULL_OCC)
     __syncthreads();
     if (threadIdx.x == 0 && s_found) atomicAdd(&ctr->out_cnt, s_found);
   }
-  warp_add_u64(scanned_out, scanned);
-  warp_add_u64(&ctr->u[2], opened);
-  if (deg_out) warp_add_u64(deg_out, degs);
+  unsigned long long* const dst[3] = {scanned_out, &ctr->u[2], deg_out};
+  const uint64_t val[3] = {scanned, opened, degs};
+  block_add_u64<3>(dst, val);
 }
 
 // pull step, stage 2: rows longer than the record, 8 lanes per vertex from arc
@@ -660,6 +684,8 @@ __global__ void __launch_bounds__(256)
   unsigned long long degs = 0;
   __shared__ uint32_t s_found;
   const uint32_t nl = *long_cnt;
+  // CTAs past the queue leave at once (an empty stage used to cost ~5 us)
+  if (blockIdx.x * (256 / kPullGroup * kGroupIters) >= nl) return;
   const unsigned lane = threadIdx.x & 31u;
   const unsigned sub = lane & (kPullGroup - 1);
   const unsigned gbase = lane & ~(kPullGroup - 1);
@@ -755,8 +781,9 @@ __global__ void __launch_bounds__(256)
     __syncthreads();
     if (threadIdx.x == 0 && s_found) atomicAdd(&ctr->out_cnt, s_found);
   }
-  warp_add_u64(scanned_out, scanned);
-  if (deg_out) warp_add_u64(deg_out, degs);
+  unsigned long long* const dst[2] = {scanned_out, deg_out};
+  const uint64_t val[2] = {scanned, degs};
+  block_add_u64<2>(dst, val);
 }
 
 // frontier list = vis & ~prev (the vertices discovered in the previous
@@ -1092,8 +1119,10 @@ struct DobfsPrim : PrimBase {
                  w.su32[3].ptr, next_label, mark_preds ? 1 : 0, c.owner_view(), emit ? 1 : 0,
                  w.output.ptr, w.ul_buf[dst].ptr, ulcnt, w.ul_buf[2].ptr, cnts + 1, c.ctr(),
                  scanned, deg_out, DobfsDyn{nullptr, nullptr, nullptr});
+      uint32_t* gq = w.ul_buf[2].ptr;  // cooperative-stage input
+      uint32_t* gq_cnt = cnts + 1;
       MGB_LAUNCH(dobfs_pull_group_kernel, num_sms() * 8, 256, 0, w.stream, w.graph(),
-                 w.pull_rec.ptr, w.ul_buf[2].ptr, cnts + 1, w.su32[0].ptr, w.su32[1].ptr,
+                 w.pull_rec.ptr, gq, gq_cnt, w.su32[0].ptr, w.su32[1].ptr,
                  w.su32[2].ptr, w.su32[3].ptr, next_label, mark_preds ? 1 : 0, c.owner_view(),
                  emit ? 1 : 0, w.output.ptr, w.ul_buf[dst].ptr, ulcnt, c.ctr(), scanned, deg_out,
                  DobfsDyn{nullptr, nullptr, nullptr});
@@ -1371,8 +1400,10 @@ class DobfsGraphRunner {
                w.su32[0].ptr, w.su32[1].ptr, w.su32[2].ptr, w.su32[3].ptr, 0u, mp, ow, 0,
                w.loop_front[1].ptr, nullptr, &ctr->misc, w.ul_buf[2].ptr, cnts + 1, ctr,
                (unsigned long long*)nullptr, &ctr->next_deg, dyn);
+    uint32_t* gq = w.ul_buf[2].ptr;
+    uint32_t* gq_cnt = cnts + 1;
     MGB_LAUNCH(dobfs_pull_group_kernel, num_sms() * 8, 256, 0, s, gv, w.pull_rec.ptr,
-               w.ul_buf[2].ptr, cnts + 1, w.su32[0].ptr, w.su32[1].ptr, w.su32[2].ptr,
+               gq, gq_cnt, w.su32[0].ptr, w.su32[1].ptr, w.su32[2].ptr,
                w.su32[3].ptr, 0u, mp, ow, 0, w.loop_front[1].ptr, nullptr, &ctr->misc, ctr,
                (unsigned long long*)nullptr, &ctr->next_deg, dyn);
     MGB_CUDA(cudaStreamEndCapture(s, &tmp));
