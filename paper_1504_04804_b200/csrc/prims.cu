@@ -444,8 +444,11 @@ __device__ __forceinline__ void warp_set_bits_smem(uint32_t* bits, uint32_t* win
   const uint32_t pw = __shfl_up_sync(0xffffffffu, in ? wd : 0xFFFFFFFFu, 1);
   const unsigned firsts = __ballot_sync(0xffffffffu, in && (lane == 0 || pw != wd));
   if ((firsts >> lane) & 1u) {
-    atomicOr(&bits[wd], win[idx]);
-    win[idx] = 0u;
+    // exchange, not read-then-clear: lanes of one word that are not adjacent
+    // (a lane outside the window between them) both flush, and the second
+    // then finds 0 (compute-sanitizer racecheck clean)
+    const uint32_t m = atomicExch(&win[idx], 0u);
+    if (m) atomicOr(&bits[wd], m);
   }
   __syncwarp();
 }
@@ -792,21 +795,38 @@ __global__ void __launch_bounds__(256)
 __global__ void __launch_bounds__(256)
     bitmap_diff_list_kernel(const uint32_t* __restrict__ vis, const uint32_t* __restrict__ prev,
                             uint32_t nw, uint32_t* out, uint32_t* cnt) {
-  using Scan = cub::BlockScan<uint32_t, 256>;
-  __shared__ typename Scan::TempStorage tmp;
+  __shared__ uint32_t s_warp[8];
   __shared__ uint32_t s_base;
+  const uint32_t lane = lane_id(), warp = threadIdx.x >> 5;
   for (uint32_t base = blockIdx.x * 256; base < nw; base += gridDim.x * 256) {
     const uint32_t i = base + threadIdx.x;
     uint32_t d = i < nw ? (__ldg(&vis[i]) & ~__ldg(&prev[i])) : 0u;
-    uint32_t excl, total;
-    Scan(tmp).ExclusiveSum((uint32_t)__popc(d), excl, total);
-    if (threadIdx.x == 0) s_base = total ? atomicAdd(cnt, total) : 0u;
+    // CTA exclusive scan of the popcounts: warp shuffles, then the 8 warp sums
+    const uint32_t c = __popc(d);
+    uint32_t x = c;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+      if (lane >= (uint32_t)o) x += y;
+    }
+    if (lane == 31) s_warp[warp] = x;
     __syncthreads();
-    uint32_t o = s_base + excl;
+    if (threadIdx.x == 0) {
+      uint32_t run = 0;
+      for (int k = 0; k < 8; ++k) {
+        const uint32_t t = s_warp[k];
+        s_warp[k] = run;
+        run += t;
+      }
+      s_base = run ? atomicAdd(cnt, run) : 0u;
+    }
+    __syncthreads();
+    uint32_t o = s_base + s_warp[warp] + x - c;
     while (d) {
       out[o++] = i * 32 + (__ffs(d) - 1);
       d &= d - 1;
     }
+    __syncwarp();
     __syncthreads();
   }
 }
@@ -870,6 +890,7 @@ __global__ void dobfs_loop_decide_kernel(DobfsLoop* st, DobfsHist* hist,
   st->physical = phys;
   hist[t].dir = st->dir;
   hist[t].physical = phys;
+  hist[t].pad = 0u;
   if (!phys) st->in_count = 0;  // the push recounts its list from the bitmap
   cudaGraphSetConditional(h_pull, phys);
   cudaGraphSetConditional(h_push, phys ? 0u : 1u);
