@@ -368,6 +368,7 @@ class RunStats:
         self.exchange_ms = st.exchange_ms
         self.device_ms = st.device_ms
         self.gpu_launches = st.gpu_launches
+        self.device_loop = bool(st.device_loop)  # supersteps ran as one CUDA graph
         self.exchange_bytes = st.exchange_bytes
         self.stop_reason = STOP_REASONS[st.stop_reason]
         self.communication = "broadcast" if st.communication == MG_COMM_BROADCAST else "selective"

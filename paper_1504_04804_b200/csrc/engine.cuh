@@ -229,9 +229,11 @@ __global__ void __launch_bounds__(256)
 // fence makes the record stores visible before the count (P2P over NVLink)
 // (multi-process, device protocol: then raise this superstep's publish flag
 // in every peer's mailbox once all counts are out)
+// (epoch_dev: the device-driven loop keeps the epoch in device memory)
 static __global__ void publish_kernel(const Counters* ctr, uint32_t* const* cnt_ptr, uint32_t n,
                                       uint32_t p, Mailbox* const* mbox, uint32_t parity,
-                                      uint32_t epoch) {
+                                      uint32_t epoch, const uint32_t* epoch_dev = nullptr) {
+  if (epoch_dev) epoch = *epoch_dev;
   uint32_t d = threadIdx.x;
   __threadfence_system();
   if (d < n && d != p) *cnt_ptr[d] = ctr->send_cnt[d] < 0xFFFFFFFFu ? ctr->send_cnt[d] : 0u;
@@ -247,7 +249,9 @@ constexpr long long kSpinCycles = 120000000000ll;
 // multi-process, device protocol: the merge may start once every peer raised
 // its publish flag for this superstep (replaces the host barrier, E:922)
 static __global__ void mp_wait_pub_kernel(Mailbox* mine, uint32_t parity, uint32_t epoch,
-                                          uint32_t n, uint32_t me, uint32_t* err) {
+                                          uint32_t n, uint32_t me, uint32_t* err,
+                                          const uint32_t* epoch_dev = nullptr) {
+  if (epoch_dev) epoch = *epoch_dev;
   const uint32_t q = threadIdx.x;
   if (q < n && q != me) {
     const volatile uint32_t* f = &mine->pub[parity][q];
@@ -277,7 +281,9 @@ struct HostReportPart {
 // (E:784-820) without a host barrier
 static __global__ void mp_report_kernel(Counters* ctr, Counters* host_ctr, HostReportPart hp,
                                         Mailbox* const* mbox, uint32_t n, uint32_t me,
-                                        uint32_t epoch, DevReport* host_out, uint32_t* err) {
+                                        uint32_t epoch, DevReport* host_out, uint32_t* err,
+                                        const uint32_t* epoch_dev = nullptr) {
+  if (epoch_dev) epoch = *epoch_dev;
   const uint32_t slot = epoch & 1u;
   if (threadIdx.x == 0) {
     DevReport r;
@@ -303,11 +309,11 @@ static __global__ void mp_report_kernel(Counters* ctr, Counters* host_ctr, HostR
       *reinterpret_cast<volatile uint32_t*>(&mbox[d]->rep[slot][me].epoch) = epoch;
   }
   __syncthreads();
-  {  // own counters to the host, cleared for the next superstep
+  {  // own counters to the host (unless null), cleared for the next superstep
     uint32_t* src = reinterpret_cast<uint32_t*>(ctr);
     volatile uint32_t* dst = reinterpret_cast<volatile uint32_t*>(host_ctr);
     for (uint32_t i = threadIdx.x; i < sizeof(Counters) / 4; i += blockDim.x) {
-      dst[i] = src[i];
+      if (dst) dst[i] = src[i];
       src[i] = 0u;
     }
   }
@@ -325,6 +331,7 @@ static __global__ void mp_report_kernel(Counters* ctr, Counters* host_ctr, HostR
   }
   __threadfence();
   __syncthreads();
+  if (!host_out) return;
   const uint32_t words = n * (uint32_t)(sizeof(DevReport) / 4);
   const volatile uint32_t* src = reinterpret_cast<const volatile uint32_t*>(mbox[me]->rep[slot]);
   volatile uint32_t* dst = reinterpret_cast<volatile uint32_t*>(host_out);
@@ -338,7 +345,11 @@ __global__ void __launch_bounds__(256)
     merge_kernel(F f, const SlotView* __restrict__ slots, const uint32_t* __restrict__ inbox_cnt,
                  uint32_t p, uint32_t stamp, uint32_t iteration, uint32_t* merge_stamp,
                  uint32_t* __restrict__ next, Counters* ctr, GraphView g, int nva, int nvv,
-                 int enqueue, int want_deg) {
+                 int enqueue, int want_deg, const uint32_t* iter_dev = nullptr) {
+  if (iter_dev) {  // device-driven loop: the superstep index lives in device memory
+    iteration = *iter_dev;
+    stamp = iteration + 1;
+  }
   const uint32_t src = blockIdx.y;
   if (src == p) return;
   const uint32_t cnt = inbox_cnt[src];
@@ -382,7 +393,12 @@ __global__ void __launch_bounds__(256)
     merge_dense_kernel(F f, DenseView dv, const SlotView* __restrict__ slots,
                        const uint32_t* __restrict__ inbox_cnt, uint32_t p, uint32_t stamp,
                        uint32_t iteration, uint32_t* merge_stamp, uint32_t* __restrict__ next,
-                       Counters* ctr, GraphView g, int want_deg) {
+                       Counters* ctr, GraphView g, int want_deg,
+                       const uint32_t* iter_dev = nullptr) {
+  if (iter_dev) {
+    iteration = *iter_dev;
+    stamp = iteration + 1;
+  }
   constexpr int A = AssocCap<F>::value;
   const uint32_t src = blockIdx.y;
   if (src == p) return;
@@ -631,6 +647,30 @@ auto with_dev(Prim& prim, Ctx& c, Fn&& fn) -> decltype(prim.dev32(c), void()) {
 }
 
 // ---------------------------------------------------------------------------
+// device-driven superstep loop (a primitive may run the whole loop as one
+// CUDA graph; the enactor then rebuilds its statistics from the history)
+struct DeviceLoopOut {
+  uint32_t supersteps = 0;
+  int stop_reason = MG_STOP_FRONTIERS_EMPTY;
+  std::vector<uint64_t> out, next, edges, combine;
+  std::vector<std::vector<uint64_t>> h_src;     // per superstep: records sent by each worker
+  std::vector<std::vector<uint64_t>> h_matrix;  // [src][dst] totals
+  uint64_t wire = 0, xbytes = 0;
+};
+
+template <class Prim>
+auto try_device_loop(Prim& prim, Plan& P, std::vector<Ctx>& ctx, RunState& rs,
+                     const mg_config& cfg, DeviceLoopOut& o, int)
+    -> decltype(prim.device_loop(P, ctx, rs, cfg, o)) {
+  return prim.device_loop(P, ctx, rs, cfg, o);
+}
+template <class Prim>
+bool try_device_loop(Prim&, Plan&, std::vector<Ctx>&, RunState&, const mg_config&,
+                     DeviceLoopOut&, long) {
+  return false;
+}
+
+// ---------------------------------------------------------------------------
 // the enactor
 
 // MG_TRACE_HOST=1: host timestamps of the enactor's phases on stderr
@@ -764,7 +804,30 @@ void run_primitive(Plan& P, Prim& prim, const mg_config& cfg) {
     }
   }
 
-  for (uint64_t iter = 0;; ++iter) {
+  DeviceLoopOut dlo;
+  const bool on_device = try_device_loop(prim, P, ctx, rs, cfg, dlo, 0);
+  if (on_device) {
+    for (uint32_t t = 0; t < dlo.supersteps; ++t) {
+      GlobalView v;
+      v.iteration = t;
+      v.num_workers = n;
+      v.reports.resize(n);
+      v.total_out = dlo.out[t];
+      v.total_next = dlo.next[t];
+      rs.views.push_back(std::move(v));
+      P.out_per_iter.push_back(dlo.out[t]);
+      P.h_per_iter.push_back(dlo.h_src[t]);
+      P.edges_per_iter.push_back(dlo.edges[t]);
+      P.combine_per_iter.push_back(dlo.combine[t]);
+      total_edges += dlo.edges[t];
+      total_combine += dlo.combine[t];
+    }
+    P.h_matrix = dlo.h_matrix;
+    wire = dlo.wire * inflation;
+    xbytes = dlo.xbytes;
+    stop_reason = dlo.stop_reason;
+  }
+  for (uint64_t iter = 0; !on_device; ++iter) {
     const GlobalView* prev = rs.views.empty() ? nullptr : &rs.views.back();
     const uint32_t parity = iter & 1u;
     if (dev_fabric) ++P.mp_epoch;  // same sequence on every rank (same decisions)
@@ -1036,6 +1099,7 @@ void run_primitive(Plan& P, Prim& prim, const mg_config& cfg) {
   st.kernel2_ms = P.prof2_ms;
   st.kernel2_launches = P.prof2_launches;
   st.kernel2_bytes = P.prof2_bytes;
+  st.device_loop = on_device ? 1 : 0;
   collect_buffer_stats(P);
 }
 

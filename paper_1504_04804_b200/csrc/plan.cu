@@ -48,6 +48,8 @@ static void free_worker(Worker& w) {
   for (auto& a : w.ul_buf) a.free_();
   for (int i = 0; i < 2; ++i)
     if (w.loop_exec[i]) cudaGraphExecDestroy(w.loop_exec[i]);
+  if (w.mp_exec) cudaGraphExecDestroy(w.mp_exec);
+  w.mp_state.free_(); w.mp_hist.free_();
   if (w.loop_host) cudaFreeHost(w.loop_host);
   if (w.loop_hist_host) cudaFreeHost(w.loop_hist_host);
   w.loop_state.free_(); w.loop_hist.free_(); w.loop_front[0].free_(); w.loop_front[1].free_();

@@ -156,6 +156,12 @@ struct Worker {
   cudaGraphExec_t loop_exec[2] = {nullptr, nullptr};  // by mark_preds
   uint32_t loop_n_pull[2] = {0, 0}, loop_n_push[2] = {0, 0};
   std::vector<const void*> loop_ptrs[2];  // device pointers each graph captured
+  // device-driven DOBFS across processes (one partition per rank): loop state,
+  // history and the instantiated graph
+  DevArray<uint8_t> mp_state, mp_hist;
+  cudaGraphExec_t mp_exec = nullptr;
+  uint32_t mp_n_pull = 0, mp_n_push = 0, mp_n_fixed = 0;  // kernels per branch / superstep
+  std::vector<const void*> mp_ptrs;
   // transpose of the sub-graph (in-arcs from hosted vertices), rows sorted by
   // source; built once per plan for the pull-form PageRank accumulation
   DevArray<uint32_t> toff, tcol, tlong;

@@ -1196,6 +1196,10 @@ struct DobfsPrim : PrimBase {
     MGB_LAUNCH(dobfs_share_kernel, 1, 1, 0, c.w->stream, c.ctr(), pulled_ ? 1 : 0,
                ul_len[c.w->p]);
   }
+  // several processes (one partition per rank, device fabric): the whole
+  // superstep loop as one CUDA graph per rank (DobfsMpGraphRunner below)
+  bool device_loop(Plan& P, std::vector<Ctx>& ctx, RunState& rs, const mg_config& cfg,
+                   DeviceLoopOut& o);
   std::vector<bool> pending_ul_ = std::vector<bool>(kMaxWorkers, false);
   std::vector<bool> list_free;  // per worker: last pull step counted, did not list
   std::vector<bool> prof_pending_ = std::vector<bool>(kMaxWorkers, false);
@@ -1464,6 +1468,450 @@ class DobfsGraphRunner {
     return {w.loop_exec[gi], w.loop_n_pull[gi], w.loop_n_push[gi]};
   }
 };
+
+// ---------------------------------------------------------------------------
+// Device-driven DOBFS across processes (one GPU and one partition per rank,
+// the device fabric of engine.cuh).  Every superstep of the enactor —
+//   decide   the reference direction rule (primitives.cpp:197-205) on the
+//            global quantities, and the exact-cost physical choice on the sums
+//            all ranks reported last superstep (u[0], u[1]), in the same double
+//            arithmetic as the host path
+//   IF pull  frontier_diff, pull thread + cooperative stages (discoveries listed)
+//   IF push  prev = visited, edge-balanced advance from the input frontier
+//   split + pack (discovery bitmap or records into the peers' inboxes),
+//   publish, wait for the peers' publish flags, merge (records + dense),
+//   report all-gather through the mailboxes, end (global sums, history,
+//   convergence: Σ next frontiers == 0, E:784-820)
+// — runs inside ONE graph launch: a WHILE node whose body holds two
+// supersteps (even / odd, so the frontier ping-pong buffers and the inbox
+// parity are fixed in each), the second behind an IF on "not converged".  No
+// superstep waits for the host; every rank takes the same decisions from the
+// same all-gathered reports.  Results and statistics equal the host loop's
+// (tests/test_fabric.py::test_dobfs_device_loop_*).
+constexpr uint32_t kMpHist = 65536;
+constexpr uint32_t kMpMaxRanks = 8;  // history keeps an n x n send matrix per superstep
+
+struct DobfsMpLoop {
+  DobfsLoop b;  // first: the pull / frontier kernels read it as a DobfsLoop
+  uint32_t n, me, epoch, overflow;
+  uint32_t own_next;               // this rank's next frontier (global discoveries)
+  unsigned long long own_next_deg;
+};
+struct DobfsMpHist {
+  uint32_t dir, physical;
+  unsigned long long out, next, edges, combine;
+  uint32_t send[kMpMaxRanks][kMpMaxRanks];  // [src][dst], kDenseFlag kept
+};
+
+__global__ void dobfs_mp_init_kernel(DobfsMpLoop* st, uint32_t* labels, uint32_t* vis) {
+  (void)labels;
+  (void)vis;
+  DobfsLoop& b = st->b;
+  b.iter = 0;
+  b.dir = 0;
+  b.switched = 0;
+  b.physical = 0;
+  b.ul_src = 2;  // every non-isolated record, no list
+  b.ul_len = b.n_nonisolated;
+  b.visited = 1;
+  st->overflow = 0;
+}
+
+__global__ void dobfs_mp_decide_kernel(DobfsMpLoop* st, DobfsMpHist* hist, const Mailbox* mine,
+                                       cudaGraphConditionalHandle h_pull,
+                                       cudaGraphConditionalHandle h_push) {
+  DobfsLoop& b = st->b;
+  const uint32_t t = b.iter;
+  st->epoch += 1;  // the host loop's ++mp_epoch at the top of a superstep
+  if (t >= 1) {    // primitives.cpp:197-205, as DobfsPrim::body
+    b.visited += b.in_count;
+    const double fv = b.nv > 0 ? (double)b.in_count * b.ne_d / b.nv_d : 0.0;
+    const double bv = b.visited > 0 ? (double)((unsigned long long)b.nv - b.visited) * b.nv_d /
+                                          (double)b.visited
+                                    : 0.0;
+    uint32_t next;
+    if (b.dir == 0) next = (!b.switched && fv > bv * b.do_a) ? 1u : 0u;
+    else next = fv < bv * b.do_b ? 0u : 1u;
+    if (next == 1 && b.dir == 0) b.switched = 1;
+    b.dir = next;
+  }
+  uint32_t phys = b.dir == 1;
+  if (b.dir == 0 && b.exact && t > 0) {
+    // the sums every rank reported last superstep (slot of epoch - 1)
+    const uint32_t ps = (st->epoch - 1) & 1u;
+    unsigned long long gw = 0, gul = 0;
+    for (uint32_t q = 0; q < st->n; ++q) {
+      const volatile DevReport* r = &mine->rep[ps][q];
+      gw += r->u[1];
+      gul += r->u[0];
+    }
+    phys = (double)gw > b.pull_ratio * (double)gul;
+  }
+  b.physical = phys;
+  hist[t].dir = b.dir;
+  hist[t].physical = phys;
+  cudaGraphSetConditional(h_pull, phys);
+  cudaGraphSetConditional(h_push, phys ? 0u : 1u);
+}
+
+// before the report clears the counters: keep what the next superstep needs,
+// and share the exact-cost inputs (dobfs_share_kernel)
+__global__ void dobfs_mp_pre_report_kernel(DobfsMpLoop* st, Counters* ctr) {
+  DobfsLoop& b = st->b;
+  st->own_next = ctr->next_cnt;
+  st->own_next_deg = ctr->next_deg;
+  if (b.exact) {
+    ctr->u[0] = b.physical ? ctr->misc : b.ul_len;
+    ctr->u[1] = ctr->next_deg;
+  }
+  if (b.physical) {  // the pull compacted the unvisited list (ping-pong)
+    b.ul_len = ctr->misc;
+    b.ul_src = b.ul_src == 0 ? 1 : 0;
+  }
+}
+
+__global__ void dobfs_mp_end_kernel(DobfsMpLoop* st, const Mailbox* mine, DobfsMpHist* hist,
+                                    const uint32_t* err, cudaGraphConditionalHandle h_next,
+                                    cudaGraphConditionalHandle h_while) {
+  DobfsLoop& b = st->b;
+  const uint32_t t = b.iter, slot = st->epoch & 1u, n = st->n;
+  unsigned long long out = 0, next = 0, edges = 0, comb = 0;
+  uint32_t ovf = 0;
+  DobfsMpHist& h = hist[t];
+  for (uint32_t q = 0; q < n; ++q) {
+    const volatile DevReport* r = &mine->rep[slot][q];
+    out += r->out_frontier;
+    next += r->next_frontier;
+    edges += r->edges_delta;
+    comb += r->combine_delta;
+    ovf |= r->overflow;
+    for (uint32_t d = 0; d < kMpMaxRanks; ++d) h.send[q][d] = d < n ? r->send_cnt[d] : 0u;
+  }
+  h.out = out;
+  h.next = next;
+  h.edges = edges;
+  h.combine = comb;
+  b.in_count = st->own_next;
+  b.in_degsum = st->own_next_deg;
+  b.iter = t + 1;
+  st->overflow |= ovf;
+  const bool more = next > 0 && t + 1 < b.max_supersteps && t + 1 < kMpHist && !ovf &&
+                    !*reinterpret_cast<const volatile uint32_t*>(err);
+  if (h_next) cudaGraphSetConditional(h_next, more ? 1u : 0u);
+  cudaGraphSetConditional(h_while, more ? 1u : 0u);
+}
+
+class DobfsMpGraphRunner {
+ public:
+  static bool eligible(const Plan& P, const mg_config& c, bool mark_preds) {
+    const char* e = getenv("MG_MP_GRAPH_LOOP");
+    if ((e && e[0] == '0') || getenv("MG_NO_GRAPH")) return false;
+    const bool fused = c.fused == MG_FUSED_ON || (c.fused == MG_FUSED_AUTO &&
+                                                  c.policy == MG_POLICY_FUSED);
+    return P.n > 1 && P.n <= kMpMaxRanks && P.shm && P.device_fabric &&
+           P.local_workers.size() == 1 && P.dup == MG_DUP_ALL && !P.profile && !mark_preds &&
+           c.policy == MG_POLICY_MAX && fused && !c.drop_enabled && c.hard_cap_bytes == 0;
+  }
+
+  // runs the supersteps of a prepared run (run_primitive's prologue done:
+  // inboxes, send tables, init, source seeded into next_input)
+  static void run(Plan& P, DobfsPrim& prim, Ctx& c, RunState& rs, const mg_config& cfg,
+                  DeviceLoopOut& o) {
+    Worker& w = *c.w;
+    const uint32_t n = P.n, p = w.p;
+    DeviceGuard dg(w.dev);
+    // frontier buffers at their superstep bound before capture (next_input
+    // keeps the seeded source)
+    uint64_t incoming = w.nv;
+    for (uint32_t s = 0; s < n; ++s) incoming += (s == p) ? 0 : w.slot_cap[s];
+    w.output.ensure(w.nv, w.stream);
+    w.next_input.ensure(w.output.cap + incoming, w.stream, rs.next_count[p]);
+    w.input.ensure(w.output.cap + incoming, w.stream);
+    ensure_buffers(w);
+    const DenseView dv = prim.dense_view(c);
+    cudaGraphExec_t exec = graph(P, w, c, prim, dv);
+    DobfsMpLoop h{};
+    DobfsLoop& b = h.b;
+    b.nv_d = (double)P.nv;
+    b.ne_d = (double)P.ne;
+    b.do_a = prim.do_a;
+    b.do_b = prim.do_b;
+    b.pull_ratio = pull_ratio();
+    b.nv = P.nv;
+    b.source = prim.source;
+    b.max_supersteps = (uint32_t)(cfg.max_supersteps < kMpHist ? cfg.max_supersteps : kMpHist);
+    b.exact = prim.exact_cost ? 1u : 0u;
+    b.n_nonisolated = w.n_nonisolated;
+    b.in_count = rs.next_count[p];
+    b.in_degsum = 0;
+    h.n = n;
+    h.me = P.rank;
+    h.epoch = P.mp_epoch;
+    DobfsMpLoop* st = reinterpret_cast<DobfsMpLoop*>(w.mp_state.ptr);
+    MGB_CUDA(cudaMemcpyAsync(st, &h, sizeof(h), cudaMemcpyHostToDevice, w.stream));
+    MGB_LAUNCH(dobfs_mp_init_kernel, 1, 1, 0, w.stream, st, w.su32[0].ptr, w.su32[2].ptr);
+    MGB_CUDA(cudaGraphLaunch(exec, w.stream));
+    MGB_CUDA(cudaMemcpyAsync(&h, st, sizeof(h), cudaMemcpyDeviceToHost, w.stream));
+    MGB_CUDA(cudaStreamSynchronize(w.stream));
+    if (*reinterpret_cast<volatile uint32_t*>(P.host_reports + kMaxMpRanks))
+      throw Error(MG_EWORKER, "fabric: a peer rank did not arrive within the timeout");
+    if (h.overflow) throw Error(MG_EWORKER, "inbox overflow on a peer worker");
+    const uint32_t S = b.iter;
+    std::vector<DobfsMpHist> hist(S);
+    MGB_CUDA(cudaMemcpy(hist.data(), w.mp_hist.ptr, sizeof(DobfsMpHist) * S,
+                        cudaMemcpyDeviceToHost));
+    if (S && hist[S - 1].next && S >= kMpHist && cfg.max_supersteps > kMpHist)
+      throw Error(MG_EWORKER, "dobfs: the device-driven loop records at most 65536 supersteps "
+                              "(MG_MP_GRAPH_LOOP=0 runs the host loop)");
+    P.mp_epoch = h.epoch;
+    // statistics in the enactor's shapes
+    o.supersteps = S;
+    o.h_matrix.assign(n, std::vector<uint64_t>(n, 0));
+    const uint64_t rec_bytes = 4ull + 4ull * prim.nva + 8ull * prim.nvv;
+    const uint64_t dense_bytes = 4ull * (dv.kind ? dv.words : 0);
+    uint64_t launches = 2;  // init + graph
+    for (uint32_t t = 0; t < S; ++t) {
+      const DobfsMpHist& e = hist[t];
+      prim.dir_log.push_back((int)e.dir);
+      if (e.physical && e.dir == 0) ++prim.physical_pull_steps;
+      o.out.push_back(e.out);
+      o.next.push_back(e.next);
+      o.edges.push_back(e.edges);
+      o.combine.push_back(e.combine);
+      std::vector<uint64_t> hs(n, 0);
+      for (uint32_t q = 0; q < n; ++q)
+        for (uint32_t d = 0; d < n; ++d) {
+          if (d == q) continue;
+          const uint32_t raw = e.send[q][d];
+          const uint64_t len = raw & ~kDenseFlag;
+          o.h_matrix[q][d] += len;
+          hs[q] += len;
+          o.wire += len;
+          if (q == P.rank) o.xbytes += (raw & kDenseFlag) ? dense_bytes : len * rec_bytes;
+        }
+      o.h_src.push_back(hs);
+      launches += w.mp_n_fixed + (e.physical ? w.mp_n_pull : w.mp_n_push);
+    }
+    o.stop_reason = (S && hist[S - 1].next == 0) ? MG_STOP_FRONTIERS_EMPTY
+                                                 : MG_STOP_MAX_SUPERSTEPS;
+    g_launches.fetch_add(launches, std::memory_order_relaxed);
+  }
+
+ private:
+  static void ensure_buffers(Worker& w) {
+    if (!w.mp_state.ptr) w.mp_state.alloc(sizeof(DobfsMpLoop));
+    if (!w.mp_hist.ptr) w.mp_hist.alloc(sizeof(DobfsMpHist) * kMpHist);
+    const uint64_t nw = (w.nv + 31) / 32 + 1;
+    if (w.su32[3].n < nw || !w.su32[3].ptr) w.su32[3].alloc(nw);  // frontier bitmap
+    if (w.aux[2].n < 4 || !w.aux[2].ptr) w.aux[2].alloc(4);
+    // advance scratch for an input of up to the frontier buffer's capacity
+    const uint64_t cap = w.input.cap > 1 ? w.input.cap : 1;
+    if (w.loop_lb_row.n < cap) w.loop_lb_row.alloc(cap);
+    if (w.loop_lb_pref.n < cap) w.loop_lb_pref.alloc(cap);
+    if (w.loop_lb_bsum.n < cap / kLbBlock + 4) w.loop_lb_bsum.alloc(cap / kLbBlock + 4);
+    if (!w.loop_total.ptr) w.loop_total.alloc(1);
+    const uint64_t tiles = (2 * w.ne + 1) / kTile + 2 + kMinTiles + 1;
+    if (w.loop_tiles.n < tiles) w.loop_tiles.alloc(tiles);
+  }
+
+  static std::vector<const void*> pointers(const Plan& P, const Worker& w) {
+    return {w.su32[0].ptr, w.su32[2].ptr, w.su32[3].ptr, w.aux[2].ptr, w.aux[4].ptr,
+            w.ul_buf[0].ptr, w.ul_buf[1].ptr, w.ul_buf[2].ptr, w.pull_rec.ptr, w.off.ptr,
+            w.col.ptr, w.owner.ptr, w.ctr.ptr, w.mp_state.ptr, w.mp_hist.ptr, w.input.ptr,
+            w.next_input.ptr, w.output.ptr, w.send_table.ptr, w.send_cnt_ptr.ptr,
+            w.recv_table.ptr, w.inbox_cnt.ptr, w.merge_stamp.ptr, w.loop_lb_row.ptr,
+            w.loop_lb_pref.ptr, w.loop_lb_bsum.ptr, w.loop_total.ptr, w.loop_tiles.ptr,
+            P.mbox.ptr, P.mbox_ptrs.ptr, P.host_reports_dev,
+            reinterpret_cast<const void*>((uintptr_t)P.n)};
+  }
+  // ... plus the slot capacities (merge grids) and the output capacity (split grid)
+  static std::vector<const void*> signature(const Plan& P, const Worker& w) {
+    std::vector<const void*> v = pointers(P, w);
+    for (uint64_t c : w.slot_cap) v.push_back(reinterpret_cast<const void*>((uintptr_t)c));
+    v.push_back(reinterpret_cast<const void*>((uintptr_t)w.output.cap));
+    return v;
+  }
+
+  // the leaf nodes of an ongoing capture (to hang the next node on)
+  static std::vector<cudaGraphNode_t> leaves(cudaStream_t s) {
+    cudaStreamCaptureStatus cs;
+    const cudaGraphNode_t* deps = nullptr;
+    size_t nd = 0;
+    MGB_CUDA(cudaStreamGetCaptureInfo(s, &cs, nullptr, nullptr, &deps, &nd));
+    return std::vector<cudaGraphNode_t>(deps, deps + nd);
+  }
+
+  // one superstep at a fixed parity into graph g; returns its leaf nodes
+  static std::vector<cudaGraphNode_t> substep(Plan& P, Worker& w, Ctx& c, const DenseView& dv,
+                                              bool st_exact, cudaGraph_t g, int parity,
+                                              cudaGraphConditionalHandle h_next,
+                                              cudaGraphConditionalHandle h_while,
+                                              uint64_t& n_pull, uint64_t& n_push,
+                                              uint64_t& n_fixed) {
+    cudaStream_t s = w.stream;
+    const uint32_t n = P.n, p = w.p;
+    const uint64_t nw = (w.nv + 31) / 32 + 1;
+    DobfsMpLoop* st = reinterpret_cast<DobfsMpLoop*>(w.mp_state.ptr);
+    DobfsMpHist* hist = reinterpret_cast<DobfsMpHist*>(w.mp_hist.ptr);
+    Mailbox* mine = reinterpret_cast<Mailbox*>(P.mbox.ptr);
+    uint32_t* err = reinterpret_cast<uint32_t*>(P.host_reports_dev + kMaxMpRanks);
+    Counters* ctr = w.ctr.ptr;
+    uint32_t* cnts = w.aux[2].ptr;
+    GraphView gv = w.graph();
+    OwnerView ow = c.owner_view();
+    // even supersteps read input A and fill B, odd ones the reverse
+    // (A = the buffer the prologue seeded: next_input)
+    uint32_t* in = parity == 0 ? w.next_input.ptr : w.input.ptr;
+    uint32_t* nxt = parity == 0 ? w.input.ptr : w.next_input.ptr;
+    DobfsDev f{w.su32[0].ptr, w.su32[1].ptr, w.su32[2].ptr, w.su32[3].ptr, ow, 0u, 0,
+               &st->b.iter};
+    cudaGraphConditionalHandle h_pull, h_push;
+    MGB_CUDA(cudaGraphConditionalHandleCreate(&h_pull, g, 0, cudaGraphCondAssignDefault));
+    MGB_CUDA(cudaGraphConditionalHandleCreate(&h_push, g, 0, cudaGraphCondAssignDefault));
+    cudaGraph_t tmp;
+    const uint64_t l0 = g_launches.load();
+    // decide
+    MGB_CUDA(cudaStreamBeginCaptureToGraph(s, g, nullptr, nullptr, 0, cudaStreamCaptureModeRelaxed));
+    MGB_LAUNCH(dobfs_mp_decide_kernel, 1, 1, 0, s, st, hist, mine, h_pull, h_push);
+    std::vector<cudaGraphNode_t> dec = leaves(s);
+    MGB_CUDA(cudaStreamEndCapture(s, &tmp));
+    cudaGraphNode_t ifs[2];
+    cudaGraph_t bodies[2];
+    cudaGraphConditionalHandle hs[2] = {h_pull, h_push};
+    for (int i = 0; i < 2; ++i) {
+      cudaGraphNodeParams ip = {};
+      ip.type = cudaGraphNodeTypeConditional;
+      ip.conditional.handle = hs[i];
+      ip.conditional.type = cudaGraphCondTypeIf;
+      ip.conditional.size = 1;
+      MGB_CUDA(cudaGraphAddNode(&ifs[i], g, dec.data(), dec.size(), &ip));
+      bodies[i] = ip.conditional.phGraph_out[0];
+    }
+    const uint64_t l1 = g_launches.load();
+    // pull branch: discoveries listed into output (several partitions)
+    MGB_CUDA(cudaStreamBeginCaptureToGraph(s, bodies[0], nullptr, nullptr, 0,
+                                           cudaStreamCaptureModeRelaxed));
+    DobfsDyn dyn{&st->b, w.ul_buf[0].ptr, w.ul_buf[1].ptr};
+    MGB_LAUNCH(frontier_diff_kernel, grid_for(nw, 256, num_sms() * 8), 256, 0, s, w.su32[2].ptr,
+               w.aux[4].ptr, w.su32[3].ptr, (uint32_t)nw, cnts, nullptr, 0ull, &st->b,
+               &ctr->edges);
+    MGB_LAUNCH(dobfs_pull_thread_kernel<true>, num_sms() * MG_PULL_OCC, 256, 0, s, gv,
+               w.pull_rec.ptr, nullptr, 0u, w.su32[0].ptr, w.su32[1].ptr, w.su32[2].ptr,
+               w.su32[3].ptr, 0u, 0, ow, 1, w.output.ptr, nullptr, &ctr->misc, w.ul_buf[2].ptr,
+               cnts + 1, ctr, (unsigned long long*)nullptr, (unsigned long long*)nullptr, dyn);
+    MGB_LAUNCH(dobfs_pull_group_kernel, num_sms() * 8, 256, 0, s, gv, w.pull_rec.ptr,
+               w.ul_buf[2].ptr, cnts + 1, w.su32[0].ptr, w.su32[1].ptr, w.su32[2].ptr,
+               w.su32[3].ptr, 0u, 0, ow, 1, w.output.ptr, nullptr, &ctr->misc, ctr,
+               (unsigned long long*)nullptr, (unsigned long long*)nullptr, dyn);
+    MGB_CUDA(cudaStreamEndCapture(s, &tmp));
+    const uint64_t l2 = g_launches.load();
+    // push branch: prev = visited, edge-balanced advance from the input list
+    MGB_CUDA(cudaStreamBeginCaptureToGraph(s, bodies[1], nullptr, nullptr, 0,
+                                           cudaStreamCaptureModeRelaxed));
+    MGB_CUDA(cudaMemcpyAsync(w.aux[4].ptr, w.su32[2].ptr, 4 * nw, cudaMemcpyDeviceToDevice, s));
+    const uint32_t* nin = &st->b.in_count;
+    MGB_LAUNCH(lb_degree_kernel, num_sms() * 8, kLbBlock, 0, s, w.off.ptr, in, 0u,
+               w.loop_lb_row.ptr, w.loop_lb_pref.ptr, w.loop_lb_bsum.ptr, nin);
+    MGB_LAUNCH(lb_scan_kernel, 1, 1024, 0, s, w.loop_lb_bsum.ptr, 0u, w.loop_total.ptr,
+               &ctr->edges, nin);
+    const uint64_t max_tiles = (2 * w.ne + 1) / kTile + 2 + kMinTiles;
+    MGB_LAUNCH(lb_tiles_kernel, num_sms() * 8, 256, 0, s, w.loop_lb_pref.ptr, w.loop_lb_bsum.ptr,
+               0u, w.loop_total.ptr, w.loop_tiles.ptr, (uint32_t)max_tiles, nin);
+    MGB_LAUNCH((lb_expand_kernel<DobfsDev, true>), num_sms() * 6, kExpBlock, 0, s, f, gv, in, 0u,
+               w.loop_lb_row.ptr, w.loop_lb_pref.ptr, w.loop_lb_bsum.ptr, w.loop_total.ptr,
+               w.loop_tiles.ptr, w.output.ptr, &ctr->out_cnt, nin);
+    MGB_CUDA(cudaStreamEndCapture(s, &tmp));
+    const uint64_t l3 = g_launches.load();
+    // exchange + completion, after both branches
+    MGB_CUDA(cudaStreamBeginCaptureToGraph(s, g, ifs, nullptr, 2, cudaStreamCaptureModeRelaxed));
+    // Σdeg of the next frontier, the exact-cost input (reports_deg, E:845)
+    const int want_deg = st_exact ? 1 : 0;
+    const uint64_t items = w.output.cap > dv.words ? w.output.cap : dv.words;
+    MGB_LAUNCH(split_pack_kernel<DobfsDev>, grid_for(items, 256, num_sms() * 8), 256, 0, s, f, ow,
+               gv, w.output.ptr, ctr, nxt, w.send_table.ptr + parity * n, n, 1, 0ull, 0, 0,
+               want_deg, dv);
+    MGB_LAUNCH(publish_kernel, 1, 64, 0, s, ctr, w.send_cnt_ptr.ptr + parity * n, n, p,
+               P.mbox_ptrs.ptr, (uint32_t)parity, 0u, &st->epoch);
+    MGB_LAUNCH(mp_wait_pub_kernel, 1, 32, 0, s, mine, (uint32_t)parity, 0u, n, P.rank, err,
+               &st->epoch);
+    uint64_t maxcap = 0;
+    for (uint32_t q = 0; q < n; ++q)
+      if (q != p && w.slot_cap[q] > maxcap) maxcap = w.slot_cap[q];
+    MGB_LAUNCH(merge_kernel<DobfsDev>, dim3(grid_for(maxcap, 256, num_sms() * 2), n), 256, 0, s,
+               f, w.recv_table.ptr + parity * n, w.inbox_cnt.ptr + parity * kMaxWorkers, p, 0u, 0u,
+               w.merge_stamp.ptr, nxt, ctr, gv, 0, 0, 1, want_deg, &st->b.iter);
+    if (dv.kind)
+      MGB_LAUNCH(merge_dense_kernel<DobfsDev>, dim3(grid_for(dv.words, 256, num_sms() * 2), n),
+                 256, 0, s, f, dv, w.recv_table.ptr + parity * n,
+                 w.inbox_cnt.ptr + parity * kMaxWorkers, p, 0u, 0u, w.merge_stamp.ptr, nxt, ctr,
+                 gv, want_deg, &st->b.iter);
+    MGB_LAUNCH(dobfs_mp_pre_report_kernel, 1, 1, 0, s, st, ctr);
+    MGB_LAUNCH(mp_report_kernel, 1, 128, 0, s, ctr, (Counters*)nullptr, HostReportPart{},
+               P.mbox_ptrs.ptr, n, P.rank, 0u, (DevReport*)nullptr, err, &st->epoch);
+    MGB_LAUNCH(dobfs_mp_end_kernel, 1, 1, 0, s, st, mine, hist, err, h_next, h_while);
+    std::vector<cudaGraphNode_t> out = leaves(s);
+    MGB_CUDA(cudaStreamEndCapture(s, &tmp));
+    const uint64_t l4 = g_launches.load();
+    n_pull = l2 - l1;
+    n_push = l3 - l2;
+    n_fixed = (l1 - l0) + (l4 - l3);
+    return out;
+  }
+
+  static cudaGraphExec_t graph(Plan& P, Worker& w, Ctx& c, DobfsPrim& prim,
+                               const DenseView& dv) {
+    std::vector<const void*> ptrs = signature(P, w);
+    ptrs.push_back(reinterpret_cast<const void*>((uintptr_t)(prim.exact_cost ? 1 : 0)));
+    if (w.mp_exec && w.mp_ptrs == ptrs) return w.mp_exec;
+    if (w.mp_exec) {
+      cudaGraphExecDestroy(w.mp_exec);
+      w.mp_exec = nullptr;
+    }
+    const uint64_t launches0 = g_launches.load();
+    cudaGraph_t g;
+    MGB_CUDA(cudaGraphCreate(&g, 0));
+    cudaGraphConditionalHandle h_while;
+    MGB_CUDA(cudaGraphConditionalHandleCreate(&h_while, g, 1, cudaGraphCondAssignDefault));
+    cudaGraphNodeParams wp = {};
+    wp.type = cudaGraphNodeTypeConditional;
+    wp.conditional.handle = h_while;
+    wp.conditional.type = cudaGraphCondTypeWhile;
+    wp.conditional.size = 1;
+    cudaGraphNode_t wnode;
+    MGB_CUDA(cudaGraphAddNode(&wnode, g, nullptr, 0, &wp));
+    cudaGraph_t body = wp.conditional.phGraph_out[0];
+    // even superstep, then the odd one behind IF(not converged)
+    cudaGraphConditionalHandle h_odd;
+    MGB_CUDA(cudaGraphConditionalHandleCreate(&h_odd, body, 0, cudaGraphCondAssignDefault));
+    uint64_t np, nq, nf;
+    std::vector<cudaGraphNode_t> tail =
+        substep(P, w, c, dv, prim.exact_cost, body, 0, h_odd, h_while, np, nq, nf);
+    cudaGraphNodeParams ip = {};
+    ip.type = cudaGraphNodeTypeConditional;
+    ip.conditional.handle = h_odd;
+    ip.conditional.type = cudaGraphCondTypeIf;
+    ip.conditional.size = 1;
+    cudaGraphNode_t inode;
+    MGB_CUDA(cudaGraphAddNode(&inode, body, tail.data(), tail.size(), &ip));
+    substep(P, w, c, dv, prim.exact_cost, ip.conditional.phGraph_out[0], 1, 0, h_while, np, nq,
+            nf);
+    g_launches.store(launches0);  // capture is not execution
+    MGB_CUDA(cudaGraphInstantiate(&w.mp_exec, g, 0));
+    MGB_CUDA(cudaGraphDestroy(g));
+    w.mp_ptrs = ptrs;
+    w.mp_n_pull = (uint32_t)np;
+    w.mp_n_push = (uint32_t)nq;
+    w.mp_n_fixed = (uint32_t)nf;
+    return w.mp_exec;
+  }
+};
+
+bool DobfsPrim::device_loop(Plan& P, std::vector<Ctx>& ctx, RunState& rs, const mg_config& cfg,
+                            DeviceLoopOut& o) {
+  if (!DobfsMpGraphRunner::eligible(P, cfg, mark_preds)) return false;
+  DobfsMpGraphRunner::run(P, *this, ctx[P.rank], rs, cfg, o);
+  return true;
+}
 
 // ===========================================================================
 // SSSP (primitives.cpp:307-397)

@@ -189,3 +189,71 @@ def test_three_processes_dobfs_device_fabric_and_exact_cost():
         assert o["ref"] and o["exact"], o
         assert o["ref_dir"] == o["exact_dir"] and o["ref_S"] == o["exact_S"]
     assert all(o["ref_dir"] == outs[0]["ref_dir"] for o in outs)
+
+
+def _gpu_worker_dobfs_loop(rank, world, port, q, scale):
+    """DOBFS through the device-driven superstep loop (one CUDA graph per
+    rank) and through the host loop on the same plan: everything the run
+    reports must be identical"""
+    sys.path.insert(0, ROOT)
+    try:
+        import torch.distributed as dist
+
+        import paper_1504_04804_b200 as mg
+        from oracle import seq
+        dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank,
+                                world_size=world)
+        obj = [uuid.uuid4().hex if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0)
+        g = mg.Csr.rmat(scale, 16, 2)
+        off, col, _ = g.arrays()
+        owner = mg.partition_random(g.num_vertices, world, 7)
+        mine = owner == rank
+        plan = mg.PartitionPlan.multiprocess(g, owner, world, rank, 0, obj[0])
+        out = {}
+        for exact in (False, True):
+            cfg = mg.EngineConfig(policy=mg.AllocPolicyKind.Maximum, fused=mg.FusedMode.On,
+                                  dobfs_exact_cost=exact)
+            for src in (0, 5):
+                want = seq.bfs_levels(off, col, src)
+                res = {}
+                for mode in ("0", "1", "1"):  # host loop, device loop (twice: graph reuse)
+                    os.environ["MG_MP_GRAPH_LOOP"] = mode
+                    r = mg.dobfs(plan, mg.DobfsOptions(source=src), cfg)
+                    st = r.stats
+                    res.setdefault(mode, []).append(dict(
+                        ok=bool(np.array_equal(r.labels[mine], want[mine])),
+                        dir=[int(x) for x in r.direction_log], S=int(st.supersteps),
+                        W=int(st.edges_examined), C=int(st.combine_ops),
+                        H=st.h_matrix.astype(int).tolist(),
+                        Hi=st.h_per_iter_by_src.astype(int).tolist(),
+                        out=st.out_per_iter.astype(int).tolist(),
+                        loop=bool(st.device_loop), stop=st.stop_reason,
+                        fe=int(r.forward_edges), be=int(r.backward_edges)))
+                out[f"{int(exact)}_{src}"] = res
+        del plan
+        dist.barrier()
+        dist.destroy_process_group()
+        q.put((rank, 0, out))
+    except Exception as ex:  # pragma: no cover
+        q.put((rank, 1, repr(ex)))
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("world,scale", [(2, 12), (3, 11)])
+def test_dobfs_device_loop_equals_host_loop(world, scale):
+    """the whole superstep loop on the device (decide, pull / push, pack,
+    publish, merge, report all-gather, convergence) gives the host loop's
+    labels, direction log, S, W, C, H matrix, per-iteration H and frontier
+    sizes, on every rank, for the reference schedule and the exact-cost
+    extension"""
+    res = _spawn(_gpu_worker_dobfs_loop, world, scale)
+    assert all(rc == 0 for _, rc, _ in res), res
+    for _, _, o in res:
+        for key, r in o.items():
+            host, dev = r["0"][0], r["1"]
+            assert host["ok"] and not host["loop"], (key, host)
+            for d in dev:
+                assert d["loop"], (key, d)
+                for k in ("ok", "dir", "S", "W", "C", "H", "Hi", "out", "stop", "fe", "be"):
+                    assert d[k] == host[k], (key, k, d[k], host[k])
