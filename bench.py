@@ -335,10 +335,13 @@ def run_ours(args, rank, world, local):
         mg.lib().mg_plan_set_profiling(plan._h, 1)
         e2e_call(mg, plan, sources[0], cfg, None, do_a, do_b)
         barrier()
-        acc = {"pull": [0.0, 0.0, 0], "push": [0.0, 0.0, 0], "dev_ms": 0.0}
+        acc = {"pull": [0.0, 0.0, 0], "push": [0.0, 0.0, 0], "dev_ms": 0.0, "xms": 0.0,
+               "xbytes": 0}
         for s in steps:
             st = e2e_call(mg, plan, s, cfg, None, do_a, do_b)
             acc["dev_ms"] += st.device_ms
+            acc["xms"] += st.exchange_ms
+            acc["xbytes"] += st.exchange_bytes
             for key, ms, b, n in (("pull", st.kernel_ms, st.kernel_bytes, st.kernel_launches),
                                   ("push", st.kernel2_ms, st.kernel2_bytes,
                                    st.kernel2_launches)):
@@ -393,18 +396,22 @@ def run_ours(args, rank, world, local):
                          if prof["dev_ms"] else None}}
     xchg = None
     if world > 1:
-        xa = main["xbytes"] / (main["xms"] * 1e-3) / 1e9 if main["xms"] else None
+        # the device-driven loop runs the exchange inside one graph launch, so
+        # its kernels are timed in the profiled (host-driven) pass
+        xsrc = main if main["xms"] else prof
+        xa = xsrc["xbytes"] / (xsrc["xms"] * 1e-3) / 1e9 if xsrc["xms"] else None
         xchg = {"bound": "nvlink", "kernel": "dobfs exchange pack + publish (P2P stores into "
                                              "peer inboxes)",
                 "achieved": round(xa, 1) if xa else None, "peak": NVLINK_GBS,
                 "peak_kind": "NVLink 5 nominal per direction per GPU", "unit": "GB/s",
                 "frac": round(xa / NVLINK_GBS, 4) if xa else None, "traffic": None,
-                "bytes_per_step": main["xbytes"] / args.steps,
-                "ms_per_step": round(main["xms"] / args.steps, 4),
-                "share_of_step": round(main["xms"] / main["dev_ms"], 4) if main["dev_ms"] else None,
+                "bytes_per_step": xsrc["xbytes"] / args.steps,
+                "ms_per_step": round(xsrc["xms"] / args.steps, 4),
+                "share_of_step": round(xsrc["xms"] / xsrc["dev_ms"], 4) if xsrc["dev_ms"] else None,
                 "note": "rank 0: bytes its pack kernels stored into peer inboxes / their "
                         "CUDA-event time" + (" (every rank on one GPU: HBM, not NVLink)"
-                                             if "MG_BENCH_DEVICE" in os.environ else "")}
+                                             if "MG_BENCH_DEVICE" in os.environ else "") +
+                        ("" if xsrc is main else "; timed in the profiled host-driven pass")}
     roofline = dict(xchg, hbm_kernel=hbm_roof) if xchg else hbm_roof
     dev_ms = main["dev_max_ms"]
     loop = "device (CUDA-graph loop)" if main["device_loop"] == len(steps) else \
