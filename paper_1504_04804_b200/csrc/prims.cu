@@ -779,14 +779,19 @@ __global__ void __launch_bounds__(256)
 // superstep), rebuilt for a push step that follows a list-free pull step:
 // per round 256 words, a CTA scan of their popcounts, one atomic per round
 __global__ void __launch_bounds__(256)
-    bitmap_diff_list_kernel(const uint32_t* __restrict__ vis, const uint32_t* __restrict__ prev,
-                            uint32_t nw, uint32_t* out, uint32_t* cnt) {
+    bitmap_diff_list_kernel(const uint32_t* __restrict__ vis, uint32_t* prev, uint32_t nw,
+                            uint32_t* out, uint32_t* cnt, int set_prev = 0) {
   __shared__ uint32_t s_warp[8];
   __shared__ uint32_t s_base;
   const uint32_t lane = lane_id(), warp = threadIdx.x >> 5;
   for (uint32_t base = blockIdx.x * 256; base < nw; base += gridDim.x * 256) {
     const uint32_t i = base + threadIdx.x;
-    uint32_t d = i < nw ? (__ldg(&vis[i]) & ~__ldg(&prev[i])) : 0u;
+    uint32_t d = 0;
+    if (i < nw) {
+      const uint32_t a = __ldg(&vis[i]);
+      d = a & ~prev[i];
+      if (set_prev) prev[i] = a;  // prev = vis in the same pass (push step follows)
+    }
     // CTA exclusive scan of the popcounts: warp shuffles, then the 8 warp sums
     const uint32_t c = __popc(d);
     uint32_t x = c;
@@ -1208,15 +1213,13 @@ struct DobfsGraphRun {
 class DobfsGraphRunner {
  public:
   static bool eligible(const Plan& P, const mg_config& c) {
-    // The graph removes the per-superstep host round trip (~4 us each), which
-    // pays on small graphs (RMAT-18..22: 7-10% less device time); on RMAT-26
-    // the superstep kernels dominate and the host loop measured 1.3% faster
-    // (tools/graph_probe.py), so by default only graphs under 2^30 arcs use
-    // it.  MG_GRAPH_LOOP=1 forces it on, MG_NO_GRAPH (any value) forces off.
+    // The graph removes the per-superstep host round trip (~4 us each): 7-10%
+    // less device time on RMAT-18..22; on RMAT-26 1.6% (8.18 -> 8.05 ms over
+    // the bench sources, tools/gpu/graph_vs_host.sh, after the round-2 pull
+    // changes; the host loop had been 1.3% faster before them).
+    // MG_GRAPH_LOOP=0 or MG_NO_GRAPH (any value) forces the host loop.
     const char* force = getenv("MG_GRAPH_LOOP");
-    const bool big = P.ne >= (1ull << 30);
-    const bool off = getenv("MG_NO_GRAPH") != nullptr ||
-                     (force ? force[0] == '0' : big);
+    const bool off = getenv("MG_NO_GRAPH") != nullptr || (force && force[0] == '0');
     const bool fused = c.fused == MG_FUSED_ON || (c.fused == MG_FUSED_AUTO &&
                                                   c.policy == MG_POLICY_FUSED);
     return !off && P.n == 1 && P.dup == MG_DUP_ALL && c.dobfs_exact_cost && !P.profile &&
@@ -1422,9 +1425,13 @@ class DobfsGraphRunner {
     // push branch: frontier list from the bitmap, prev = vis, edge-balanced advance
     MGB_CUDA(cudaStreamBeginCaptureToGraph(s, bodies[1], nullptr, nullptr, 0,
                                            cudaStreamCaptureModeRelaxed));
+#ifndef MG_DIFF_FUSE
+#define MG_DIFF_FUSE 1
+#endif
     MGB_LAUNCH(bitmap_diff_list_kernel, grid_for(nw, 256, num_sms() * 8), 256, 0, s, w.su32[2].ptr,
-               w.aux[4].ptr, (uint32_t)nw, w.loop_front[0].ptr, &st->in_count);
-    MGB_CUDA(cudaMemcpyAsync(w.aux[4].ptr, w.su32[2].ptr, 4 * nw, cudaMemcpyDeviceToDevice, s));
+               w.aux[4].ptr, (uint32_t)nw, w.loop_front[0].ptr, &st->in_count, MG_DIFF_FUSE);
+    if (!MG_DIFF_FUSE)
+      MGB_CUDA(cudaMemcpyAsync(w.aux[4].ptr, w.su32[2].ptr, 4 * nw, cudaMemcpyDeviceToDevice, s));
     const uint32_t* nin = &st->in_count;
     MGB_LAUNCH(lb_degree_kernel, num_sms() * 8, kLbBlock, 0, s, w.off.ptr, w.loop_front[0].ptr, 0u,
                w.loop_lb_row.ptr, w.loop_lb_pref.ptr, w.loop_lb_bsum.ptr, nin);

@@ -1,6 +1,8 @@
 """Device time of the bench workload (exact-cost DOBFS, RMAT-26, the 8 bench
 sources) with the device-driven graph loop and, with MG_NO_GRAPH=1, the
-host-driven loop.  No profiler attached."""
+host-driven loop.  No profiler attached.
+
+    python tools/graph_probe.py [scale] [graph|host]"""
 import os
 import sys
 
@@ -16,7 +18,8 @@ off, _, _ = plan.download_graph().arrays()
 srcs = bench.pick_sources(off, 8)
 cfg = mg.EngineConfig(policy=mg.AllocPolicyKind.Maximum, fused=mg.FusedMode.On,
                       dobfs_exact_cost=True)
-for mode in ("graph", "host"):
+modes = [sys.argv[2]] if len(sys.argv) > 2 else ["graph", "host"]
+for mode in modes:
     if mode == "host":
         os.environ["MG_NO_GRAPH"] = "1"
     for s in srcs:
