@@ -685,11 +685,24 @@ struct HostTrace {
   }
 };
 
+// does the primitive leave a DOBFS label array behind (DobfsPrim)?  Every
+// other run invalidates the incremental label reset (Worker::dobfs_labels_ok)
+template <class Prim>
+auto keeps_dobfs_labels(const Prim& p, int) -> decltype(bool(p.keeps_dobfs_labels)) {
+  return p.keeps_dobfs_labels;
+}
+template <class Prim>
+bool keeps_dobfs_labels(const Prim&, long) {
+  return false;
+}
+
 template <class Prim>
 void run_primitive(Plan& P, Prim& prim, const mg_config& cfg) {
   HostTrace trace;
   trace("enter");
   const uint32_t n = P.n;
+  if (!keeps_dobfs_labels(prim, 0))
+    for (uint32_t p : P.local_workers) P.workers[p]->dobfs_labels_ok = false;
   if (prim.nva < 0 || prim.nva > kMaxAssoc || prim.nvv < 0 || prim.nvv > kMaxAssoc)
     throw Error(MG_EINVAL, std::string(prim.name) + ": at most " + std::to_string(kMaxAssoc) +
                                " vertex and value associates per record");

@@ -50,6 +50,7 @@ static void free_worker(Worker& w) {
     if (w.loop_exec[i]) cudaGraphExecDestroy(w.loop_exec[i]);
   if (w.mp_exec) cudaGraphExecDestroy(w.mp_exec);
   w.mp_state.free_(); w.mp_hist.free_();
+  w.dobfs_lastvis.free_();
   if (w.loop_host) cudaFreeHost(w.loop_host);
   if (w.loop_hist_host) cudaFreeHost(w.loop_hist_host);
   w.loop_state.free_(); w.loop_hist.free_(); w.loop_front[0].free_(); w.loop_front[1].free_();

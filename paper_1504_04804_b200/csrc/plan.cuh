@@ -174,6 +174,12 @@ struct Worker {
   DevArray<double> bc_acc;              // BC: huge-row partial sums
   uint32_t n_nonisolated = 0;
   bool nonisolated_ready = false;
+  // DOBFS labels: when the label array holds a completed DOBFS run's result,
+  // the next run skips the |V|-entry fill and only resets the vertices the
+  // previous run reached and this one does not (dobfs_lastvis = the previous
+  // run's visited bitmap).  Any other primitive clears the flag.
+  DevArray<uint32_t> dobfs_lastvis;
+  bool dobfs_labels_ok = false;
   std::vector<uint32_t> hosted_host;  // hosted local IDs (host copy)
   DevArray<uint32_t> border_dst;      // PR: destination-local ID of every border entry
 

@@ -337,6 +337,50 @@ __global__ void bitmap_set_kernel(const uint32_t* __restrict__ in, uint32_t n, u
   }
 }
 
+// end of a DOBFS run whose label fill was skipped: every vertex the previous
+// run reached and this one did not goes back to infinity (lastvis & ~vis;
+// in RMAT runs from the giant component that is no vertex at all), then
+// lastvis = vis for the next run
+__global__ void dobfs_label_fixup_kernel(uint32_t* lastvis, const uint32_t* __restrict__ vis,
+                                         uint32_t nw, uint32_t* labels, uint32_t nv) {
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < nw; i += gridDim.x * blockDim.x) {
+    const uint32_t cur = vis[i];
+    uint32_t d = lastvis[i] & ~cur;
+    lastvis[i] = cur;
+    while (d) {
+      const uint32_t v = i * 32 + (__ffs(d) - 1);
+      if (v < nv) labels[v] = kInfLabel;
+      d &= d - 1;
+    }
+  }
+}
+
+// start of a DOBFS run on worker w: the labels are filled with infinity only
+// when the array does not hold a completed DOBFS result; otherwise the
+// previous run's visited bitmap is kept for the end-of-run fixup (16 MB of
+// bitmap traffic instead of the 268 MB fill at RMAT-26)
+void dobfs_labels_begin(Worker& w, uint64_t nw) {
+  if (w.dobfs_lastvis.n < nw || !w.dobfs_lastvis.ptr) {
+    w.dobfs_lastvis.alloc(nw);
+    w.dobfs_labels_ok = false;
+  }
+  if (w.dobfs_labels_ok && w.su32[0].ptr && w.su32[0].n >= w.nv && w.su32[2].ptr &&
+      w.su32[2].n >= nw && !getenv("MG_DOBFS_FILL")) {
+    MGB_CUDA(cudaMemcpyAsync(w.dobfs_lastvis.ptr, w.su32[2].ptr, 4 * nw, cudaMemcpyDeviceToDevice,
+                             w.stream));
+  } else {
+    if (w.su32[0].n < w.nv || !w.su32[0].ptr) w.su32[0].alloc(w.nv ? w.nv : 1);
+    MGB_CUDA(cudaMemsetAsync(w.su32[0].ptr, 0xFF, 4ull * (w.nv ? w.nv : 1), w.stream));
+    MGB_CUDA(cudaMemsetAsync(w.dobfs_lastvis.ptr, 0, 4 * nw, w.stream));
+  }
+  w.dobfs_labels_ok = false;  // until this run completes
+}
+
+void dobfs_labels_end(Worker& w, uint64_t nw) {
+  MGB_LAUNCH(dobfs_label_fixup_kernel, grid_for(nw, 256, num_sms() * 8), 256, 0, w.stream,
+             w.dobfs_lastvis.ptr, w.su32[2].ptr, (uint32_t)nw, w.su32[0].ptr, w.nv);
+}
+
 __global__ void select_nonisolated_kernel(const uint32_t* __restrict__ hosted, uint32_t nh,
                                           const uint32_t* __restrict__ off, uint32_t* out,
                                           uint32_t* cnt) {
@@ -927,6 +971,7 @@ struct DobfsPrim : PrimBase {
   std::vector<uint32_t> ul_len;
   bool exact_cost = false;
   uint64_t physical_pull_steps = 0;
+  static constexpr bool keeps_dobfs_labels = true;
   DobfsPrim(uint32_t s, double a, double b, bool m, bool exact, uint32_t nparts)
       : source(s), do_a(a), do_b(b), mark_preds(m), exact_cost(exact) {
     reports_deg = exact;  // n = 1: by the pull / push kernels; n > 1: by split + merge
@@ -989,7 +1034,8 @@ struct DobfsPrim : PrimBase {
     // unvisited lists (ping-pong) and the long-row queue: plan-lifetime buffers
     for (int i = 0; i < 3; ++i)
       if (w.ul_buf[i].n < k + 1 || !w.ul_buf[i].ptr) w.ul_buf[i].alloc(k + 1);
-    fill(w.su32[0], w.nv, 0xFF, w.stream);        // labels
+    if (w.su32[2].n < words(w.nv) || !w.su32[2].ptr) w.dobfs_labels_ok = false;
+    dobfs_labels_begin(w, words(w.nv));           // labels (fill or fixup)
     fill(w.su32[2], words(w.nv), 0, w.stream);    // visited bitmap
     fill(w.aux[4], words(w.nv), 0, w.stream);     // visited as of the previous superstep
     if (w.su32[3].n < words(w.nv) || !w.su32[3].ptr) w.su32[3].alloc(words(w.nv));  // frontier
@@ -1178,7 +1224,10 @@ struct DobfsPrim : PrimBase {
     c.P->prof_launches += 1;
   }
   std::vector<int> prof_kind_ = std::vector<int>(kMaxWorkers, 0);
-  void finalize(Ctx& c, const GlobalView&) { collect_profile(c); }
+  void finalize(Ctx& c, const GlobalView&) {
+    collect_profile(c);
+    dobfs_labels_end(*c.w, words(c.w->nv));
+  }
   // several partitions with the exact-cost test: share this worker's list
   // length and next-frontier degree sum through the report (u[0], u[1])
   bool pulled_ = false;
@@ -1254,18 +1303,20 @@ class DobfsGraphRunner {
     MGB_CUDA(cudaMemcpyAsync(w.loop_state.ptr, w.loop_host, sizeof(DobfsLoop),
                              cudaMemcpyHostToDevice, w.stream));
     MGB_CUDA(cudaMemsetAsync(w.ctr.ptr, 0, sizeof(Counters), w.stream));
-    MGB_CUDA(cudaMemsetAsync(w.su32[0].ptr, 0xFF, 4ull * w.nv, w.stream));  // labels
+    dobfs_labels_begin(w, nw);                                              // labels
     MGB_CUDA(cudaMemsetAsync(w.su32[2].ptr, 0, 4 * nw, w.stream));          // visited
     MGB_CUDA(cudaMemsetAsync(w.aux[4].ptr, 0, 4 * nw, w.stream));           // visited (prev)
     if (mark_preds) MGB_CUDA(cudaMemsetAsync(w.su32[1].ptr, 0xFF, 4ull * w.nv, w.stream));
     MGB_LAUNCH(dobfs_loop_init_kernel, 1, 1, 0, w.stream,
                reinterpret_cast<DobfsLoop*>(w.loop_state.ptr), w.su32[0].ptr, w.su32[2].ptr);
     MGB_CUDA(cudaGraphLaunch(G.exec, w.stream));
+    dobfs_labels_end(w, nw);
     MGB_CUDA(cudaEventRecord(w.ev_end, w.stream));
     MGB_CUDA(cudaMemcpyAsync(w.loop_host, w.loop_state.ptr, sizeof(DobfsLoop),
                              cudaMemcpyDeviceToHost, w.stream));
     MGB_CUDA(cudaStreamSynchronize(w.stream));
     const uint32_t S = lh->iter;
+    w.dobfs_labels_ok = true;  // labels = this run's result (fixup done)
     MGB_CUDA(cudaMemcpy(hh, w.loop_hist.ptr, sizeof(DobfsHist) * S, cudaMemcpyDeviceToHost));
     DobfsGraphRun r;
     uint64_t W = 0, launches = 2;  // init kernel + graph
@@ -3642,6 +3693,7 @@ int mg_bfs(mg_plan* plan, uint32_t source, int mark_preds, const mg_config* cfg,
       prim.name = "bfs";
       prim.communication = MG_COMM_SELECTIVE;
       run_primitive(P, prim, c);
+      for (uint32_t p : P.local_workers) P.workers[p]->dobfs_labels_ok = true;
     } else {
       BfsPrim prim(source, mark_preds != 0);
       run_primitive(P, prim, c);
@@ -3697,6 +3749,7 @@ int mg_dobfs(mg_plan* plan, uint32_t source, double do_a, double do_b, int mark_
       DobfsPrim prim(source, do_a, do_b, mark_preds != 0, c.dobfs_exact_cost != 0, P.n);
       P.last = mg_stats{};
       run_primitive(P, prim, c);
+      for (uint32_t p : P.local_workers) P.workers[p]->dobfs_labels_ok = true;
       dir_log = prim.dir_log;
     }
     P.last_result_kind = 0;

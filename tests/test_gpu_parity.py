@@ -550,3 +550,50 @@ def test_dobfs_pull_first_hit_positions(n, do_a):
             assert list(r.direction_log) == list(rr.direction_log)
             assert r.stats.edges_examined == rr.stats.edges_examined
             assert r.stats.supersteps == rr.stats.supersteps
+
+
+def _two_components():
+    """RMAT-10 on [0, 1024), RMAT-9 shifted to [1024, 1536), plus 64 isolated
+    vertices at the end: sources in different components reach disjoint sets"""
+    def edges(g, shift):
+        off, col, _ = g.arrays()
+        src = np.repeat(np.arange(len(off) - 1), np.diff(off))
+        return np.stack([src + shift, col.astype(np.int64) + shift], axis=1)
+    e = np.concatenate([edges(mg.Csr.rmat(10, 8, 3), 0), edges(mg.Csr.rmat(9, 8, 5), 1024)])
+    g = mg.Csr.from_edges(1536 + 64, e)
+    return g, g.arrays()
+
+
+@pytest.mark.parametrize("n,loop", [(1, "graph"), (1, "host"), (2, "host"), (3, "host")])
+def test_dobfs_labels_across_runs_without_fill(n, loop):
+    """a DOBFS run that follows a completed DOBFS run skips the |V| label
+    fill and resets only what the previous run reached and this one did not:
+    labels stay exact across sources in different components, an isolated
+    source, a max_supersteps cut and interleaved runs of other primitives
+    (which clear the reuse)"""
+    import os
+    g, (off, col, _) = _two_components()
+    plan = mg.PartitionPlan(g, mg.partition_random(g.num_vertices, n, 3) if n > 1 else None, n)
+    comp_a = int(np.nonzero(np.diff(off)[:1024])[0][0])
+    comp_b = 1024 + int(np.nonzero(np.diff(off)[1024:1536])[0][0])
+    iso = 1536 + 5
+    cut = mg.EngineConfig(policy=mg.AllocPolicyKind.Maximum, fused=mg.FusedMode.On,
+                          dobfs_exact_cost=True, max_supersteps=2)
+    if loop == "host":
+        os.environ["MG_NO_GRAPH"] = "1"
+    try:
+        for src, cfg, other in ((comp_a, GRAPH_CFG, None), (comp_b, GRAPH_CFG, None),
+                                (iso, GRAPH_CFG, None), (comp_a, GRAPH_CFG, "bc"),
+                                (comp_a, cut, None), (comp_b, GRAPH_CFG, None),
+                                (comp_b, GRAPH_CFG, "bfs"), (comp_a, None, None)):
+            if other == "bc":
+                mg.bc(plan, comp_b)
+            elif other == "bfs":
+                mg.bfs(plan, mg.BfsOptions(source=comp_a))
+            r = mg.dobfs(plan, mg.DobfsOptions(source=src), cfg)
+            want = seq.bfs_levels(off, col, src)
+            if cfg is cut:
+                want = np.where(want <= 2, want, mg.kInfLabel).astype(want.dtype)
+            assert np.array_equal(r.labels, want), (src, other)
+    finally:
+        os.environ.pop("MG_NO_GRAPH", None)
