@@ -339,20 +339,36 @@ __global__ void bitmap_set_kernel(const uint32_t* __restrict__ in, uint32_t n, u
 
 // end of a DOBFS run whose label fill was skipped: every vertex the previous
 // run reached and this one did not goes back to infinity (lastvis & ~vis;
-// in RMAT runs from the giant component that is no vertex at all), then
-// lastvis = vis for the next run
-__global__ void dobfs_label_fixup_kernel(uint32_t* lastvis, const uint32_t* __restrict__ vis,
-                                         uint32_t nw, uint32_t* labels, uint32_t nv) {
-  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < nw; i += gridDim.x * blockDim.x) {
-    const uint32_t cur = vis[i];
-    uint32_t d = lastvis[i] & ~cur;
-    lastvis[i] = cur;
-    while (d) {
-      const uint32_t v = i * 32 + (__ffs(d) - 1);
-      if (v < nv) labels[v] = kInfLabel;
-      d &= d - 1;
+// in RMAT runs from the giant component that is no vertex at all).  Two
+// streaming 16-byte reads per 128 vertices; the next run's begin copies vis
+// into lastvis.
+__device__ __forceinline__ void reset_unreached(uint32_t d, uint32_t word, uint32_t* labels,
+                                                uint32_t nv) {
+  while (d) {
+    const uint32_t v = word * 32 + (__ffs(d) - 1);
+    if (v < nv) labels[v] = kInfLabel;
+    d &= d - 1;
+  }
+}
+__global__ void dobfs_label_fixup_kernel(const uint32_t* __restrict__ lastvis,
+                                         const uint32_t* __restrict__ vis, uint32_t nw,
+                                         uint32_t* labels, uint32_t nv) {
+  const uint32_t n4 = nw / 4;
+  const uint4* l4 = reinterpret_cast<const uint4*>(lastvis);
+  const uint4* v4 = reinterpret_cast<const uint4*>(vis);
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n4; i += gridDim.x * blockDim.x) {
+    const uint4 a = __ldcs(&l4[i]), b = __ldcs(&v4[i]);
+    const uint32_t d0 = a.x & ~b.x, d1 = a.y & ~b.y, d2 = a.z & ~b.z, d3 = a.w & ~b.w;
+    if (d0 | d1 | d2 | d3) {
+      reset_unreached(d0, 4 * i, labels, nv);
+      reset_unreached(d1, 4 * i + 1, labels, nv);
+      reset_unreached(d2, 4 * i + 2, labels, nv);
+      reset_unreached(d3, 4 * i + 3, labels, nv);
     }
   }
+  for (uint32_t i = n4 * 4 + blockIdx.x * blockDim.x + threadIdx.x; i < nw;
+       i += gridDim.x * blockDim.x)
+    reset_unreached(lastvis[i] & ~vis[i], i, labels, nv);
 }
 
 // start of a DOBFS run on worker w: the labels are filled with infinity only
@@ -377,7 +393,7 @@ void dobfs_labels_begin(Worker& w, uint64_t nw) {
 }
 
 void dobfs_labels_end(Worker& w, uint64_t nw) {
-  MGB_LAUNCH(dobfs_label_fixup_kernel, grid_for(nw, 256, num_sms() * 8), 256, 0, w.stream,
+  MGB_LAUNCH(dobfs_label_fixup_kernel, grid_for(nw / 4 + 1, 256, num_sms() * 8), 256, 0, w.stream,
              w.dobfs_lastvis.ptr, w.su32[2].ptr, (uint32_t)nw, w.su32[0].ptr, w.nv);
 }
 
