@@ -333,7 +333,8 @@ def run_ours(args, rank, world, local):
         """the same K steps with per-kernel CUDA events on the library stream
         (host-driven loop): the roofline of the dominant kernel classes"""
         mg.lib().mg_plan_set_profiling(plan._h, 1)
-        e2e_call(mg, plan, sources[0], cfg, None, do_a, do_b)
+        for s in sources:  # the host loop's scratch at its size before the timed steps
+            e2e_call(mg, plan, s, cfg, None, do_a, do_b)
         barrier()
         acc = {"pull": [0.0, 0.0, 0], "push": [0.0, 0.0, 0], "dev_ms": 0.0, "xms": 0.0,
                "xbytes": 0}

@@ -45,6 +45,7 @@ static void free_worker(Worker& w) {
   for (auto& a : w.aux) a.free_();
   w.nonisolated.free_();
   w.pull_rec.free_();
+  w.pull_ext.free_();
   for (auto& a : w.ul_buf) a.free_();
   for (int i = 0; i < 2; ++i)
     if (w.loop_exec[i]) cudaGraphExecDestroy(w.loop_exec[i]);
@@ -342,12 +343,21 @@ void prepare_worker(Plan& P, Worker& w, const mg_config& cfg) {
     return static_cast<uint64_t>(f * static_cast<double>(unit) + 0.9999);
   };
   switch (cfg.policy) {
-    case MG_POLICY_MAX:
+    case MG_POLICY_MAX: {
       w.advance_out.prealloc(E, w.stream);
       w.output.prealloc(V, w.stream);
       w.input.prealloc(V, w.stream);
       w.next_input.prealloc(V, w.stream);
+      // the advance's load-balancing scratch at its bound too, so no run of a
+      // max-policy plan allocates inside its superstep loop
+      const uint64_t nb = (V + kLbBlock - 1) / kLbBlock;
+      const uint64_t tiles = (2 * E + 1) / kTile + 2 + kMinTiles + 1;
+      if (w.lb_row.n < V) w.lb_row.alloc(V ? V : 1);
+      if (w.lb_pref.n < V) w.lb_pref.alloc(V ? V : 1);
+      if (w.lb_bsum.n < nb + 1) w.lb_bsum.alloc(nb + 1);
+      if (w.lb_tile.n < tiles) w.lb_tile.alloc(tiles);
       break;
+    }
     case MG_POLICY_FIXED:
     case MG_POLICY_FUSED:
       w.advance_out.prealloc(items(cfg.factors[MG_ROLE_ADVANCE_OUTPUT], E), w.stream);

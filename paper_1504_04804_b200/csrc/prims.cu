@@ -434,6 +434,8 @@ constexpr uint32_t kPullQ = 256 * kPV + MG_PULL_QX;  // CTA queue capacity (>= o
 // by the thread stage itself (one offset load + one or two col sectors per row);
 // only rows longer than kPullStart go on to the cooperative stage
 constexpr int kPullMid = MG_PULL_MID;
+static_assert(kPullMid >= 3, "stage 1b takes arcs 2-4 from the record extension");
+constexpr int kExtArcs = 3;  // arcs 2..4 held by the record extension
 constexpr uint32_t kPullStart = kPullK + kPullMid;
 // (measured: stage 1b as its own kernel over the long-row queue, one row per
 // thread and no CTA barrier, is slower — 8.93 -> 10.61 ms over the bench
@@ -450,6 +452,19 @@ __global__ void pull_records_kernel(GraphView g, const uint32_t* __restrict__ ni
     uint32_t v = ni[i];
     uint32_t b = g.off[v], d = g.off[v + 1] - b;
     rec[i] = make_uint4(v, d, d > 0 ? g.col[b] : kInfLabel, d > 1 ? g.col[b + 1] : kInfLabel);
+  }
+}
+
+// record extensions (plan lifetime, same positions): {off[v], arc2, arc3, arc4}
+// for stage 1b, so a row the record's two arcs did not settle starts on
+// arcs 2-4 without first loading its row offset
+__global__ void pull_ext_kernel(GraphView g, const uint32_t* __restrict__ ni, uint32_t n,
+                                uint4* ext) {
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    const uint32_t v = ni[i];
+    const uint32_t b = g.off[v], d = g.off[v + 1] - b;
+    ext[i] = make_uint4(b, d > 2 ? g.col[b + 2] : kInfLabel, d > 3 ? g.col[b + 3] : kInfLabel,
+                        d > 4 ? g.col[b + 4] : kInfLabel);
   }
 }
 
@@ -500,7 +515,7 @@ constexpr uint32_t kVisWin = 128;   // per-warp visited-word window of the pull 
 template <bool kEmit>
 __global__ void __launch_bounds__(256, MG_PULL_OCC)
     dobfs_pull_thread_kernel(GraphView g, const uint4* __restrict__ rec,
-                             const uint32_t* __restrict__ ul,
+                             const uint4* __restrict__ ext, const uint32_t* __restrict__ ul,
                              uint32_t nul, uint32_t* labels, uint32_t* preds, uint32_t* vis,
                              const uint32_t* __restrict__ fb, uint32_t next_label, int mark_preds,
                              OwnerView ow, int emit_found, uint32_t* out, uint32_t* ul_out,
@@ -620,21 +635,30 @@ __global__ void __launch_bounds__(256, MG_PULL_OCC)
         const uint32_t t = t0 + lane_id();
         const bool act = t < cnt;
         uint32_t p = act ? lst[t] : 0u;
+        // the record again (L1/L2) and its extension {off, arc2, arc3, arc4},
+        // both addressed by the position: arcs 2-4 need no offset load
         const uint4 rr = act ? rec[p] : make_uint4(0, 0, 0, 0);
+        const uint4 ex = act ? __ldcs(&ext[p]) : make_uint4(0, 0, 0, 0);
         uint32_t v = rr.x;
         const uint32_t d = rr.y;
-        const uint32_t o = act ? __ldg(&g.off[v]) : 0u;
+        const uint32_t o = ex.x;
         const uint32_t e = d < kPullStart ? d : kPullStart;
         uint32_t wv[kPullMid > 0 ? kPullMid : 1];
         bool h[kPullMid > 0 ? kPullMid : 1];
+        wv[0] = ex.y;
+        wv[1] = ex.z;
+        wv[2] = ex.w;
 #pragma unroll
-        for (int k = 0; k < kPullMid; ++k) {
-          const bool ok = act && kPullK + k < e;
+        for (int k = 0; k < kExtArcs; ++k) h[k] = act && kPullK + k < e && bit_set(fb, wv[k]);
+        const bool hit_ext = h[0] || h[1] || h[2];
+#pragma unroll
+        for (int k = kExtArcs; k < kPullMid; ++k) {  // arcs 5..9 only past a miss
+          const bool ok = act && !hit_ext && kPullK + k < e;
           wv[k] = ok ? __ldg(&g.col[o + kPullK + k]) : 0u;
           h[k] = ok;
         }
 #pragma unroll
-        for (int k = 0; k < kPullMid; ++k) h[k] = h[k] && bit_set(fb, wv[k]);
+        for (int k = kExtArcs; k < kPullMid; ++k) h[k] = h[k] && bit_set(fb, wv[k]);
         int f = -1;
         uint32_t pw = 0;
 #pragma unroll
@@ -1037,9 +1061,13 @@ struct DobfsPrim : PrimBase {
     MGB_CUDA(cudaMemcpy(w.nonisolated.ptr, h.data(), 4ull * k, cudaMemcpyHostToDevice));
     w.n_nonisolated = k;
     w.pull_rec.alloc(k ? k : 1);
-    if (k)
+    w.pull_ext.alloc(k ? k : 1);
+    if (k) {
       MGB_LAUNCH(pull_records_kernel, grid_for(k, 256, num_sms() * 16), 256, 0, w.stream, w.graph(),
                  w.nonisolated.ptr, k, w.pull_rec.ptr);
+      MGB_LAUNCH(pull_ext_kernel, grid_for(k, 256, num_sms() * 16), 256, 0, w.stream, w.graph(),
+                 w.nonisolated.ptr, k, w.pull_ext.ptr);
+    }
     MGB_CUDA(cudaStreamSynchronize(w.stream));
     w.nonisolated_ready = true;
   }
@@ -1189,7 +1217,8 @@ struct DobfsPrim : PrimBase {
     if (nul) {
       auto* kern = emit ? dobfs_pull_thread_kernel<true> : dobfs_pull_thread_kernel<false>;
       MGB_LAUNCH(kern, grid_for(nul, 256 * kPV, num_sms() * MG_PULL_OCC), 256, 0,
-                 w.stream, w.graph(), w.pull_rec.ptr, ul, nul, w.su32[0].ptr, w.su32[1].ptr, w.su32[2].ptr,
+                 w.stream, w.graph(), w.pull_rec.ptr, w.pull_ext.ptr, ul, nul, w.su32[0].ptr,
+                 w.su32[1].ptr, w.su32[2].ptr,
                  w.su32[3].ptr, next_label, mark_preds ? 1 : 0, c.owner_view(), emit ? 1 : 0,
                  w.output.ptr, w.ul_buf[dst].ptr, ulcnt, w.ul_buf[2].ptr, cnts + 1, c.ctr(),
                  scanned, deg_out, DobfsDyn{nullptr, nullptr, nullptr});
@@ -1379,7 +1408,7 @@ class DobfsGraphRunner {
   // primitive regrew) forces a re-capture
   static std::vector<const void*> pointers(const Worker& w) {
     return {w.su32[0].ptr, w.su32[1].ptr, w.su32[2].ptr, w.su32[3].ptr, w.aux[2].ptr,
-            w.aux[4].ptr, w.ul_buf[0].ptr, w.ul_buf[1].ptr, w.ul_buf[2].ptr, w.pull_rec.ptr,
+            w.aux[4].ptr, w.ul_buf[0].ptr, w.ul_buf[1].ptr, w.ul_buf[2].ptr, w.pull_rec.ptr, w.pull_ext.ptr,
             w.off.ptr, w.col.ptr, w.owner.ptr, w.ctr.ptr, w.loop_state.ptr, w.loop_hist.ptr,
             w.loop_front[0].ptr, w.loop_front[1].ptr, w.loop_lb_row.ptr, w.loop_lb_pref.ptr,
             w.loop_lb_bsum.ptr, w.loop_total.ptr, w.loop_tiles.ptr};
@@ -1477,7 +1506,8 @@ class DobfsGraphRunner {
     MGB_LAUNCH(frontier_diff_kernel, grid_for(nw, 256, num_sms() * 8), 256, 0, s, w.su32[2].ptr,
                w.aux[4].ptr, w.su32[3].ptr, (uint32_t)nw, cnts, nullptr, 0ull,
                (const DobfsLoop*)st, &ctr->edges);
-    MGB_LAUNCH(dobfs_pull_thread_kernel<false>, num_sms() * MG_PULL_OCC, 256, 0, s, gv, w.pull_rec.ptr, nullptr, 0u,
+    MGB_LAUNCH(dobfs_pull_thread_kernel<false>, num_sms() * MG_PULL_OCC, 256, 0, s, gv, w.pull_rec.ptr,
+               w.pull_ext.ptr, nullptr, 0u,
                w.su32[0].ptr, w.su32[1].ptr, w.su32[2].ptr, w.su32[3].ptr, 0u, mp, ow, 0,
                w.loop_front[1].ptr, nullptr, &ctr->misc, w.ul_buf[2].ptr, cnts + 1, ctr,
                (unsigned long long*)nullptr, &ctr->next_deg, dyn);
@@ -1776,7 +1806,8 @@ class DobfsMpGraphRunner {
 
   static std::vector<const void*> pointers(const Plan& P, const Worker& w) {
     return {w.su32[0].ptr, w.su32[2].ptr, w.su32[3].ptr, w.aux[2].ptr, w.aux[4].ptr,
-            w.ul_buf[0].ptr, w.ul_buf[1].ptr, w.ul_buf[2].ptr, w.pull_rec.ptr, w.off.ptr,
+            w.ul_buf[0].ptr, w.ul_buf[1].ptr, w.ul_buf[2].ptr, w.pull_rec.ptr, w.pull_ext.ptr,
+            w.off.ptr,
             w.col.ptr, w.owner.ptr, w.ctr.ptr, w.mp_state.ptr, w.mp_hist.ptr, w.input.ptr,
             w.next_input.ptr, w.output.ptr, w.send_table.ptr, w.send_cnt_ptr.ptr,
             w.recv_table.ptr, w.inbox_cnt.ptr, w.merge_stamp.ptr, w.loop_lb_row.ptr,
@@ -1856,7 +1887,7 @@ class DobfsMpGraphRunner {
                w.aux[4].ptr, w.su32[3].ptr, (uint32_t)nw, cnts, nullptr, 0ull, &st->b,
                &ctr->edges);
     MGB_LAUNCH(dobfs_pull_thread_kernel<true>, num_sms() * MG_PULL_OCC, 256, 0, s, gv,
-               w.pull_rec.ptr, nullptr, 0u, w.su32[0].ptr, w.su32[1].ptr, w.su32[2].ptr,
+               w.pull_rec.ptr, w.pull_ext.ptr, nullptr, 0u, w.su32[0].ptr, w.su32[1].ptr, w.su32[2].ptr,
                w.su32[3].ptr, 0u, 0, ow, 1, w.output.ptr, nullptr, &ctr->misc, w.ul_buf[2].ptr,
                cnts + 1, ctr, (unsigned long long*)nullptr, (unsigned long long*)nullptr, dyn);
     MGB_LAUNCH(dobfs_pull_group_kernel, num_sms() * 8, 256, 0, s, gv, w.pull_rec.ptr,
