@@ -434,8 +434,8 @@ constexpr uint32_t kPullQ = 256 * kPV + MG_PULL_QX;  // CTA queue capacity (>= o
 // by the thread stage itself (one offset load + one or two col sectors per row);
 // only rows longer than kPullStart go on to the cooperative stage
 constexpr int kPullMid = MG_PULL_MID;
-static_assert(kPullMid >= 3, "stage 1b takes arcs 2-4 from the record extension");
-constexpr int kExtArcs = 3;  // arcs 2..4 held by the record extension
+constexpr int kExtArcs = 7;  // arcs 2..8 held by the record extension
+static_assert(kPullMid >= kExtArcs, "stage 1b takes arcs 2-8 from the record extension");
 constexpr uint32_t kPullStart = kPullK + kPullMid;
 // (measured: stage 1b as its own kernel over the long-row queue, one row per
 // thread and no CTA barrier, is slower — 8.93 -> 10.61 ms over the bench
@@ -455,16 +455,21 @@ __global__ void pull_records_kernel(GraphView g, const uint32_t* __restrict__ ni
   }
 }
 
-// record extensions (plan lifetime, same positions): {off[v], arc2, arc3, arc4}
-// for stage 1b, so a row the record's two arcs did not settle starts on
-// arcs 2-4 without first loading its row offset
+// record extensions (plan lifetime, same positions, one 32-byte sector each):
+// {off[v], arc2 .. arc8} for stage 1b, so a row the record's two arcs did not
+// settle tests arcs 2-8 from one sector — no offset load, no col_indices
+// sectors (a 16-byte extension costs the same sector; measured {off, arc2-4}
+// first: 7.90 -> 7.55 ms over the bench sources)
 __global__ void pull_ext_kernel(GraphView g, const uint32_t* __restrict__ ni, uint32_t n,
                                 uint4* ext) {
   for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
     const uint32_t v = ni[i];
     const uint32_t b = g.off[v], d = g.off[v + 1] - b;
-    ext[i] = make_uint4(b, d > 2 ? g.col[b + 2] : kInfLabel, d > 3 ? g.col[b + 3] : kInfLabel,
-                        d > 4 ? g.col[b + 4] : kInfLabel);
+    uint32_t a[7];
+#pragma unroll
+    for (int k = 0; k < 7; ++k) a[k] = d > 2u + k ? g.col[b + 2 + k] : kInfLabel;
+    ext[2 * i] = make_uint4(b, a[0], a[1], a[2]);
+    ext[2 * i + 1] = make_uint4(a[3], a[4], a[5], a[6]);
   }
 }
 
@@ -638,7 +643,8 @@ __global__ void __launch_bounds__(256, MG_PULL_OCC)
         // the record again (L1/L2) and its extension {off, arc2, arc3, arc4},
         // both addressed by the position: arcs 2-4 need no offset load
         const uint4 rr = act ? rec[p] : make_uint4(0, 0, 0, 0);
-        const uint4 ex = act ? __ldcs(&ext[p]) : make_uint4(0, 0, 0, 0);
+        const uint4 ex = act ? __ldcs(&ext[2 * p]) : make_uint4(0, 0, 0, 0);
+        const uint4 ex2 = act ? __ldcs(&ext[2 * p + 1]) : make_uint4(0, 0, 0, 0);
         uint32_t v = rr.x;
         const uint32_t d = rr.y;
         const uint32_t o = ex.x;
@@ -648,11 +654,17 @@ __global__ void __launch_bounds__(256, MG_PULL_OCC)
         wv[0] = ex.y;
         wv[1] = ex.z;
         wv[2] = ex.w;
+        wv[3] = ex2.x;
+        wv[4] = ex2.y;
+        wv[5] = ex2.z;
+        wv[6] = ex2.w;
 #pragma unroll
         for (int k = 0; k < kExtArcs; ++k) h[k] = act && kPullK + k < e && bit_set(fb, wv[k]);
-        const bool hit_ext = h[0] || h[1] || h[2];
+        bool hit_ext = false;
 #pragma unroll
-        for (int k = kExtArcs; k < kPullMid; ++k) {  // arcs 5..9 only past a miss
+        for (int k = 0; k < kExtArcs; ++k) hit_ext |= h[k];
+#pragma unroll
+        for (int k = kExtArcs; k < kPullMid; ++k) {  // arc 9 only past a miss
           const bool ok = act && !hit_ext && kPullK + k < e;
           wv[k] = ok ? __ldg(&g.col[o + kPullK + k]) : 0u;
           h[k] = ok;
@@ -1061,7 +1073,7 @@ struct DobfsPrim : PrimBase {
     MGB_CUDA(cudaMemcpy(w.nonisolated.ptr, h.data(), 4ull * k, cudaMemcpyHostToDevice));
     w.n_nonisolated = k;
     w.pull_rec.alloc(k ? k : 1);
-    w.pull_ext.alloc(k ? k : 1);
+    w.pull_ext.alloc(2ull * (k ? k : 1));
     if (k) {
       MGB_LAUNCH(pull_records_kernel, grid_for(k, 256, num_sms() * 16), 256, 0, w.stream, w.graph(),
                  w.nonisolated.ptr, k, w.pull_rec.ptr);
