@@ -145,7 +145,7 @@ struct Worker {
   DevArray<uint32_t> aux[6];          // primitive-private scratch (bitmaps, queues)
   DevArray<uint32_t> nonisolated;     // hosted vertices with out-degree > 0 (ascending)
   DevArray<uint4> pull_rec;           // DOBFS pull records {v, deg, arc0, arc1} per nonisolated
-  DevArray<uint4> pull_ext;           // their 32-byte extensions {off, arc2..arc8} (stage 1b)
+  DevArray<uint4> pull_ext;           // their 32-byte extensions: arcs 2..9 (stage 1b)
   DevArray<uint32_t> ul_buf[3];       // DOBFS unvisited lists (ping-pong) + long-row queue
   // device-driven DOBFS (graph mode): loop state, history, fixed frontier and
   // advance scratch, the instantiated graphs (by mark_preds)

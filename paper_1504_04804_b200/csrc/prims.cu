@@ -434,8 +434,11 @@ constexpr uint32_t kPullQ = 256 * kPV + MG_PULL_QX;  // CTA queue capacity (>= o
 // by the thread stage itself (one offset load + one or two col sectors per row);
 // only rows longer than kPullStart go on to the cooperative stage
 constexpr int kPullMid = MG_PULL_MID;
-constexpr int kExtArcs = 7;  // arcs 2..8 held by the record extension
-static_assert(kPullMid >= kExtArcs, "stage 1b takes arcs 2-8 from the record extension");
+static_assert(kPullMid == 8, "stage 1b takes arcs 2-9 from the 32-byte record extension");
+#ifndef MG_MID_WAVE
+#define MG_MID_WAVE 5
+#endif
+constexpr int kMidWave = MG_MID_WAVE;  // stage-1b probes in the first wave (3: 7.26 ms, 5: 7.17, 8: 7.31)
 constexpr uint32_t kPullStart = kPullK + kPullMid;
 // (measured: stage 1b as its own kernel over the long-row queue, one row per
 // thread and no CTA barrier, is slower — 8.93 -> 10.61 ms over the bench
@@ -456,20 +459,20 @@ __global__ void pull_records_kernel(GraphView g, const uint32_t* __restrict__ ni
 }
 
 // record extensions (plan lifetime, same positions, one 32-byte sector each):
-// {off[v], arc2 .. arc8} for stage 1b, so a row the record's two arcs did not
-// settle tests arcs 2-8 from one sector — no offset load, no col_indices
-// sectors (a 16-byte extension costs the same sector; measured {off, arc2-4}
-// first: 7.90 -> 7.55 ms over the bench sources)
+// arcs 2..9 of the row for stage 1b, so a row the record's two arcs did not
+// settle tests its next 8 arcs from one sector, with no offset load and no
+// col_indices sector (measured: {off, arc2-4} 7.90 -> 7.55 ms over the bench
+// sources, {off, arc2-8} 7.27, {arc2-9} below)
 __global__ void pull_ext_kernel(GraphView g, const uint32_t* __restrict__ ni, uint32_t n,
                                 uint4* ext) {
   for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
     const uint32_t v = ni[i];
     const uint32_t b = g.off[v], d = g.off[v + 1] - b;
-    uint32_t a[7];
+    uint32_t a[8];
 #pragma unroll
-    for (int k = 0; k < 7; ++k) a[k] = d > 2u + k ? g.col[b + 2 + k] : kInfLabel;
-    ext[2 * i] = make_uint4(b, a[0], a[1], a[2]);
-    ext[2 * i + 1] = make_uint4(a[3], a[4], a[5], a[6]);
+    for (int k = 0; k < 8; ++k) a[k] = d > 2u + k ? g.col[b + 2 + k] : kInfLabel;
+    ext[2 * i] = make_uint4(a[0], a[1], a[2], a[3]);
+    ext[2 * i + 1] = make_uint4(a[4], a[5], a[6], a[7]);
   }
 }
 
@@ -640,37 +643,26 @@ __global__ void __launch_bounds__(256, MG_PULL_OCC)
         const uint32_t t = t0 + lane_id();
         const bool act = t < cnt;
         uint32_t p = act ? lst[t] : 0u;
-        // the record again (L1/L2) and its extension {off, arc2, arc3, arc4},
-        // both addressed by the position: arcs 2-4 need no offset load
+        // the record again (L1/L2) and its 32-byte extension (arcs 2-9), both
+        // addressed by the position: no offset load, no col_indices sector
         const uint4 rr = act ? rec[p] : make_uint4(0, 0, 0, 0);
         const uint4 ex = act ? __ldcs(&ext[2 * p]) : make_uint4(0, 0, 0, 0);
         const uint4 ex2 = act ? __ldcs(&ext[2 * p + 1]) : make_uint4(0, 0, 0, 0);
         uint32_t v = rr.x;
         const uint32_t d = rr.y;
-        const uint32_t o = ex.x;
         const uint32_t e = d < kPullStart ? d : kPullStart;
-        uint32_t wv[kPullMid > 0 ? kPullMid : 1];
-        bool h[kPullMid > 0 ? kPullMid : 1];
-        wv[0] = ex.y;
-        wv[1] = ex.z;
-        wv[2] = ex.w;
-        wv[3] = ex2.x;
-        wv[4] = ex2.y;
-        wv[5] = ex2.z;
-        wv[6] = ex2.w;
+        const uint32_t wv[kPullMid] = {ex.x, ex.y, ex.z, ex.w, ex2.x, ex2.y, ex2.z, ex2.w};
+        bool h[kPullMid];
+        // two waves of frontier probes: arcs 2-6, then 7-9 only past a miss
+        // (probes are L2 requests; most rows hit early)
 #pragma unroll
-        for (int k = 0; k < kExtArcs; ++k) h[k] = act && kPullK + k < e && bit_set(fb, wv[k]);
-        bool hit_ext = false;
+        for (int k = 0; k < kMidWave; ++k) h[k] = act && kPullK + k < e && bit_set(fb, wv[k]);
+        bool early = false;
 #pragma unroll
-        for (int k = 0; k < kExtArcs; ++k) hit_ext |= h[k];
+        for (int k = 0; k < kMidWave; ++k) early |= h[k];
 #pragma unroll
-        for (int k = kExtArcs; k < kPullMid; ++k) {  // arc 9 only past a miss
-          const bool ok = act && !hit_ext && kPullK + k < e;
-          wv[k] = ok ? __ldg(&g.col[o + kPullK + k]) : 0u;
-          h[k] = ok;
-        }
-#pragma unroll
-        for (int k = kExtArcs; k < kPullMid; ++k) h[k] = h[k] && bit_set(fb, wv[k]);
+        for (int k = kMidWave; k < kPullMid; ++k)
+          h[k] = act && !early && kPullK + k < e && bit_set(fb, wv[k]);
         int f = -1;
         uint32_t pw = 0;
 #pragma unroll
