@@ -223,6 +223,7 @@ struct DobfsLoop {
   uint32_t iter, dir, switched, physical;
   uint32_t in_count, ul_src, ul_len, n_nonisolated;
   unsigned long long in_degsum, visited;
+  uint32_t prev_physical, pad_;  // the last superstep was a pull (its list is clean)
 };
 struct DobfsHist {
   uint32_t dir, physical, out, pad;
@@ -435,6 +436,9 @@ constexpr uint32_t kPullQ = 256 * kPV + MG_PULL_QX;  // CTA queue capacity (>= o
 // only rows longer than kPullStart go on to the cooperative stage
 constexpr int kPullMid = MG_PULL_MID;
 static_assert(kPullMid == 8, "stage 1b takes arcs 2-9 from the 32-byte record extension");
+#ifndef MG_A1_LAZY
+#define MG_A1_LAZY 1
+#endif
 #ifndef MG_MID_WAVE
 #define MG_MID_WAVE 5
 #endif
@@ -529,8 +533,9 @@ __global__ void __launch_bounds__(256, MG_PULL_OCC)
                              OwnerView ow, int emit_found, uint32_t* out, uint32_t* ul_out,
                              uint32_t* ul_out_cnt, uint32_t* longq, uint32_t* long_cnt,
                              Counters* ctr, unsigned long long* scanned_out,
-                             unsigned long long* deg_out, DobfsDyn dyn) {
+                             unsigned long long* deg_out, DobfsDyn dyn, int list_clean = 0) {
   if (dyn.st) {
+    list_clean = dyn.st->prev_physical;
     const uint32_t src = dyn.st->ul_src;
     nul = dyn.st->ul_len;
     ul = src == 2 ? nullptr : (src == 0 ? dyn.ub0 : dyn.ub1);
@@ -561,6 +566,7 @@ __global__ void __launch_bounds__(256, MG_PULL_OCC)
   if (threadIdx.x == 0) s_found = 0;
   __syncthreads();
   const uint32_t chunk = 256 * kPV;
+  const bool clean = ul != nullptr && list_clean;
   for (uint32_t base = blockIdx.x * chunk; base < nul; base += gridDim.x * chunk) {
     uint32_t pos[kPV];
     uint4 r[kPV];
@@ -588,10 +594,19 @@ __global__ void __launch_bounds__(256, MG_PULL_OCC)
     bool open[kPV], h0[kPV], h1[kPV];
 #pragma unroll
     for (int j = 0; j < kPV; ++j) {
-      open[j] = pos[j] != kInfLabel && !((__ldcg(&vis[r[j].x >> 5]) >> (r[j].x & 31)) & 1u);
+      // a list written by the previous superstep's pull holds only unvisited
+      // vertices (no push ran since): no visited probe
+      open[j] = pos[j] != kInfLabel &&
+                (clean || !((__ldcg(&vis[r[j].x >> 5]) >> (r[j].x & 31)) & 1u));
       h0[j] = open[j] && bit_set(fb, r[j].z);
+#if !MG_A1_LAZY
       h1[j] = open[j] && r[j].y > 1 && bit_set(fb, r[j].w);
+#endif
     }
+#if MG_A1_LAZY
+#pragma unroll
+    for (int j = 0; j < kPV; ++j) h1[j] = open[j] && !h0[j] && r[j].y > 1 && bit_set(fb, r[j].w);
+#endif
     bool found[kPV], keep[kPV], lng[kPV];
     uint32_t vv[kPV];
 #pragma unroll
@@ -944,6 +959,7 @@ __global__ void dobfs_loop_init_kernel(DobfsLoop* st, uint32_t* labels, uint32_t
   st->ul_len = st->n_nonisolated;
   st->in_degsum = 0;
   st->visited = 1;
+  st->prev_physical = 0;
 }
 
 __global__ void dobfs_loop_decide_kernel(DobfsLoop* st, DobfsHist* hist,
@@ -988,6 +1004,7 @@ __global__ void dobfs_loop_end_kernel(DobfsLoop* st, Counters* ctr, DobfsHist* h
       st->ul_len = ctr->misc;
       st->ul_src = st->ul_src == 0 ? 1 : 0;
     }
+    st->prev_physical = st->physical;
     st->in_count = out;
     st->in_degsum = ctr->next_deg;
   }
@@ -1134,6 +1151,8 @@ struct DobfsPrim : PrimBase {
     }
     const uint64_t nw = words(w.nv);
     pulled_ = false;
+    const bool prev_pull = prev_pull_[w.p];  // the unvisited list is clean
+    prev_pull_[w.p] = false;                 // set again below if this step pulls
     if (list_free[w.p]) {
       // the previous (pull) superstep only counted its discoveries: rebuild the
       // input frontier list from the visited bitmap (vis & ~vis_prev); a pull
@@ -1225,7 +1244,7 @@ struct DobfsPrim : PrimBase {
                  w.su32[1].ptr, w.su32[2].ptr,
                  w.su32[3].ptr, next_label, mark_preds ? 1 : 0, c.owner_view(), emit ? 1 : 0,
                  w.output.ptr, w.ul_buf[dst].ptr, ulcnt, w.ul_buf[2].ptr, cnts + 1, c.ctr(),
-                 scanned, deg_out, DobfsDyn{nullptr, nullptr, nullptr});
+                 scanned, deg_out, DobfsDyn{nullptr, nullptr, nullptr}, prev_pull ? 1 : 0);
       uint32_t* gq = w.ul_buf[2].ptr;  // cooperative-stage input
       uint32_t* gq_cnt = cnts + 1;
       MGB_LAUNCH(dobfs_pull_group_kernel, num_sms() * 8, 256, 0, w.stream, w.graph(),
@@ -1235,6 +1254,7 @@ struct DobfsPrim : PrimBase {
                  DobfsDyn{nullptr, nullptr, nullptr});
     }
     list_free[w.p] = !emit;
+    prev_pull_[w.p] = true;
     if (c.P->profile) {
       MGB_CUDA(cudaEventRecord(w.ev_k1, w.stream));
       prof_pending_[w.p] = true;
@@ -1290,6 +1310,7 @@ struct DobfsPrim : PrimBase {
   bool device_loop(Plan& P, std::vector<Ctx>& ctx, RunState& rs, const mg_config& cfg,
                    DeviceLoopOut& o);
   std::vector<bool> pending_ul_ = std::vector<bool>(kMaxWorkers, false);
+  std::vector<bool> prev_pull_ = std::vector<bool>(kMaxWorkers, false);
   std::vector<bool> list_free;  // per worker: last pull step counted, did not list
   std::vector<bool> prof_pending_ = std::vector<bool>(kMaxWorkers, false);
   std::vector<uint32_t> prof_nul_ = std::vector<uint32_t>(kMaxWorkers, 0);
@@ -1608,6 +1629,7 @@ __global__ void dobfs_mp_init_kernel(DobfsMpLoop* st, uint32_t* labels, uint32_t
   b.ul_src = 2;  // every non-isolated record, no list
   b.ul_len = b.n_nonisolated;
   b.visited = 1;
+  b.prev_physical = 0;
   st->overflow = 0;
 }
 
@@ -1662,6 +1684,7 @@ __global__ void dobfs_mp_pre_report_kernel(DobfsMpLoop* st, Counters* ctr) {
     b.ul_len = ctr->misc;
     b.ul_src = b.ul_src == 0 ? 1 : 0;
   }
+  b.prev_physical = b.physical;
 }
 
 __global__ void dobfs_mp_end_kernel(DobfsMpLoop* st, const Mailbox* mine, DobfsMpHist* hist,
