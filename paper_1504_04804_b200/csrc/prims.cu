@@ -2062,7 +2062,13 @@ struct SsspDev {
     }
     return false;
   }
-  __device__ bool keep(uint32_t v) const { return atomicExch(&seen[v], iter + 1) != iter + 1; }
+  // once per superstep: a |V|/8-byte bitmap cleared at every superstep (2 MB
+  // at 2^24, L2-resident) instead of a 4-byte stamp per vertex, so the random
+  // relaxation traffic leaves the L2 to the distances
+  __device__ bool keep(uint32_t v) const {
+    const uint32_t b = 1u << (v & 31);
+    return !(atomicOr(&seen[v >> 5], b) & b);
+  }
   __device__ bool prefilter(uint32_t) const { return true; }
   __device__ bool combine(uint32_t v, const uint32_t* va, const double* vv, uint32_t) const {
     T nd = (T)vv[0];
@@ -2154,7 +2160,7 @@ struct SsspPrim : PrimBase {
       MGB_LAUNCH(set_one_kernel<unsigned long long>, 1, 1, 0, w.stream, w.su64[0].ptr, source,
                  0ull);
     }
-    fill(w.su32[2], w.nv, 0, w.stream);     // seen
+    fill(w.su32[2], w.nv / 32 + 1, 0, w.stream);  // output dedup bitmap (cleared per superstep)
     if (mark_preds) fill(w.su32[1], w.nv, 0xFF, w.stream);
     if (c.P->owner_host[source] == w.p) c.push_initial({source});
   }
@@ -2170,6 +2176,8 @@ struct SsspPrim : PrimBase {
   }
   void body(Ctx& c) {
     Worker& w = *c.w;
+    if (c.iter > 0)
+      MGB_CUDA(cudaMemsetAsync(w.su32[2].ptr, 0, 4ull * (w.nv / 32 + 1), w.stream));
     if (narrow) {
       if (c.in_count)
         MGB_LAUNCH(snapshot_kernel<uint32_t>, grid_for(c.in_count, 256), 256, 0, w.stream,
