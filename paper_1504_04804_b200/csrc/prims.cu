@@ -2630,7 +2630,10 @@ struct BcDev {
     if (old == kInfLabel || old == cand) atomicAdd(&sigma[v], sigma[u]);
     return old == kInfLabel;
   }
-  __device__ bool keep(uint32_t v) const { return atomicExch(&seen[v], iter + 1) != iter + 1; }
+  // the claiming CAS accepts each vertex exactly once per superstep, so the
+  // output needs no second dedup (the per-vertex stamp cost an atomic and 4
+  // bytes of random L2 traffic per discovery)
+  __device__ bool keep(uint32_t) const { return true; }
   __device__ bool prefilter(uint32_t) const { return true; }
   __device__ bool combine(uint32_t v, const uint32_t*, const double* vv, uint32_t it) const {
     if (phase == kFwd) {  // primitives.cpp:639-648
