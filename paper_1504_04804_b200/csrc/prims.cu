@@ -2616,7 +2616,6 @@ struct BcDev {
   double* sigma;
   double* delta;
   uint32_t* bstamp;
-  uint32_t* seen;
   double* coef;
   OwnerView ow;
   uint32_t iter;
@@ -2987,7 +2986,6 @@ struct BcPrim : PrimBase {
   void init(Ctx& c) {  // primitives.cpp:528-541
     Worker& w = *c.w;
     fill(w.su32[0], w.nv, 0xFF, w.stream);  // labels
-    fill(w.su32[2], w.nv, 0, w.stream);     // seen
     fill(w.su32[3], w.nv, 0, w.stream);     // bstamp
     fill(w.sf64[0], w.nv, 0, w.stream);     // sigma
     fill(w.sf64[1], w.nv, 0, w.stream);     // delta
@@ -3001,8 +2999,8 @@ struct BcPrim : PrimBase {
   }
   BcDev dev(Ctx& c) {
     Worker& w = *c.w;
-    return {w.su32[0].ptr, w.sf64[0].ptr, w.sf64[1].ptr, w.su32[3].ptr, w.su32[2].ptr,
-            w.sf64[3].ptr, c.owner_view(), (uint32_t)c.iter, phase};
+    return {w.su32[0].ptr, w.sf64[0].ptr, w.sf64[1].ptr, w.su32[3].ptr, w.sf64[3].ptr,
+            c.owner_view(), (uint32_t)c.iter, phase};
   }
   int phase_at_body = kFwd;
   void body(Ctx& c) {  // primitives.cpp:543-625
