@@ -7,7 +7,8 @@ Every primitive at n = 1, 2, 3 partitions on one GPU (rmat 12/16 and a grid),
 the DOBFS pull kernels and the device-driven superstep loop (scale 16,
 exact-cost), the dense exchange (bitmap / value arrays, scale 14 at n = 2),
 each result checked against the oracle so a silent corruption also fails.
---mp runs the two-process CUDA-IPC fabric (every rank on GPU 0)."""
+--mp runs the two-process CUDA-IPC fabric (every rank on GPU 0), including
+the device-driven DOBFS superstep loop (one CUDA graph per rank)."""
 import os
 import sys
 
@@ -64,6 +65,14 @@ def single_process():
     check(np.array_equal(mg.dobfs(plan, mg.DobfsOptions(source=0)).labels,
                          seq.bfs_levels(off, col, 0)), "dobfs dense")
     check(np.array_equal(mg.cc(plan).components, seq.connected_components(off, col)), "cc dense")
+    # DOBFS runs back to back (incremental label reset), an interleaved BC
+    g = mg.Csr.rmat(13, 8, 4)
+    off, col, _ = g.arrays()
+    plan = mg.PartitionPlan(g, None, 1)
+    for s in (0, 9, 0):
+        check(np.array_equal(mg.dobfs(plan, mg.DobfsOptions(source=s), exact).labels,
+                             seq.bfs_levels(off, col, s)), "dobfs reuse")
+        mg.bc(plan, 1)
     print("sanitize cases ok")
 
 
@@ -84,12 +93,20 @@ owner = mg.partition_random(g.num_vertices, 2, 7)
 plan = mg.PartitionPlan.multiprocess(g, owner, 2, rank, 0, {key!r})
 hosted = owner == rank
 want = seq.bfs_levels(off, col, 0)
-for f in (lambda: mg.bfs(plan, mg.BfsOptions(source=0)).labels,
-          lambda: mg.dobfs(plan, mg.DobfsOptions(source=0)).labels):
+mx = mg.EngineConfig(policy=mg.AllocPolicyKind.Maximum, fused=mg.FusedMode.On,
+                    dobfs_exact_cost=True)
+cases = [lambda: mg.bfs(plan, mg.BfsOptions(source=0)).labels,
+         lambda: mg.dobfs(plan, mg.DobfsOptions(source=0)).labels,
+         lambda: mg.dobfs(plan, mg.DobfsOptions(source=0), mx).labels]  # device loop
+import os
+if os.environ.get("MG_SAN_ONLY_LOOP"):
+    cases = cases[2:]
+for f in cases:
     lab = f()
     assert np.array_equal(lab[hosted], want[hosted])
-comp = mg.cc(plan).components
-assert np.array_equal(comp[hosted], seq.connected_components(off, col)[hosted])
+if not os.environ.get("MG_SAN_ONLY_LOOP"):
+    comp = mg.cc(plan).components
+    assert np.array_equal(comp[hosted], seq.connected_components(off, col)[hosted])
 print("rank", rank, "ok")
 """
     with tempfile.NamedTemporaryFile("w", suffix=".py", delete=False) as f:
@@ -102,7 +119,10 @@ print("rank", rank, "ok")
 
 
 if __name__ == "__main__":
-    if "--mp" in sys.argv:
+    if "--mp-loop" in sys.argv:  # only the device-driven DOBFS loop, two processes
+        os.environ["MG_SAN_ONLY_LOOP"] = "1"
+        multi_process()
+    elif "--mp" in sys.argv:
         multi_process()
     else:
         single_process()
