@@ -427,7 +427,15 @@ constexpr int kPV = MG_PV;     // records per thread per iteration (loads in fli
 #ifndef MG_PULL_QX
 #define MG_PULL_QX 0
 #endif
-constexpr uint32_t kPullQ = 256 * kPV + MG_PULL_QX;  // CTA queue capacity (>= one chunk of 256 * kPV)
+#ifndef MG_PULL_BLOCK
+#define MG_PULL_BLOCK 128  // 128: 7.08 ms over the bench sources, 256: 7.16
+#endif
+#ifndef MG_PULL_OCC
+#define MG_PULL_OCC 4  // resident 256-thread CTAs' worth of warps per SM
+#endif
+constexpr uint32_t kPullBlock = MG_PULL_BLOCK;  // threads per CTA of the pull thread kernel
+constexpr uint32_t kPullCtas = MG_PULL_OCC * 256 / kPullBlock;  // resident CTAs per SM
+constexpr uint32_t kPullQ = kPullBlock * kPV + MG_PULL_QX;  // CTA queue capacity (>= one chunk)
 #ifndef MG_PULL_MID
 #define MG_PULL_MID 8
 #endif
@@ -519,13 +527,10 @@ constexpr uint32_t kVisWin = 128;   // per-warp visited-word window of the pull 
 // partition) the discovered vertices are only counted (and their degrees
 // summed into deg_out when non-null): the next superstep rebuilds the frontier
 // list from the visited bitmap only if it pushes.
-#ifndef MG_PULL_OCC
-#define MG_PULL_OCC 4
-#endif
 // kEmit: discoveries listed (several partitions); otherwise only counted and
 // the found queue takes no shared memory
 template <bool kEmit>
-__global__ void __launch_bounds__(256, MG_PULL_OCC)
+__global__ void __launch_bounds__(kPullBlock, kPullCtas)
     dobfs_pull_thread_kernel(GraphView g, const uint4* __restrict__ rec,
                              const uint4* __restrict__ ext, const uint32_t* __restrict__ ul,
                              uint32_t nul, uint32_t* labels, uint32_t* preds, uint32_t* vis,
@@ -556,16 +561,16 @@ __global__ void __launch_bounds__(256, MG_PULL_OCC)
   // shared memory and each touched word gets ONE global atomicOr per chunk
   // (measured: also loading the window's words for the open tests, instead
   // of one visited probe per record, is slower — 8.28 -> 8.89 ms)
-  __shared__ uint32_t s_nw[256 / 32][kVisWin];
-  __shared__ uint32_t s_mid[kInline1b ? 256 / 32 : 1][kInline1b ? 32 * kPV / kMidParts : 1];
-  for (uint32_t i = threadIdx.x; i < 8 * kVisWin; i += blockDim.x) (&s_nw[0][0])[i] = 0u;
+  __shared__ uint32_t s_nw[kPullBlock / 32][kVisWin];
+  __shared__ uint32_t s_mid[kInline1b ? kPullBlock / 32 : 1][kInline1b ? 32 * kPV / kMidParts : 1];
+  for (uint32_t i = threadIdx.x; i < (kPullBlock / 32) * kVisWin; i += blockDim.x) (&s_nw[0][0])[i] = 0u;
   uint32_t* nwin = s_nw[threadIdx.x >> 5];
   q_found.reset();
   q_keep.reset();
   q_long.reset();
   if (threadIdx.x == 0) s_found = 0;
   __syncthreads();
-  const uint32_t chunk = 256 * kPV;
+  const uint32_t chunk = kPullBlock * kPV;
   const bool clean = ul != nullptr && list_clean;
   for (uint32_t base = blockIdx.x * chunk; base < nul; base += gridDim.x * chunk) {
     uint32_t pos[kPV];
@@ -729,9 +734,9 @@ __global__ void __launch_bounds__(256, MG_PULL_OCC)
         q_long.base = q_long.n ? atomicAdd(long_cnt, q_long.n) : 0u;
       }
       __syncthreads();
-      for (uint32_t k = threadIdx.x; k < q_found.n; k += 256) out[q_found.base + k] = q_found.buf[k];
-      for (uint32_t k = threadIdx.x; k < q_keep.n; k += 256) ul_out[q_keep.base + k] = q_keep.buf[k];
-      for (uint32_t k = threadIdx.x; k < q_long.n; k += 256) longq[q_long.base + k] = q_long.buf[k];
+      for (uint32_t k = threadIdx.x; k < q_found.n; k += kPullBlock) out[q_found.base + k] = q_found.buf[k];
+      for (uint32_t k = threadIdx.x; k < q_keep.n; k += kPullBlock) ul_out[q_keep.base + k] = q_keep.buf[k];
+      for (uint32_t k = threadIdx.x; k < q_long.n; k += kPullBlock) longq[q_long.base + k] = q_long.buf[k];
       __syncthreads();
       if (threadIdx.x == 0) q_found.n = q_keep.n = q_long.n = 0;
       __syncthreads();
@@ -1239,7 +1244,7 @@ struct DobfsPrim : PrimBase {
         reports_deg && !c.want_deg && c.P->n == 1 ? &c.ctr()->next_deg : nullptr;
     if (nul) {
       auto* kern = emit ? dobfs_pull_thread_kernel<true> : dobfs_pull_thread_kernel<false>;
-      MGB_LAUNCH(kern, grid_for(nul, 256 * kPV, num_sms() * MG_PULL_OCC), 256, 0,
+      MGB_LAUNCH(kern, grid_for(nul, kPullBlock * kPV, num_sms() * kPullCtas), kPullBlock, 0,
                  w.stream, w.graph(), w.pull_rec.ptr, w.pull_ext.ptr, ul, nul, w.su32[0].ptr,
                  w.su32[1].ptr, w.su32[2].ptr,
                  w.su32[3].ptr, next_label, mark_preds ? 1 : 0, c.owner_view(), emit ? 1 : 0,
@@ -1531,7 +1536,7 @@ class DobfsGraphRunner {
     MGB_LAUNCH(frontier_diff_kernel, grid_for(nw, 256, num_sms() * 8), 256, 0, s, w.su32[2].ptr,
                w.aux[4].ptr, w.su32[3].ptr, (uint32_t)nw, cnts, nullptr, 0ull,
                (const DobfsLoop*)st, &ctr->edges);
-    MGB_LAUNCH(dobfs_pull_thread_kernel<false>, num_sms() * MG_PULL_OCC, 256, 0, s, gv, w.pull_rec.ptr,
+    MGB_LAUNCH(dobfs_pull_thread_kernel<false>, num_sms() * kPullCtas, kPullBlock, 0, s, gv, w.pull_rec.ptr,
                w.pull_ext.ptr, nullptr, 0u,
                w.su32[0].ptr, w.su32[1].ptr, w.su32[2].ptr, w.su32[3].ptr, 0u, mp, ow, 0,
                w.loop_front[1].ptr, nullptr, &ctr->misc, w.ul_buf[2].ptr, cnts + 1, ctr,
@@ -1913,7 +1918,7 @@ class DobfsMpGraphRunner {
     MGB_LAUNCH(frontier_diff_kernel, grid_for(nw, 256, num_sms() * 8), 256, 0, s, w.su32[2].ptr,
                w.aux[4].ptr, w.su32[3].ptr, (uint32_t)nw, cnts, nullptr, 0ull, &st->b,
                &ctr->edges);
-    MGB_LAUNCH(dobfs_pull_thread_kernel<true>, num_sms() * MG_PULL_OCC, 256, 0, s, gv,
+    MGB_LAUNCH(dobfs_pull_thread_kernel<true>, num_sms() * kPullCtas, kPullBlock, 0, s, gv,
                w.pull_rec.ptr, w.pull_ext.ptr, nullptr, 0u, w.su32[0].ptr, w.su32[1].ptr, w.su32[2].ptr,
                w.su32[3].ptr, 0u, 0, ow, 1, w.output.ptr, nullptr, &ctr->misc, w.ul_buf[2].ptr,
                cnts + 1, ctr, (unsigned long long*)nullptr, (unsigned long long*)nullptr, dyn);
