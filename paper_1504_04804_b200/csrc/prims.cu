@@ -1604,7 +1604,8 @@ class DobfsGraphRunner {
 //   convergence: Σ next frontiers == 0, E:784-820)
 // — runs inside ONE graph launch: a WHILE node whose body holds two
 // supersteps (even / odd, so the frontier ping-pong buffers and the inbox
-// parity are fixed in each), the second behind an IF on "not converged".  No
+// parity are fixed in each); the second one's decide kernel turns all of it
+// off once the first converged (conditionals nest two levels deep).  No
 // superstep waits for the host; every rank takes the same decisions from the
 // same all-gathered reports.  Results and statistics equal the host loop's
 // (tests/test_fabric.py::test_dobfs_device_loop_*).
@@ -1615,6 +1616,7 @@ struct DobfsMpLoop {
   DobfsLoop b;  // first: the pull / frontier kernels read it as a DobfsLoop
   uint32_t n, me, epoch, overflow;
   uint32_t own_next;               // this rank's next frontier (global discoveries)
+  uint32_t more;                   // the loop continues after the last end kernel
   unsigned long long own_next_deg;
 };
 struct DobfsMpHist {
@@ -1638,9 +1640,20 @@ __global__ void dobfs_mp_init_kernel(DobfsMpLoop* st, uint32_t* labels, uint32_t
   st->overflow = 0;
 }
 
+// (h_rest: the odd superstep's exchange-and-report IF, 0 for the even one;
+// an odd superstep after convergence runs nothing)
 __global__ void dobfs_mp_decide_kernel(DobfsMpLoop* st, DobfsMpHist* hist, const Mailbox* mine,
                                        cudaGraphConditionalHandle h_pull,
-                                       cudaGraphConditionalHandle h_push) {
+                                       cudaGraphConditionalHandle h_push,
+                                       cudaGraphConditionalHandle h_rest) {
+  if (h_rest) {
+    cudaGraphSetConditional(h_rest, st->more ? 1u : 0u);
+    if (!st->more) {
+      cudaGraphSetConditional(h_pull, 0u);
+      cudaGraphSetConditional(h_push, 0u);
+      return;
+    }
+  }
   DobfsLoop& b = st->b;
   const uint32_t t = b.iter;
   st->epoch += 1;  // the host loop's ++mp_epoch at the top of a superstep
@@ -1693,8 +1706,7 @@ __global__ void dobfs_mp_pre_report_kernel(DobfsMpLoop* st, Counters* ctr) {
 }
 
 __global__ void dobfs_mp_end_kernel(DobfsMpLoop* st, const Mailbox* mine, DobfsMpHist* hist,
-                                    const uint32_t* err, cudaGraphConditionalHandle h_next,
-                                    cudaGraphConditionalHandle h_while) {
+                                    const uint32_t* err, cudaGraphConditionalHandle h_while) {
   DobfsLoop& b = st->b;
   const uint32_t t = b.iter, slot = st->epoch & 1u, n = st->n;
   unsigned long long out = 0, next = 0, edges = 0, comb = 0;
@@ -1719,7 +1731,7 @@ __global__ void dobfs_mp_end_kernel(DobfsMpLoop* st, const Mailbox* mine, DobfsM
   st->overflow |= ovf;
   const bool more = next > 0 && t + 1 < b.max_supersteps && t + 1 < kMpHist && !ovf &&
                     !*reinterpret_cast<const volatile uint32_t*>(err);
-  if (h_next) cudaGraphSetConditional(h_next, more ? 1u : 0u);
+  st->more = more ? 1u : 0u;
   cudaGraphSetConditional(h_while, more ? 1u : 0u);
 }
 
@@ -1865,9 +1877,13 @@ class DobfsMpGraphRunner {
   }
 
   // one superstep at a fixed parity into graph g; returns its leaf nodes
+  // one superstep at a fixed parity into graph g, after the nodes `deps`
+  // (none: the graph's roots); the odd superstep's exchange-and-report part
+  // sits in its own IF node, so no conditional nests deeper than two levels
+  // (WHILE -> IF).  Returns the superstep's leaf nodes.
   static std::vector<cudaGraphNode_t> substep(Plan& P, Worker& w, Ctx& c, const DenseView& dv,
                                               bool st_exact, cudaGraph_t g, int parity,
-                                              cudaGraphConditionalHandle h_next,
+                                              const std::vector<cudaGraphNode_t>& deps,
                                               cudaGraphConditionalHandle h_while,
                                               uint64_t& n_pull, uint64_t& n_push,
                                               uint64_t& n_fixed) {
@@ -1888,14 +1904,17 @@ class DobfsMpGraphRunner {
     uint32_t* nxt = parity == 0 ? w.input.ptr : w.next_input.ptr;
     DobfsDev f{w.su32[0].ptr, w.su32[1].ptr, w.su32[2].ptr, w.su32[3].ptr, ow, 0u, 0,
                &st->b.iter};
-    cudaGraphConditionalHandle h_pull, h_push;
+    cudaGraphConditionalHandle h_pull, h_push, h_rest = 0;
     MGB_CUDA(cudaGraphConditionalHandleCreate(&h_pull, g, 0, cudaGraphCondAssignDefault));
     MGB_CUDA(cudaGraphConditionalHandleCreate(&h_push, g, 0, cudaGraphCondAssignDefault));
+    if (parity == 1)
+      MGB_CUDA(cudaGraphConditionalHandleCreate(&h_rest, g, 0, cudaGraphCondAssignDefault));
     cudaGraph_t tmp;
     const uint64_t l0 = g_launches.load();
     // decide
-    MGB_CUDA(cudaStreamBeginCaptureToGraph(s, g, nullptr, nullptr, 0, cudaStreamCaptureModeRelaxed));
-    MGB_LAUNCH(dobfs_mp_decide_kernel, 1, 1, 0, s, st, hist, mine, h_pull, h_push);
+    MGB_CUDA(cudaStreamBeginCaptureToGraph(s, g, deps.data(), nullptr, deps.size(),
+                                           cudaStreamCaptureModeRelaxed));
+    MGB_LAUNCH(dobfs_mp_decide_kernel, 1, 1, 0, s, st, hist, mine, h_pull, h_push, h_rest);
     std::vector<cudaGraphNode_t> dec = leaves(s);
     MGB_CUDA(cudaStreamEndCapture(s, &tmp));
     cudaGraphNode_t ifs[2];
@@ -1945,8 +1964,22 @@ class DobfsMpGraphRunner {
                w.loop_tiles.ptr, w.output.ptr, &ctr->out_cnt, nin);
     MGB_CUDA(cudaStreamEndCapture(s, &tmp));
     const uint64_t l3 = g_launches.load();
-    // exchange + completion, after both branches
-    MGB_CUDA(cudaStreamBeginCaptureToGraph(s, g, ifs, nullptr, 2, cudaStreamCaptureModeRelaxed));
+    // exchange + completion, after both branches (the odd superstep: inside IF(rest))
+    cudaGraph_t rg = g;
+    cudaGraphNode_t rest_node = nullptr;
+    if (parity == 1) {
+      cudaGraphNodeParams rp = {};
+      rp.type = cudaGraphNodeTypeConditional;
+      rp.conditional.handle = h_rest;
+      rp.conditional.type = cudaGraphCondTypeIf;
+      rp.conditional.size = 1;
+      MGB_CUDA(cudaGraphAddNode(&rest_node, g, ifs, 2, &rp));
+      rg = rp.conditional.phGraph_out[0];
+      MGB_CUDA(cudaStreamBeginCaptureToGraph(s, rg, nullptr, nullptr, 0,
+                                             cudaStreamCaptureModeRelaxed));
+    } else {
+      MGB_CUDA(cudaStreamBeginCaptureToGraph(s, g, ifs, nullptr, 2, cudaStreamCaptureModeRelaxed));
+    }
     // Σdeg of the next frontier, the exact-cost input (reports_deg, E:845)
     const int want_deg = st_exact ? 1 : 0;
     const uint64_t items = w.output.cap > dv.words ? w.output.cap : dv.words;
@@ -1971,9 +2004,10 @@ class DobfsMpGraphRunner {
     MGB_LAUNCH(dobfs_mp_pre_report_kernel, 1, 1, 0, s, st, ctr);
     MGB_LAUNCH(mp_report_kernel, 1, 128, 0, s, ctr, (Counters*)nullptr, HostReportPart{},
                P.mbox_ptrs.ptr, n, P.rank, 0u, (DevReport*)nullptr, err, &st->epoch);
-    MGB_LAUNCH(dobfs_mp_end_kernel, 1, 1, 0, s, st, mine, hist, err, h_next, h_while);
+    MGB_LAUNCH(dobfs_mp_end_kernel, 1, 1, 0, s, st, mine, hist, err, h_while);
     std::vector<cudaGraphNode_t> out = leaves(s);
     MGB_CUDA(cudaStreamEndCapture(s, &tmp));
+    if (rest_node) out.assign(1, rest_node);
     const uint64_t l4 = g_launches.load();
     n_pull = l2 - l1;
     n_push = l3 - l2;
@@ -2003,21 +2037,11 @@ class DobfsMpGraphRunner {
     cudaGraphNode_t wnode;
     MGB_CUDA(cudaGraphAddNode(&wnode, g, nullptr, 0, &wp));
     cudaGraph_t body = wp.conditional.phGraph_out[0];
-    // even superstep, then the odd one behind IF(not converged)
-    cudaGraphConditionalHandle h_odd;
-    MGB_CUDA(cudaGraphConditionalHandleCreate(&h_odd, body, 0, cudaGraphCondAssignDefault));
+    // even superstep, then the odd one (a no-op once the even one converged)
     uint64_t np, nq, nf;
     std::vector<cudaGraphNode_t> tail =
-        substep(P, w, c, dv, prim.exact_cost, body, 0, h_odd, h_while, np, nq, nf);
-    cudaGraphNodeParams ip = {};
-    ip.type = cudaGraphNodeTypeConditional;
-    ip.conditional.handle = h_odd;
-    ip.conditional.type = cudaGraphCondTypeIf;
-    ip.conditional.size = 1;
-    cudaGraphNode_t inode;
-    MGB_CUDA(cudaGraphAddNode(&inode, body, tail.data(), tail.size(), &ip));
-    substep(P, w, c, dv, prim.exact_cost, ip.conditional.phGraph_out[0], 1, 0, h_while, np, nq,
-            nf);
+        substep(P, w, c, dv, prim.exact_cost, body, 0, {}, h_while, np, nq, nf);
+    substep(P, w, c, dv, prim.exact_cost, body, 1, tail, h_while, np, nq, nf);
     g_launches.store(launches0);  // capture is not execution
     MGB_CUDA(cudaGraphInstantiate(&w.mp_exec, g, 0));
     MGB_CUDA(cudaGraphDestroy(g));
