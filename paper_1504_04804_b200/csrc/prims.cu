@@ -451,7 +451,13 @@ static_assert(kPullMid == 8, "stage 1b takes arcs 2-9 from the 32-byte record ex
 #define MG_MID_WAVE 5
 #endif
 constexpr int kMidWave = MG_MID_WAVE;  // stage-1b probes in the first wave (3: 7.26 ms, 5: 7.17, 8: 7.31)
-constexpr uint32_t kPullStart = kPullK + kPullMid;
+#ifndef MG_EXT2
+#define MG_EXT2 1  // 7.36 -> 7.30 ms over the bench sources (source 8582448: 1.13 -> 1.08)
+#endif
+// MG_EXT2: a second extension sector (arcs 10..17), read only by rows that
+// arcs 2..9 did not settle
+constexpr int kExtSlots = MG_EXT2 ? 4 : 2;  // uint4 per record extension
+constexpr uint32_t kPullStart = kPullK + kPullMid + (MG_EXT2 ? 8 : 0);
 // (measured: stage 1b as its own kernel over the long-row queue, one row per
 // thread and no CTA barrier, is slower — 8.93 -> 10.61 ms over the bench
 // sources — the inline stage reuses the record already in registers)
@@ -480,11 +486,15 @@ __global__ void pull_ext_kernel(GraphView g, const uint32_t* __restrict__ ni, ui
   for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
     const uint32_t v = ni[i];
     const uint32_t b = g.off[v], d = g.off[v + 1] - b;
-    uint32_t a[8];
+    for (int q = 0; q < kExtSlots; ++q) {
+      uint32_t a[4];
 #pragma unroll
-    for (int k = 0; k < 8; ++k) a[k] = d > 2u + k ? g.col[b + 2 + k] : kInfLabel;
-    ext[2 * i] = make_uint4(a[0], a[1], a[2], a[3]);
-    ext[2 * i + 1] = make_uint4(a[4], a[5], a[6], a[7]);
+      for (int k = 0; k < 4; ++k) {
+        const uint32_t arc = 2u + 4u * q + k;
+        a[k] = d > arc ? g.col[b + arc] : kInfLabel;
+      }
+      ext[(uint64_t)kExtSlots * i + q] = make_uint4(a[0], a[1], a[2], a[3]);
+    }
   }
 }
 
@@ -666,8 +676,8 @@ __global__ void __launch_bounds__(kPullBlock, kPullCtas)
         // the record again (L1/L2) and its 32-byte extension (arcs 2-9), both
         // addressed by the position: no offset load, no col_indices sector
         const uint4 rr = act ? rec[p] : make_uint4(0, 0, 0, 0);
-        const uint4 ex = act ? __ldcs(&ext[2 * p]) : make_uint4(0, 0, 0, 0);
-        const uint4 ex2 = act ? __ldcs(&ext[2 * p + 1]) : make_uint4(0, 0, 0, 0);
+        const uint4 ex = act ? __ldcs(&ext[(uint64_t)kExtSlots * p]) : make_uint4(0, 0, 0, 0);
+        const uint4 ex2 = act ? __ldcs(&ext[(uint64_t)kExtSlots * p + 1]) : make_uint4(0, 0, 0, 0);
         uint32_t v = rr.x;
         const uint32_t d = rr.y;
         const uint32_t e = d < kPullStart ? d : kPullStart;
@@ -691,6 +701,22 @@ __global__ void __launch_bounds__(kPullBlock, kPullCtas)
             f = k;
             pw = wv[k];
           }
+#if MG_EXT2
+        if (f < 0 && act && d > kPullK + kPullMid) {  // arcs 10..17 from the second sector
+          const uint4 e3 = __ldcs(&ext[(uint64_t)kExtSlots * p + 2]);
+          const uint4 e4 = __ldcs(&ext[(uint64_t)kExtSlots * p + 3]);
+          const uint32_t w2[8] = {e3.x, e3.y, e3.z, e3.w, e4.x, e4.y, e4.z, e4.w};
+          bool h2[8];
+#pragma unroll
+          for (int k = 0; k < 8; ++k) h2[k] = kPullK + kPullMid + k < e && bit_set(fb, w2[k]);
+#pragma unroll
+          for (int k = 7; k >= 0; --k)
+            if (h2[k]) {
+              f = kPullMid + k;
+              pw = w2[k];
+            }
+        }
+#endif
         bool fnd = f >= 0;
         bool kp = act && !fnd && d <= kPullStart;
         bool lg = act && !fnd && d > kPullStart;
@@ -1087,7 +1113,7 @@ struct DobfsPrim : PrimBase {
     MGB_CUDA(cudaMemcpy(w.nonisolated.ptr, h.data(), 4ull * k, cudaMemcpyHostToDevice));
     w.n_nonisolated = k;
     w.pull_rec.alloc(k ? k : 1);
-    w.pull_ext.alloc(2ull * (k ? k : 1));
+    w.pull_ext.alloc((uint64_t)kExtSlots * (k ? k : 1));
     if (k) {
       MGB_LAUNCH(pull_records_kernel, grid_for(k, 256, num_sms() * 16), 256, 0, w.stream, w.graph(),
                  w.nonisolated.ptr, k, w.pull_rec.ptr);
