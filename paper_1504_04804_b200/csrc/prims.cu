@@ -977,27 +977,12 @@ __global__ void dobfs_share_kernel(Counters* ctr, int pulled, uint32_t ul_keep) 
 // host-driven path's (tests/test_gpu_parity.py::test_dobfs_graph_*).
 constexpr uint32_t kLoopHist = 65536;  // supersteps recorded per run
 
-__global__ void dobfs_loop_init_kernel(DobfsLoop* st, uint32_t* labels, uint32_t* vis) {
-  const uint32_t s = st->source;
-  labels[s] = 0u;
-  vis[s >> 5] |= 1u << (s & 31);
-  st->iter = 0;
-  st->dir = 0;
-  st->switched = 0;
-  st->physical = 0;
-  st->in_count = 1;
-  st->ul_src = 2;  // every non-isolated record, no list
-  st->ul_len = st->n_nonisolated;
-  st->in_degsum = 0;
-  st->visited = 1;
-  st->prev_physical = 0;
-}
-
-__global__ void dobfs_loop_decide_kernel(DobfsLoop* st, DobfsHist* hist,
-                                         cudaGraphConditionalHandle h_pull,
-                                         cudaGraphConditionalHandle h_push) {
+// the direction of superstep st->iter (primitives.cpp:197-205, the reference
+// rule on global quantities) and the exact-cost physical choice, in the host
+// path's double arithmetic; returns the physical direction (1: pull)
+__device__ uint32_t dobfs_loop_decide(DobfsLoop* st, DobfsHist* hist) {
   const uint32_t t = st->iter;
-  if (t >= 1) {  // primitives.cpp:197-205: decision on global quantities
+  if (t >= 1) {
     st->visited += st->in_count;
     const double fv = st->nv > 0 ? (double)st->in_count * st->ne_d / st->nv_d : 0.0;
     const double bv = st->visited > 0 ? (double)((unsigned long long)st->nv - st->visited) *
@@ -1018,12 +1003,35 @@ __global__ void dobfs_loop_decide_kernel(DobfsLoop* st, DobfsHist* hist,
   hist[t].physical = phys;
   hist[t].pad = 0u;
   if (!phys) st->in_count = 0;  // the push recounts its list from the bitmap
-  cudaGraphSetConditional(h_pull, phys);
-  cudaGraphSetConditional(h_push, phys ? 0u : 1u);
+  return phys;
+}
+
+// superstep 0 is always a push: its decision is taken here, before the graph
+// (the graph's IF handles default to push at every launch); every later
+// decision is taken by the end kernel of the superstep before it, so a
+// superstep costs no separate decide launch
+__global__ void dobfs_loop_init_kernel(DobfsLoop* st, DobfsHist* hist, uint32_t* labels,
+                                       uint32_t* vis) {
+  const uint32_t s = st->source;
+  labels[s] = 0u;
+  vis[s >> 5] |= 1u << (s & 31);
+  st->iter = 0;
+  st->dir = 0;
+  st->switched = 0;
+  st->physical = 0;
+  st->in_count = 1;
+  st->ul_src = 2;  // every non-isolated record, no list
+  st->ul_len = st->n_nonisolated;
+  st->in_degsum = 0;
+  st->visited = 1;
+  st->prev_physical = 0;
+  dobfs_loop_decide(st, hist);
 }
 
 __global__ void dobfs_loop_end_kernel(DobfsLoop* st, Counters* ctr, DobfsHist* hist,
-                                      cudaGraphConditionalHandle h_while) {
+                                      cudaGraphConditionalHandle h_while,
+                                      cudaGraphConditionalHandle h_pull,
+                                      cudaGraphConditionalHandle h_push) {
   __shared__ uint32_t s_out;
   const uint32_t t = st->iter;
   if (threadIdx.x == 0) {
@@ -1046,6 +1054,11 @@ __global__ void dobfs_loop_end_kernel(DobfsLoop* st, Counters* ctr, DobfsHist* h
     st->iter = t + 1;
     const bool more = s_out > 0 && t + 1 < st->max_supersteps && t + 1 < kLoopHist;
     cudaGraphSetConditional(h_while, more ? 1u : 0u);
+    if (more) {  // the next superstep's direction
+      const uint32_t phys = dobfs_loop_decide(st, hist);
+      cudaGraphSetConditional(h_pull, phys);
+      cudaGraphSetConditional(h_push, phys ? 0u : 1u);
+    }
   }
 }
 
@@ -1409,7 +1422,8 @@ class DobfsGraphRunner {
     MGB_CUDA(cudaMemsetAsync(w.aux[4].ptr, 0, 4 * nw, w.stream));           // visited (prev)
     if (mark_preds) MGB_CUDA(cudaMemsetAsync(w.su32[1].ptr, 0xFF, 4ull * w.nv, w.stream));
     MGB_LAUNCH(dobfs_loop_init_kernel, 1, 1, 0, w.stream,
-               reinterpret_cast<DobfsLoop*>(w.loop_state.ptr), w.su32[0].ptr, w.su32[2].ptr);
+               reinterpret_cast<DobfsLoop*>(w.loop_state.ptr),
+               reinterpret_cast<DobfsHist*>(w.loop_hist.ptr), w.su32[0].ptr, w.su32[2].ptr);
     MGB_CUDA(cudaGraphLaunch(G.exec, w.stream));
     dobfs_labels_end(w, nw);
     MGB_CUDA(cudaEventRecord(w.ev_end, w.stream));
@@ -1427,7 +1441,7 @@ class DobfsGraphRunner {
       r.edges.push_back(e.edges);
       r.out.push_back(e.out);
       W += e.edges;
-      launches += 2 + (e.physical ? G.n_pull : G.n_push);
+      launches += 1 + (e.physical ? G.n_pull : G.n_push);  // end kernel + branch
     }
     r.launches = launches;
     const bool hit_cap = S >= kLoopHist && cfg.max_supersteps > kLoopHist && S && r.out.back();
@@ -1523,20 +1537,12 @@ class DobfsGraphRunner {
     cudaGraphNode_t wnode;
     MGB_CUDA(cudaGraphAddNode(&wnode, g, nullptr, 0, &wp));
     cudaGraph_t body = wp.conditional.phGraph_out[0];
+    // superstep 0 is a push (the defaults, assigned at every launch); the end
+    // kernel sets the next superstep's direction
     cudaGraphConditionalHandle h_pull, h_push;
     MGB_CUDA(cudaGraphConditionalHandleCreate(&h_pull, body, 0, cudaGraphCondAssignDefault));
-    MGB_CUDA(cudaGraphConditionalHandleCreate(&h_push, body, 0, cudaGraphCondAssignDefault));
-    // decide
-    MGB_CUDA(cudaStreamBeginCaptureToGraph(s, body, nullptr, nullptr, 0,
-                                           cudaStreamCaptureModeRelaxed));
-    MGB_LAUNCH(dobfs_loop_decide_kernel, 1, 1, 0, s, st, hist, h_pull, h_push);
+    MGB_CUDA(cudaGraphConditionalHandleCreate(&h_push, body, 1, cudaGraphCondAssignDefault));
     cudaGraph_t tmp;
-    MGB_CUDA(cudaStreamEndCapture(s, &tmp));
-    size_t nn = 0;
-    MGB_CUDA(cudaGraphGetNodes(body, nullptr, &nn));
-    std::vector<cudaGraphNode_t> nodes(nn);
-    MGB_CUDA(cudaGraphGetNodes(body, nodes.data(), &nn));
-    cudaGraphNode_t decide = nodes[0];
     // IF pull / IF push
     cudaGraphNode_t ifs[2];
     cudaGraph_t bodies[2];
@@ -1547,7 +1553,7 @@ class DobfsGraphRunner {
       ip.conditional.handle = hs[i];
       ip.conditional.type = cudaGraphCondTypeIf;
       ip.conditional.size = 1;
-      MGB_CUDA(cudaGraphAddNode(&ifs[i], body, &decide, 1, &ip));
+      MGB_CUDA(cudaGraphAddNode(&ifs[i], body, nullptr, 0, &ip));
       bodies[i] = ip.conditional.phGraph_out[0];
     }
     GraphView gv = w.graph();
@@ -1604,7 +1610,7 @@ class DobfsGraphRunner {
     // end (after both branches)
     MGB_CUDA(cudaStreamBeginCaptureToGraph(s, body, ifs, nullptr, 2,
                                            cudaStreamCaptureModeRelaxed));
-    MGB_LAUNCH(dobfs_loop_end_kernel, 1, 256, 0, s, st, ctr, hist, h_while);
+    MGB_LAUNCH(dobfs_loop_end_kernel, 1, 256, 0, s, st, ctr, hist, h_while, h_pull, h_push);
     MGB_CUDA(cudaStreamEndCapture(s, &tmp));
     g_launches.store(l0);  // capture is not execution
     MGB_CUDA(cudaGraphInstantiate(&w.loop_exec[gi], g, 0));
