@@ -240,7 +240,7 @@ def _gpu_worker_dobfs_loop(rank, world, port, q, scale):
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("world,scale", [(2, 12), (3, 11)])
+@pytest.mark.parametrize("world,scale", [(2, 12), (3, 11), (4, 10)])
 def test_dobfs_device_loop_equals_host_loop(world, scale):
     """the whole superstep loop on the device (decide, pull / push, pack,
     publish, merge, report all-gather, convergence) gives the host loop's
