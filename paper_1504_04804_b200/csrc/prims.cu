@@ -628,20 +628,18 @@ __global__ void __launch_bounds__(kPullBlock, kPullCtas)
     for (int j = 0; j < kPV; ++j) {
       const uint32_t v = r[j].x, d = r[j].y;
       vv[j] = v;
-      found[j] = open[j] && (h0[j] || h1[j]);
-      keep[j] = open[j] && !found[j] && d <= (uint32_t)kPullK;
-      lng[j] = open[j] && !found[j] && d > (uint32_t)kPullK;
+      const bool f = open[j] && (h0[j] || h1[j]);
+      found[j] = f;
+      keep[j] = open[j] && !f && d <= (uint32_t)kPullK;
+      lng[j] = open[j] && !f && d > (uint32_t)kPullK;
+      // counters without branches; one branch for the discovery's stores
       opened += open[j];
-      if (found[j]) {
-        scanned += h0[j] ? 1 : 2;
+      found_n += f;
+      degs += f ? d : 0u;
+      scanned += f ? (h0[j] ? 1u : 2u) : (open[j] ? min(d, (uint32_t)kPullK) : 0u);
+      if (f) {
         __stcs(&labels[v], next_label);
         if (mark_preds) preds[v] = ow.to_global(h0[j] ? r[j].z : r[j].w);
-        ++found_n;
-        degs += d;
-      } else if (open[j]) {
-        scanned += d < (uint32_t)kPullK ? d : (uint32_t)kPullK;
-      }
-      if (found[j]) {
         if (inwin) atomicOr(&nwin[(v >> 5) - w0], 1u << (v & 31));
         else atomicOr(&vis[v >> 5], 1u << (v & 31));
       }
