@@ -718,16 +718,12 @@ __global__ void __launch_bounds__(kPullBlock, kPullCtas)
         bool fnd = f >= 0;
         bool kp = act && !fnd && d <= kPullStart;
         bool lg = act && !fnd && d > kPullStart;
+        scanned += fnd ? (uint32_t)(f + 1) : (act ? e - kPullK : 0u);
+        found_n += fnd;
+        degs += fnd ? d : 0u;
         if (fnd) {
-          scanned += f + 1;
           __stcs(&labels[v], next_label);
           if (mark_preds) preds[v] = ow.to_global(pw);
-          ++found_n;
-          degs += d;
-        } else if (act) {
-          scanned += e - kPullK;
-        }
-        if (fnd) {
           if (inwin) atomicOr(&nwin[(v >> 5) - w0], 1u << (v & 31));
           else atomicOr(&vis[v >> 5], 1u << (v & 31));
         }
