@@ -908,7 +908,11 @@ __global__ void __launch_bounds__(256)
 // per round 256 words, a CTA scan of their popcounts, one atomic per round
 __global__ void __launch_bounds__(256)
     bitmap_diff_list_kernel(const uint32_t* __restrict__ vis, uint32_t* prev, uint32_t nw,
-                            uint32_t* out, uint32_t* cnt, int set_prev = 0) {
+                            uint32_t* out, uint32_t* cnt, int set_prev = 0,
+                            const DobfsLoop* st = nullptr) {
+  // device-driven loop, superstep 0: the list is the source, seeded by the
+  // init kernel together with prev (no 8 MB bitmap pass for one vertex)
+  if (st && st->iter == 0) return;
   __shared__ uint32_t s_warp[8];
   __shared__ uint32_t s_base;
   const uint32_t lane = lane_id(), warp = threadIdx.x >> 5;
@@ -996,7 +1000,7 @@ __device__ uint32_t dobfs_loop_decide(DobfsLoop* st, DobfsHist* hist) {
   hist[t].dir = st->dir;
   hist[t].physical = phys;
   hist[t].pad = 0u;
-  if (!phys) st->in_count = 0;  // the push recounts its list from the bitmap
+  if (!phys && t > 0) st->in_count = 0;  // the push recounts its list from the bitmap
   return phys;
 }
 
@@ -1005,10 +1009,12 @@ __device__ uint32_t dobfs_loop_decide(DobfsLoop* st, DobfsHist* hist) {
 // decision is taken by the end kernel of the superstep before it, so a
 // superstep costs no separate decide launch
 __global__ void dobfs_loop_init_kernel(DobfsLoop* st, DobfsHist* hist, uint32_t* labels,
-                                       uint32_t* vis) {
+                                       uint32_t* vis, uint32_t* prev, uint32_t* front) {
   const uint32_t s = st->source;
   labels[s] = 0u;
   vis[s >> 5] |= 1u << (s & 31);
+  prev[s >> 5] |= 1u << (s & 31);  // superstep 0's list is seeded here (prev = vis)
+  front[0] = s;
   st->iter = 0;
   st->dir = 0;
   st->switched = 0;
@@ -1417,7 +1423,8 @@ class DobfsGraphRunner {
     if (mark_preds) MGB_CUDA(cudaMemsetAsync(w.su32[1].ptr, 0xFF, 4ull * w.nv, w.stream));
     MGB_LAUNCH(dobfs_loop_init_kernel, 1, 1, 0, w.stream,
                reinterpret_cast<DobfsLoop*>(w.loop_state.ptr),
-               reinterpret_cast<DobfsHist*>(w.loop_hist.ptr), w.su32[0].ptr, w.su32[2].ptr);
+               reinterpret_cast<DobfsHist*>(w.loop_hist.ptr), w.su32[0].ptr, w.su32[2].ptr,
+               w.aux[4].ptr, w.loop_front[0].ptr);
     MGB_CUDA(cudaGraphLaunch(G.exec, w.stream));
     dobfs_labels_end(w, nw);
     MGB_CUDA(cudaEventRecord(w.ev_end, w.stream));
@@ -1578,13 +1585,9 @@ class DobfsGraphRunner {
     // push branch: frontier list from the bitmap, prev = vis, edge-balanced advance
     MGB_CUDA(cudaStreamBeginCaptureToGraph(s, bodies[1], nullptr, nullptr, 0,
                                            cudaStreamCaptureModeRelaxed));
-#ifndef MG_DIFF_FUSE
-#define MG_DIFF_FUSE 1
-#endif
     MGB_LAUNCH(bitmap_diff_list_kernel, grid_for(nw, 256, num_sms() * 8), 256, 0, s, w.su32[2].ptr,
-               w.aux[4].ptr, (uint32_t)nw, w.loop_front[0].ptr, &st->in_count, MG_DIFF_FUSE);
-    if (!MG_DIFF_FUSE)
-      MGB_CUDA(cudaMemcpyAsync(w.aux[4].ptr, w.su32[2].ptr, 4 * nw, cudaMemcpyDeviceToDevice, s));
+               w.aux[4].ptr, (uint32_t)nw, w.loop_front[0].ptr, &st->in_count, 1,
+               (const DobfsLoop*)st);
     const uint32_t* nin = &st->in_count;
     MGB_LAUNCH(lb_degree_kernel, num_sms() * 8, kLbBlock, 0, s, w.off.ptr, w.loop_front[0].ptr, 0u,
                w.loop_lb_row.ptr, w.loop_lb_pref.ptr, w.loop_lb_bsum.ptr, nin);
