@@ -223,7 +223,8 @@ struct DobfsLoop {
   uint32_t iter, dir, switched, physical;
   uint32_t in_count, ul_src, ul_len, n_nonisolated;
   unsigned long long in_degsum, visited;
-  uint32_t prev_physical, pad_;  // the last superstep was a pull (its list is clean)
+  uint32_t prev_physical;        // the last superstep was a pull (its list is clean)
+  uint32_t end_ticket;           // CTAs of a branch's last kernel that finished
 };
 struct DobfsHist {
   uint32_t dir, physical, out, pad;
@@ -236,6 +237,135 @@ struct DobfsDyn {
   uint32_t* ub0;
   uint32_t* ub1;
 };
+
+constexpr uint32_t kLoopHist = 65536;  // supersteps recorded per run
+
+// the direction of superstep st->iter (primitives.cpp:197-205, the reference
+// rule on global quantities) and the exact-cost physical choice, in the host
+// path's double arithmetic; returns the physical direction (1: pull)
+__device__ uint32_t dobfs_loop_decide(DobfsLoop* st, DobfsHist* hist) {
+  const uint32_t t = st->iter;
+  if (t >= 1) {
+    st->visited += st->in_count;
+    const double fv = st->nv > 0 ? (double)st->in_count * st->ne_d / st->nv_d : 0.0;
+    const double bv = st->visited > 0 ? (double)((unsigned long long)st->nv - st->visited) *
+                                            st->nv_d / (double)st->visited
+                                      : 0.0;
+    uint32_t next;
+    if (st->dir == 0) next = (!st->switched && fv > bv * st->do_a) ? 1u : 0u;
+    else next = fv < bv * st->do_b ? 0u : 1u;
+    if (next == 1 && st->dir == 0) st->switched = 1;
+    st->dir = next;
+  }
+  uint32_t phys = st->dir == 1;
+  if (!phys && st->exact && t > 0 && st->in_count &&
+      (double)st->in_degsum > st->pull_ratio * st->ul_len)
+    phys = 1;
+  st->physical = phys;
+  hist[t].dir = st->dir;
+  hist[t].physical = phys;
+  hist[t].pad = 0u;
+  if (!phys && t > 0) st->in_count = 0;  // the push recounts its list from the bitmap
+  return phys;
+}
+
+// superstep 0 is always a push: its decision is taken here, before the graph
+// (the graph's IF handles default to push at every launch); every later
+// decision is taken by the end kernel of the superstep before it, so a
+// superstep costs no separate decide launch
+__global__ void dobfs_loop_init_kernel(DobfsLoop* st, DobfsHist* hist, uint32_t* labels,
+                                       uint32_t* vis, uint32_t* prev, uint32_t* front) {
+  const uint32_t s = st->source;
+  labels[s] = 0u;
+  vis[s >> 5] |= 1u << (s & 31);
+  prev[s >> 5] |= 1u << (s & 31);  // superstep 0's list is seeded here (prev = vis)
+  front[0] = s;
+  st->iter = 0;
+  st->dir = 0;
+  st->switched = 0;
+  st->physical = 0;
+  st->in_count = 1;
+  st->ul_src = 2;  // every non-isolated record, no list
+  st->ul_len = st->n_nonisolated;
+  st->in_degsum = 0;
+  st->visited = 1;
+  st->prev_physical = 0;
+  dobfs_loop_decide(st, hist);
+}
+
+// end of a device-driven superstep (the whole CTA): history, loop state,
+// counters cleared, loop condition, the next superstep's direction
+__device__ void dobfs_loop_end_cta(DobfsLoop* st, Counters* ctr, DobfsHist* hist,
+                                   cudaGraphConditionalHandle h_while,
+                                   cudaGraphConditionalHandle h_pull,
+                                   cudaGraphConditionalHandle h_push) {
+  __shared__ uint32_t s_out;
+  const uint32_t t = st->iter;
+  if (threadIdx.x == 0) {
+    const uint32_t out = ctr->out_cnt;
+    s_out = out;
+    hist[t].out = out;
+    hist[t].edges = ctr->edges;
+    if (st->physical) {  // the pull compacted the unvisited list (ping-pong)
+      st->ul_len = ctr->misc;
+      st->ul_src = st->ul_src == 0 ? 1 : 0;
+    }
+    st->prev_physical = st->physical;
+    st->in_count = out;
+    st->in_degsum = ctr->next_deg;
+  }
+  __syncthreads();
+  uint32_t* c = reinterpret_cast<uint32_t*>(ctr);
+  for (uint32_t i = threadIdx.x; i < sizeof(Counters) / 4; i += blockDim.x) c[i] = 0u;
+  if (threadIdx.x == 0) {
+    st->iter = t + 1;
+    const bool more = s_out > 0 && t + 1 < st->max_supersteps && t + 1 < kLoopHist;
+    cudaGraphSetConditional(h_while, more ? 1u : 0u);
+    if (more) {  // the next superstep's direction
+      const uint32_t phys = dobfs_loop_decide(st, hist);
+      cudaGraphSetConditional(h_pull, phys);
+      cudaGraphSetConditional(h_push, phys ? 0u : 1u);
+    }
+  }
+}
+
+// the superstep end folded into the last kernel of each branch: the last CTA
+// to finish (atomic ticket) runs it, so a superstep needs no end launch
+struct DobfsLoopEnd {
+  DobfsLoop* st = nullptr;
+  DobfsHist* hist = nullptr;
+  cudaGraphConditionalHandle h_while = 0, h_pull = 0, h_push = 0;
+};
+
+__device__ void dobfs_loop_end_last_cta(const DobfsLoopEnd& le, Counters* ctr) {
+  __shared__ uint32_t s_last;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    s_last = atomicAdd(&le.st->end_ticket, 1u) == gridDim.x - 1;
+  }
+  __syncthreads();
+  if (!s_last) return;
+  __threadfence();
+  if (threadIdx.x == 0) le.st->end_ticket = 0u;
+  dobfs_loop_end_cta(le.st, ctr, le.hist, le.h_while, le.h_pull, le.h_push);
+}
+
+// push branch's last kernel: the degree sum of the discoveries, then the end
+__global__ void __launch_bounds__(256)
+    dobfs_degsum_end_kernel(GraphView g, const uint32_t* __restrict__ in, Counters* ctr,
+                            DobfsLoopEnd le) {
+  const uint32_t n = ctr->out_cnt;
+  unsigned long long d = 0;
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    const uint32_t v = in[i];
+    d += g.off[v + 1] - g.off[v];
+  }
+  unsigned long long* const dst[1] = {&ctr->next_deg};
+  const uint64_t val[1] = {d};
+  block_add_u64<1>(dst, val);
+  dobfs_loop_end_last_cta(le, ctr);
+}
 
 struct DobfsDev {
   uint32_t* labels;
@@ -791,7 +921,7 @@ __global__ void __launch_bounds__(256)
                             OwnerView ow, int emit_found, uint32_t* out, uint32_t* ul_out,
                             uint32_t* ul_out_cnt, Counters* ctr,
                             unsigned long long* scanned_out, unsigned long long* deg_out,
-                            DobfsDyn dyn) {
+                            DobfsDyn dyn, DobfsLoopEnd le = {}) {
   if (dyn.st) {
     ul_out = dyn.st->ul_src == 0 ? dyn.ub1 : dyn.ub0;
     next_label = dyn.st->iter + 1;
@@ -801,8 +931,12 @@ __global__ void __launch_bounds__(256)
   unsigned long long degs = 0;
   __shared__ uint32_t s_found;
   const uint32_t nl = *long_cnt;
-  // CTAs past the queue leave at once (an empty stage used to cost ~5 us)
-  if (blockIdx.x * (256 / kPullGroup * kGroupIters) >= nl) return;
+  // CTAs past the queue leave at once (an empty stage used to cost ~5 us);
+  // with the superstep end folded in they only take their ticket
+  if (blockIdx.x * (256 / kPullGroup * kGroupIters) >= nl) {
+    if (le.st) dobfs_loop_end_last_cta(le, ctr);
+    return;
+  }
   const unsigned lane = threadIdx.x & 31u;
   const unsigned sub = lane & (kPullGroup - 1);
   const unsigned gbase = lane & ~(kPullGroup - 1);
@@ -901,6 +1035,7 @@ __global__ void __launch_bounds__(256)
   unsigned long long* const dst[2] = {scanned_out, deg_out};
   const uint64_t val[2] = {scanned, degs};
   block_add_u64<2>(dst, val);
+  if (le.st) dobfs_loop_end_last_cta(le, ctr);
 }
 
 // frontier list = vis & ~prev (the vertices discovered in the previous
@@ -973,94 +1108,6 @@ __global__ void dobfs_share_kernel(Counters* ctr, int pulled, uint32_t ul_keep) 
 //   end     (history, loop state, counters cleared, loop condition)
 // so no superstep waits for the host.  Results and statistics equal the
 // host-driven path's (tests/test_gpu_parity.py::test_dobfs_graph_*).
-constexpr uint32_t kLoopHist = 65536;  // supersteps recorded per run
-
-// the direction of superstep st->iter (primitives.cpp:197-205, the reference
-// rule on global quantities) and the exact-cost physical choice, in the host
-// path's double arithmetic; returns the physical direction (1: pull)
-__device__ uint32_t dobfs_loop_decide(DobfsLoop* st, DobfsHist* hist) {
-  const uint32_t t = st->iter;
-  if (t >= 1) {
-    st->visited += st->in_count;
-    const double fv = st->nv > 0 ? (double)st->in_count * st->ne_d / st->nv_d : 0.0;
-    const double bv = st->visited > 0 ? (double)((unsigned long long)st->nv - st->visited) *
-                                            st->nv_d / (double)st->visited
-                                      : 0.0;
-    uint32_t next;
-    if (st->dir == 0) next = (!st->switched && fv > bv * st->do_a) ? 1u : 0u;
-    else next = fv < bv * st->do_b ? 0u : 1u;
-    if (next == 1 && st->dir == 0) st->switched = 1;
-    st->dir = next;
-  }
-  uint32_t phys = st->dir == 1;
-  if (!phys && st->exact && t > 0 && st->in_count &&
-      (double)st->in_degsum > st->pull_ratio * st->ul_len)
-    phys = 1;
-  st->physical = phys;
-  hist[t].dir = st->dir;
-  hist[t].physical = phys;
-  hist[t].pad = 0u;
-  if (!phys && t > 0) st->in_count = 0;  // the push recounts its list from the bitmap
-  return phys;
-}
-
-// superstep 0 is always a push: its decision is taken here, before the graph
-// (the graph's IF handles default to push at every launch); every later
-// decision is taken by the end kernel of the superstep before it, so a
-// superstep costs no separate decide launch
-__global__ void dobfs_loop_init_kernel(DobfsLoop* st, DobfsHist* hist, uint32_t* labels,
-                                       uint32_t* vis, uint32_t* prev, uint32_t* front) {
-  const uint32_t s = st->source;
-  labels[s] = 0u;
-  vis[s >> 5] |= 1u << (s & 31);
-  prev[s >> 5] |= 1u << (s & 31);  // superstep 0's list is seeded here (prev = vis)
-  front[0] = s;
-  st->iter = 0;
-  st->dir = 0;
-  st->switched = 0;
-  st->physical = 0;
-  st->in_count = 1;
-  st->ul_src = 2;  // every non-isolated record, no list
-  st->ul_len = st->n_nonisolated;
-  st->in_degsum = 0;
-  st->visited = 1;
-  st->prev_physical = 0;
-  dobfs_loop_decide(st, hist);
-}
-
-__global__ void dobfs_loop_end_kernel(DobfsLoop* st, Counters* ctr, DobfsHist* hist,
-                                      cudaGraphConditionalHandle h_while,
-                                      cudaGraphConditionalHandle h_pull,
-                                      cudaGraphConditionalHandle h_push) {
-  __shared__ uint32_t s_out;
-  const uint32_t t = st->iter;
-  if (threadIdx.x == 0) {
-    const uint32_t out = ctr->out_cnt;
-    s_out = out;
-    hist[t].out = out;
-    hist[t].edges = ctr->edges;
-    if (st->physical) {  // the pull compacted the unvisited list (ping-pong)
-      st->ul_len = ctr->misc;
-      st->ul_src = st->ul_src == 0 ? 1 : 0;
-    }
-    st->prev_physical = st->physical;
-    st->in_count = out;
-    st->in_degsum = ctr->next_deg;
-  }
-  __syncthreads();
-  uint32_t* c = reinterpret_cast<uint32_t*>(ctr);
-  for (uint32_t i = threadIdx.x; i < sizeof(Counters) / 4; i += blockDim.x) c[i] = 0u;
-  if (threadIdx.x == 0) {
-    st->iter = t + 1;
-    const bool more = s_out > 0 && t + 1 < st->max_supersteps && t + 1 < kLoopHist;
-    cudaGraphSetConditional(h_while, more ? 1u : 0u);
-    if (more) {  // the next superstep's direction
-      const uint32_t phys = dobfs_loop_decide(st, hist);
-      cudaGraphSetConditional(h_pull, phys);
-      cudaGraphSetConditional(h_push, phys ? 0u : 1u);
-    }
-  }
-}
 
 struct DobfsPrim : PrimBase {
   uint32_t source;
@@ -1442,7 +1489,7 @@ class DobfsGraphRunner {
       r.edges.push_back(e.edges);
       r.out.push_back(e.out);
       W += e.edges;
-      launches += 1 + (e.physical ? G.n_pull : G.n_push);  // end kernel + branch
+      launches += e.physical ? G.n_pull : G.n_push;  // the branch (its last kernel ends the superstep)
     }
     r.launches = launches;
     const bool hit_cap = S >= kLoopHist && cfg.max_supersteps > kLoopHist && S && r.out.back();
@@ -1576,10 +1623,17 @@ class DobfsGraphRunner {
                (unsigned long long*)nullptr, &ctr->next_deg, dyn);
     uint32_t* gq = w.ul_buf[2].ptr;
     uint32_t* gq_cnt = cnts + 1;
+    // the superstep end runs in the last CTA of each branch's last kernel
+    DobfsLoopEnd le;
+    le.st = st;
+    le.hist = hist;
+    le.h_while = h_while;
+    le.h_pull = h_pull;
+    le.h_push = h_push;
     MGB_LAUNCH(dobfs_pull_group_kernel, num_sms() * 8, 256, 0, s, gv, w.pull_rec.ptr,
                gq, gq_cnt, w.su32[0].ptr, w.su32[1].ptr, w.su32[2].ptr,
                w.su32[3].ptr, 0u, mp, ow, 0, w.loop_front[1].ptr, nullptr, &ctr->misc, ctr,
-               (unsigned long long*)nullptr, &ctr->next_deg, dyn);
+               (unsigned long long*)nullptr, &ctr->next_deg, dyn, le);
     MGB_CUDA(cudaStreamEndCapture(s, &tmp));
     const uint64_t l1 = g_launches.load();
     // push branch: frontier list from the bitmap, prev = vis, edge-balanced advance
@@ -1600,15 +1654,10 @@ class DobfsGraphRunner {
     MGB_LAUNCH((lb_expand_kernel<DobfsDev, true>), num_sms() * 6, kExpBlock, 0, s, f, gv,
                w.loop_front[0].ptr, 0u, w.loop_lb_row.ptr, w.loop_lb_pref.ptr, w.loop_lb_bsum.ptr,
                w.loop_total.ptr, w.loop_tiles.ptr, w.loop_front[1].ptr, &ctr->out_cnt, nin);
-    MGB_LAUNCH(degsum_dev_kernel, num_sms() * 4, 256, 0, s, gv, w.loop_front[1].ptr,
-               &ctr->out_cnt, &ctr->next_deg);
+    MGB_LAUNCH(dobfs_degsum_end_kernel, num_sms() * 4, 256, 0, s, gv, w.loop_front[1].ptr, ctr,
+               le);
     MGB_CUDA(cudaStreamEndCapture(s, &tmp));
     const uint64_t l2 = g_launches.load();
-    // end (after both branches)
-    MGB_CUDA(cudaStreamBeginCaptureToGraph(s, body, ifs, nullptr, 2,
-                                           cudaStreamCaptureModeRelaxed));
-    MGB_LAUNCH(dobfs_loop_end_kernel, 1, 256, 0, s, st, ctr, hist, h_while, h_pull, h_push);
-    MGB_CUDA(cudaStreamEndCapture(s, &tmp));
     g_launches.store(l0);  // capture is not execution
     MGB_CUDA(cudaGraphInstantiate(&w.loop_exec[gi], g, 0));
     MGB_CUDA(cudaGraphDestroy(g));
