@@ -2141,6 +2141,10 @@ bool DobfsPrim::device_loop(Plan& P, std::vector<Ctx>& ctx, RunState& rs, const 
 // ===========================================================================
 // SSSP (primitives.cpp:307-397)
 
+#ifndef MG_SSSP_DENSE_DIV
+#define MG_SSSP_DENSE_DIV 256  // RMAT-24 C3: off 11.3 ms, 32: 9.27, 128: 8.25, 512: 8.24, 4096: 8.29, always: 8.41
+#endif
+
 // Distances are kept in T = u32 when every finite distance fits (max edge
 // weight x |V| < 2^32 - 1: RMAT-24 with w <= 64 needs 1.07e9), else u64 like
 // the reference.  The u32 array is half the size (67 MB at |V| = 2^24, inside
@@ -2158,6 +2162,11 @@ struct SsspDev {
   OwnerView ow;
   uint32_t iter;
   int mark_preds;
+  // dense superstep (one partition, no preds): improving arcs issue
+  // fire-and-forget atomicMin (RED) and accept nothing; the output frontier is
+  // the set of vertices whose distance fell below the superstep's full
+  // snapshot, listed by dense_list_kernel<SsspFell> afterwards
+  int red = 0;
   // relax from the superstep-frozen source distance (primitives.cpp:340-348)
   __device__ bool visit(uint32_t u, uint32_t v, uint32_t e) const {
     T nd = fdist[u] + (T)w[e];
@@ -2214,6 +2223,14 @@ __device__ __forceinline__ void visit_batch(const SsspDev<T>& f, const uint32_t*
     nd[k] = pass[k] ? __ldg(&f.fdist[src[k]]) + (T)ld_stream(&f.w[eid[k]]) : (T)0;
     cur[k] = pass[k] ? __ldcg(&f.dists[nb[k]]) : (T)0;
   }
+  if (f.red) {  // no return value: RED, the thread does not wait for the L2
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+      if (pass[k] && nd[k] < cur[k]) atomicMin(&f.dists[nb[k]], nd[k]);
+      acc[k] = false;
+    }
+    return;
+  }
   T old[K];
 #pragma unroll
   for (int k = 0; k < K; ++k)
@@ -2231,6 +2248,77 @@ __global__ void snapshot_kernel(const uint32_t* __restrict__ in, uint32_t n, con
   for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
     uint32_t u = in[i];
     fdist[u] = dists[u];
+  }
+}
+
+// output frontier of a dense superstep, listed in ID order with one global
+// atomic per CTA per round, 4 vertices per thread: P(q) is the 4-bit mask of
+// vertices 4q..4q+3 that belong to it
+//  * SSSP: the distance fell below the snapshot taken at the superstep's start
+//    (= the vertices some arc improved, each once)
+//  * BC forward: the vertex was labelled in this superstep
+struct SsspFell {
+  const uint32_t* d;
+  const uint32_t* snap;
+  __device__ uint32_t operator()(uint32_t q) const {
+    const uint4 a = __ldcs(reinterpret_cast<const uint4*>(d) + q);
+    const uint4 b = __ldcs(reinterpret_cast<const uint4*>(snap) + q);
+    return (a.x < b.x) | (a.y < b.y) << 1 | (a.z < b.z) << 2 | (a.w < b.w) << 3;
+  }
+  __device__ bool one(uint32_t v) const { return d[v] < snap[v]; }
+};
+struct LabelIs {
+  const uint32_t* labels;
+  uint32_t level;
+  __device__ uint32_t operator()(uint32_t q) const {
+    const uint4 a = __ldcs(reinterpret_cast<const uint4*>(labels) + q);
+    return (a.x == level) | (a.y == level) << 1 | (a.z == level) << 2 | (a.w == level) << 3;
+  }
+  __device__ bool one(uint32_t v) const { return labels[v] == level; }
+};
+
+template <class Pred>
+__global__ void __launch_bounds__(256)
+    dense_list_kernel(Pred pred, uint32_t nv, uint32_t* out, uint32_t* cnt) {
+  __shared__ uint32_t s_warp[8];
+  __shared__ uint32_t s_base;
+  const uint32_t lane = lane_id(), warp = threadIdx.x >> 5;
+  const uint32_t nq = (nv + 3) / 4;
+  for (uint32_t base = blockIdx.x * 256; base < nq; base += gridDim.x * 256) {
+    const uint32_t q = base + threadIdx.x;
+    uint32_t m = 0;
+    if (q < nq) {
+      if (4 * q + 3 < nv) {
+        m = pred(q);
+      } else {
+        for (uint32_t k = 0; 4 * q + k < nv; ++k) m |= (uint32_t)pred.one(4 * q + k) << k;
+      }
+    }
+    const uint32_t c = __popc(m);
+    uint32_t x = c;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+      if (lane >= (uint32_t)o) x += y;
+    }
+    if (lane == 31) s_warp[warp] = x;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      uint32_t run = 0;
+      for (int k = 0; k < 8; ++k) {
+        const uint32_t t = s_warp[k];
+        s_warp[k] = run;
+        run += t;
+      }
+      s_base = run ? atomicAdd(cnt, run) : 0u;
+    }
+    __syncthreads();
+    uint32_t o = s_base + s_warp[warp] + x - c;
+    while (m) {
+      out[o++] = 4 * q + (__ffs(m) - 1);
+      m &= m - 1;
+    }
+    __syncthreads();
   }
 }
 
@@ -2281,8 +2369,25 @@ struct SsspPrim : PrimBase {
     return {w.su64[0].ptr, w.su64[1].ptr, w.su64[2].ptr, w.su32[1].ptr, w.su32[2].ptr,
             w.w.ptr, c.owner_view(), (uint32_t)c.iter, mark_preds ? 1 : 0};
   }
+  // a superstep whose frontier holds at least nv / kSsspDenseDiv vertices runs
+  // dense (SsspDev::red) when there is one partition, no predecessor output and
+  // the fused policy (its output buffer is sized for the superstep's bound)
+  static constexpr uint32_t kSsspDenseDiv = MG_SSSP_DENSE_DIV;
   void body(Ctx& c) {
     Worker& w = *c.w;
+    if (narrow && c.fused && c.num_workers() == 1 && !mark_preds && kSsspDenseDiv &&
+        (uint64_t)c.in_count * kSsspDenseDiv >= w.nv) {
+      // full snapshot (it is the frozen source distance of every frontier vertex)
+      MGB_CUDA(cudaMemcpyAsync(w.su32[3].ptr, w.su32[0].ptr, 4ull * w.nv,
+                               cudaMemcpyDeviceToDevice, w.stream));
+      SsspDev<uint32_t> f = dev32(c);
+      f.red = 1;
+      c.pipeline(f, w.nv);
+      MGB_LAUNCH(dense_list_kernel<SsspFell>, grid_for((w.nv + 3) / 4, 256, num_sms() * 8), 256,
+                 0, w.stream, SsspFell{w.su32[0].ptr, w.su32[3].ptr}, w.nv, w.output.ptr,
+                 &c.ctr()->out_cnt);
+      return;
+    }
     if (c.iter > 0)
       MGB_CUDA(cudaMemsetAsync(w.su32[2].ptr, 0, 4ull * (w.nv / 32 + 1), w.stream));
     if (narrow) {
@@ -2727,6 +2832,11 @@ struct BcDev {
   OwnerView ow;
   uint32_t iter;
   int phase;
+  // dense forward superstep (one partition): a vertex not labelled before
+  // this superstep gets a plain store of the level (every writer stores the
+  // same value) and the sigma addition, nothing is accepted; the output is
+  // listed by dense_list_kernel<LabelIs> afterwards
+  int red = 0;
   // forward visit (primitives.cpp:559-567): sigma counts are integers, so the
   // order of the atomic additions does not change the result
   __device__ bool visit(uint32_t u, uint32_t v, uint32_t) const {
@@ -2780,6 +2890,17 @@ __device__ __forceinline__ void visit_batch(const BcDev& f, const uint32_t* src,
   for (int k = 0; k < K; ++k) {
     old[k] = pass[k] ? __ldcg(&f.labels[nb[k]]) : 0u;
     su[k] = pass[k] ? f.sigma[src[k]] : 0.0;
+  }
+  if (f.red) {
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+      if (pass[k] && (old[k] == kInfLabel || old[k] == cand)) {
+        if (old[k] == kInfLabel) __stcg(&f.labels[nb[k]], cand);
+        atomicAdd(&f.sigma[nb[k]], su[k]);
+      }
+      acc[k] = false;
+    }
+    return;
   }
 #pragma unroll
   for (int k = 0; k < K; ++k)
@@ -3071,6 +3192,13 @@ __global__ void bc_level_prep_kernel(const uint32_t* __restrict__ list, uint32_t
   if (blockIdx.x == 0 && threadIdx.x == 0) ctr->out_cnt = l1 - l0;
 }
 
+#ifndef MG_BC_DENSE_DIV
+#define MG_BC_DENSE_DIV 512  // RMAT-24 C5: off 7.24 ms, 32: 7.20, 512: 7.12, always: 7.14
+#endif
+// a forward superstep whose frontier holds at least |V| / kBcDenseDiv vertices
+// runs dense (BcDev::red) on one partition under the fused policy
+constexpr uint32_t kBcDenseDiv = MG_BC_DENSE_DIV;
+
 struct BcPrim : PrimBase {
   uint32_t source;
   int phase = kFwd;
@@ -3125,7 +3253,17 @@ struct BcPrim : PrimBase {
     if (first && phase == kBwd && c.iter - backward_from >= max_level) phase = kDone;
     uint32_t nh = (uint32_t)w.hosted_host.size();
     if (phase == kFwd) {
-      c.pipeline(dev(c), w.nv);
+      if (c.fused && c.P->n == 1 && kBcDenseDiv &&
+          (uint64_t)c.in_count * kBcDenseDiv >= w.nv) {
+        BcDev f = dev(c);
+        f.red = 1;
+        c.pipeline(f, w.nv);
+        MGB_LAUNCH(dense_list_kernel<LabelIs>, grid_for((w.nv + 3) / 4, 256, num_sms() * 8),
+                   256, 0, w.stream, LabelIs{w.su32[0].ptr, (uint32_t)c.iter + 1}, w.nv,
+                   w.output.ptr, &c.ctr()->out_cnt);
+      } else {
+        c.pipeline(dev(c), w.nv);
+      }
       if (nh && c.P->n > 1)  // the global max hosted label; n = 1 derives it
         MGB_LAUNCH(max_hosted_label_kernel, grid_for(nh, 256, num_sms() * 4), 256, 0, w.stream,
                    w.su32[0].ptr, w.hosted.ptr, nh, c.ctr());

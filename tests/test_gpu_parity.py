@@ -222,6 +222,54 @@ def test_sssp_equals_dijkstra(n):
             assert np.array_equal(r.stats.h_matrix, rr.h_matrix)
 
 
+FUSED_CFGS = [mg.EngineConfig(policy=mg.AllocPolicyKind.Maximum, fused=mg.FusedMode.On),
+              mg.EngineConfig(policy=mg.AllocPolicyKind.JustEnough, fused=mg.FusedMode.On),
+              mg.EngineConfig(policy=mg.AllocPolicyKind.PreallocFused)]
+
+
+@pytest.mark.parametrize("name", ["rmat12", "grid32", "star5", "tri_iso", "rmat14"])
+def test_sssp_dense_supersteps_match_reference(name):
+    """One partition under a fused policy: supersteps whose frontier holds at least
+    |V|/32 vertices relax with fire-and-forget atomics and list their output by
+    comparing the distances with the superstep's snapshot (prims.cu SsspDev::red).
+    Distances, S, W, per-superstep frontier sizes and edge counts equal the
+    reference engine's (primitives.cpp:334-356)."""
+    g = (mg.Csr.rmat(14, 16, 5) if name == "rmat14" else graphs()[name]).with_weights(0, 64, 9)
+    off, col, w = g.arrays()
+    plan, owner = plan_for(g, 1)
+    rr = ref.RefPlan(ref.RefGraph.from_csr(off, col, w), owner, 1).sssp(0) \
+        if ref.available() else None
+    for cfg in FUSED_CFGS:
+        r = mg.sssp(plan, 0, cfg=cfg)
+        assert np.array_equal(r.dists, seq.dijkstra(off, col, w, 0))
+        if rr is not None:
+            assert r.stats.supersteps == rr.stats.supersteps
+            assert r.stats.edges_examined == rr.stats.edges_examined
+            assert np.array_equal(r.stats.out_per_iter, rr.out_per_iter)
+            assert np.array_equal(r.stats.edges_per_iter, rr.edges_per_iter)
+
+
+@pytest.mark.parametrize("name", ["rmat12", "grid32", "star5", "rmat14"])
+def test_bc_dense_forward_matches_reference(name):
+    """One partition under a fused policy: large forward supersteps label with
+    plain stores and list their output by level (prims.cu BcDev::red); sigma is
+    bit-exact, bc within 1e-5, S and per-superstep frontier sizes equal the
+    reference engine's."""
+    g = mg.Csr.rmat(14, 16, 5) if name == "rmat14" else graphs()[name]
+    off, col, _ = g.arrays()
+    plan, owner = plan_for(g, 1)
+    bc, sigma, dist = seq.brandes_bc(off, col, 1)
+    rr = ref.RefPlan(ref.RefGraph.from_csr(off, col), owner, 1).bc(1) if ref.available() else None
+    for cfg in FUSED_CFGS:
+        r = mg.bc(plan, 1, cfg=cfg)
+        assert np.array_equal(r.labels, dist)
+        assert np.array_equal(r.sigma, sigma)
+        assert rel_close(r.bc, bc, 1e-5)
+        if rr is not None:
+            assert r.stats.supersteps == rr.stats.supersteps
+            assert np.array_equal(r.stats.out_per_iter, rr.out_per_iter)
+
+
 def test_sssp_pins_and_errors(golden):
     pins, _ = golden
     pin = pins["sssp_p4_weighted"]
