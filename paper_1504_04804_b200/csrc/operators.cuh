@@ -152,6 +152,14 @@ static __global__ void lb_tiles_kernel(const unsigned long long* __restrict__ pr
     tile_lo[t] = t == ntiles ? n_in - 1 : lb_search(prefix, block_off, n_in, t * ts);
 }
 
+// A functor may declare an expansion "quiet" (nothing is ever accepted, e.g.
+// a dense DOBFS push that only sets visited bits): the kernel then skips the
+// per-batch queue ballots and flushes.  Found by argument-dependent lookup.
+template <class F>
+__device__ __forceinline__ bool expand_quiet(const F&) {
+  return false;
+}
+
 // lb 3b: edge-balanced expansion (visit [+ keep when fused]).  Per tile the
 // vertex range is staged in shared memory (chunks of kStage vertices); batches
 // of 32*kItems arcs go round-robin to the warps, lane l taking arcs l, l+32,
@@ -160,6 +168,12 @@ static __global__ void lb_tiles_kernel(const unsigned long long* __restrict__ pr
 // neighbour IDs, pre-test them (prefilter, e.g. the visited bitmap in L2),
 // then visit the survivors — so each thread keeps kItems independent loads in
 // flight instead of one dependent chain per arc.
+// Arc positions are 32-bit offsets from the tile start (a tile holds at most
+// kTile arcs): the staged row starts are clamped to [0, tile arcs] and each
+// row keeps the col index its offset 0 maps to (mod 2^32), so locating an arc
+// is 32-bit work; a lane finds its batch's row by galloping forward from the
+// row of its previous batch (one probe on long rows) instead of a binary
+// search over the whole chunk.
 template <class F, bool kFused>
 __global__ void __launch_bounds__(kExpBlock)
     lb_expand_kernel(F f, GraphView g, const uint32_t* __restrict__ in, uint32_t n_in,
@@ -170,19 +184,21 @@ __global__ void __launch_bounds__(kExpBlock)
                      uint32_t* __restrict__ out, uint32_t* out_cnt,
                      const uint32_t* n_in_ptr = nullptr) {
   if (n_in_ptr) n_in = *n_in_ptr;
-  __shared__ unsigned long long s_pref[kStage + 1];
-  __shared__ uint32_t s_row[kStage];
+  __shared__ uint32_t s_pref[kStage + 1];  // row start - tile start, clamped to [0, tn]
+  __shared__ uint32_t s_base[kStage];      // col index of tile offset 0 seen from the row
   __shared__ uint32_t s_src[kStage];
   __shared__ uint32_t s_q[kExpBlock / 32][kWarpQ];
   const unsigned long long total = *total_ptr;
   const unsigned long long ts = lb_tile_size(total);
   const unsigned long long ntiles = (total + ts - 1) / ts;
   const unsigned warp = threadIdx.x >> 5, lane = lane_id();
+  const bool quiet = expand_quiet(f);
   WarpQueue<kWarpQ, kWarpQ - 32 * kItems> q;
   q.init(s_q[warp]);
   for (unsigned long long tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
     const unsigned long long t0 = tile * ts;
     const unsigned long long t1 = t0 + ts < total ? t0 + ts : total;
+    const uint32_t tn = (uint32_t)(t1 - t0);
     const uint32_t lo = tile_lo[tile];
     const uint32_t hi = tile + 1 < ntiles ? tile_lo[tile + 1] : n_in - 1;
     const uint32_t R = hi - lo + 1;
@@ -194,40 +210,47 @@ __global__ void __launch_bounds__(kExpBlock)
     const uint32_t clo = lo + c0;
     __syncthreads();  // previous chunk done with the stage
     for (uint32_t j = threadIdx.x; j < cR; j += kExpBlock) {
-      s_pref[j] = lb_pref(prefix, block_off, clo + j);
-      s_row[j] = rowstart[clo + j];
+      const unsigned long long p = lb_pref(prefix, block_off, clo + j);
+      s_pref[j] = p <= t0 ? 0u : (p >= t1 ? tn : (uint32_t)(p - t0));
+      s_base[j] = (uint32_t)((unsigned long long)rowstart[clo + j] + t0 - p);
       s_src[j] = in[clo + j];
     }
-    if (threadIdx.x == 0)
-      s_pref[cR] = (clo + cR < n_in) ? lb_pref(prefix, block_off, clo + cR) : total;
+    if (threadIdx.x == 0) {
+      const unsigned long long p = (clo + cR < n_in) ? lb_pref(prefix, block_off, clo + cR) : total;
+      s_pref[cR] = p <= t0 ? 0u : (p >= t1 ? tn : (uint32_t)(p - t0));
+    }
     __syncthreads();
-    // arcs of this chunk inside the tile
-    const unsigned long long a0 = s_pref[0] > t0 ? s_pref[0] : t0;
-    const unsigned long long a1 = s_pref[cR] < t1 ? s_pref[cR] : t1;
+    // arcs of this chunk inside the tile (tile offsets)
+    const uint32_t a0 = s_pref[0], a1 = s_pref[cR];
+    uint32_t j = 0;  // this lane's row: monotone over its batches
     // batches of 32*kItems arcs round-robin over the warps; lane l takes arcs
     // l, l+32, ... of its batch (coalesced col_indices)
-    for (unsigned long long e0 = a0 + (unsigned long long)warp * 32 * kItems + lane; e0 - lane < a1;
-         e0 += (unsigned long long)(kExpBlock / 32) * 32 * kItems) {
-      uint32_t j;
+    for (uint32_t e0 = a0 + warp * 32 * kItems + lane; e0 - lane < a1;
+         e0 += (kExpBlock / 32) * 32 * kItems) {
       {
-        uint32_t a = 0, b = cR - 1;  // last j with s_pref[j] <= e0 (smem search)
-        const unsigned long long key = e0 < a1 ? e0 : a1 - 1;
-        while (a < b) {
-          uint32_t m = (a + b + 1) >> 1;
-          if (s_pref[m] <= key) a = m;
+        // last row with s_pref <= key, galloping forward from j (s_pref[j] <= key)
+        const uint32_t key = e0 < a1 ? e0 : a1 - 1;
+        uint32_t step = 1;
+        while (j + step < cR && s_pref[j + step] <= key) {
+          j += step;
+          step <<= 1;
+        }
+        uint32_t b = j + step < cR ? j + step - 1 : cR - 1;  // s_pref[b + 1] > key
+        while (j < b) {
+          const uint32_t m = (j + b + 1) >> 1;
+          if (s_pref[m] <= key) j = m;
           else b = m - 1;
         }
-        j = a;
       }
-      unsigned long long jnext = s_pref[j + 1];
+      uint32_t jnext = s_pref[j + 1];
       uint32_t eid[kItems], src[kItems], nb[kItems];
 #pragma unroll
       for (int k = 0; k < kItems; ++k) {  // locate: a short walk in shared memory
-        const unsigned long long e = e0 + 32ull * k;
+        const uint32_t e = e0 + 32u * k;
         eid[k] = 0xFFFFFFFFu;
         if (e < a1) {
           while (e >= jnext) jnext = s_pref[++j + 1];
-          eid[k] = s_row[j] + (uint32_t)(e - s_pref[j]);
+          eid[k] = s_base[j] + e;
           src[k] = s_src[j];
         }
       }
@@ -240,13 +263,15 @@ __global__ void __launch_bounds__(kExpBlock)
         pass[k] = eid[k] != 0xFFFFFFFFu && f.prefilter(nb[k]);
       bool acc[kItems];
       visit_batch<kItems>(f, src, nb, eid, pass, acc);
+      if (!quiet) {
 #pragma unroll
-      for (int k = 0; k < kItems; ++k) {
-        bool a = acc[k];
-        if (kFused && a) a = f.keep(nb[k]);
-        q.push(a, nb[k]);
+        for (int k = 0; k < kItems; ++k) {
+          bool a = acc[k];
+          if (kFused && a) a = f.keep(nb[k]);
+          q.push(a, nb[k]);
+        }
+        q.flush(out_cnt, out, false);
       }
-      q.flush(out_cnt, out, false);
     }
     }
   }

@@ -206,6 +206,19 @@ struct BfsPrim : PrimBase {
 
 // exact-cost physical direction: pull when Σdeg(Q) > ratio * |unvisited list|
 // (MG_PULL_RATIO overrides the default, for the sweep in DESIGN.md §7)
+// A push superstep that examines at least this many arcs runs dense
+// (DobfsDev::red) on one partition without predecessors under the fused
+// policy, in the host and the device-driven loop (MG_DOBFS_DENSE_ARCS, 0 = never;
+// RMAT-26 device loop, 8 bench sources: 2^18 6.96 ms, 2^20 6.875, 2^22 6.875,
+// 2^24 6.886, never 7.01-7.08)
+static unsigned long long dense_push_arcs() {
+  static const unsigned long long a = [] {
+    const char* e = getenv("MG_DOBFS_DENSE_ARCS");
+    return e ? (unsigned long long)atoll(e) : (1ull << 20);
+  }();
+  return a;
+}
+
 static double pull_ratio() {
   static const double r = [] {
     const char* e = getenv("MG_PULL_RATIO");
@@ -351,15 +364,55 @@ __device__ void dobfs_loop_end_last_cta(const DobfsLoopEnd& le, Counters* ctr) {
   dobfs_loop_end_cta(le.st, ctr, le.hist, le.h_while, le.h_pull, le.h_push);
 }
 
+// a device-loop push whose advance examines at least `min` arcs (*total) runs
+// dense (DobfsDev::red): the end kernel then takes the discoveries from
+// vis & ~prev (prev = vis as of the superstep's start) and writes their labels
+struct DensePush {
+  const unsigned long long* total;  // the advance's arc count (lb_scan)
+  unsigned long long min;           // 0: never
+  const uint32_t* vis;
+  const uint32_t* prev;
+  uint32_t* labels;
+  uint32_t nw;
+  __device__ bool on() const { return min && *total >= min; }
+};
+
 // push branch's last kernel: the degree sum of the discoveries, then the end
 __global__ void __launch_bounds__(256)
     dobfs_degsum_end_kernel(GraphView g, const uint32_t* __restrict__ in, Counters* ctr,
-                            DobfsLoopEnd le) {
-  const uint32_t n = ctr->out_cnt;
+                            DobfsLoopEnd le, DensePush dp) {
   unsigned long long d = 0;
-  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
-    const uint32_t v = in[i];
-    d += g.off[v + 1] - g.off[v];
+  if (dp.on()) {
+    const uint32_t level = le.st->iter + 1;
+    uint32_t cnt = 0;
+    const uint32_t lane = lane_id();
+    // warp-uniform trip count; word by word, lane l takes bit l (coalesced
+    // label stores and offset loads)
+    for (uint32_t b = (blockIdx.x * blockDim.x + threadIdx.x) & ~31u; b < dp.nw;
+         b += gridDim.x * blockDim.x) {
+      const uint32_t i = b + lane;
+      const uint32_t x = i < dp.nw ? __ldcg(&dp.vis[i]) & ~__ldcs(&dp.prev[i]) : 0u;
+      cnt += __popc(x);
+      for (unsigned m = __ballot_sync(0xffffffffu, x != 0); m; m &= m - 1) {
+        const int src = __ffs(m) - 1;
+        const uint32_t xj = __shfl_sync(0xffffffffu, x, src);
+        if ((xj >> lane) & 1u) {
+          const uint32_t v = (b + src) * 32 + lane;
+          dp.labels[v] = level;
+          d += g.off[v + 1] - g.off[v];
+        }
+      }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
+    if (lane_id() == 0 && cnt) atomicAdd(&ctr->out_cnt, cnt);
+  } else {
+    const uint32_t n = ctr->out_cnt;
+    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n;
+         i += gridDim.x * blockDim.x) {
+      const uint32_t v = in[i];
+      d += g.off[v + 1] - g.off[v];
+    }
   }
   unsigned long long* const dst[1] = {&ctr->next_deg};
   const uint64_t val[1] = {d};
@@ -409,7 +462,20 @@ struct DobfsDev {
   }
   __device__ bool send_filter(uint32_t, uint32_t) const { return true; }
   __device__ uint32_t peer_id(uint32_t v, uint32_t, uint32_t) const { return v; }
+  // dense push superstep (one partition, no predecessors): an arc whose
+  // pre-test saw the bit clear sets it with a fire-and-forget OR (RED: the
+  // thread never waits on the L2 for a return value) and accepts nothing; the
+  // labels and the output list come afterwards from vis & ~prev
+  // (bitmap_diff_list_kernel with labels), in ID order
+  int red = 0;
+  // device loop: dense when the advance's arc count reaches red_min (DensePush)
+  const unsigned long long* red_total = nullptr;
+  unsigned long long red_min = 0;
+  __device__ bool dense() const { return red || (red_min && *red_total >= red_min); }
 };
+
+// a dense push accepts nothing: no output queue work in the expansion
+__device__ __forceinline__ bool expand_quiet(const DobfsDev& f) { return f.dense(); }
 
 // batched forward visit: all test-and-set atomics of the batch in flight
 // before any result is consumed (see visit_batch in operators.cuh)
@@ -417,6 +483,18 @@ template <int K>
 __device__ __forceinline__ void visit_batch(const DobfsDev& f, const uint32_t* src,
                                             const uint32_t* nb, const uint32_t*,
                                             const bool* pass, bool* acc) {
+  if (f.dense()) {
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+      // explicit red: a plain atomicOr shares its ATOMG with the path below
+      if (pass[k])
+        asm volatile("red.relaxed.gpu.global.or.b32 [%0], %1;" ::"l"(&f.vis[nb[k] >> 5]),
+                     "r"(1u << (nb[k] & 31))
+                     : "memory");
+      acc[k] = false;
+    }
+    return;
+  }
   uint32_t old[K];
 #pragma unroll
   for (int k = 0; k < K; ++k)
@@ -996,7 +1074,8 @@ __global__ void __launch_bounds__(256)
               if (j == fj) sel = w[j];
             const uint32_t pw = __shfl_sync(gmask, sel, gbase + first);
             if (sub == 0) {
-              scanned += k - b + fj * kPullGroup + first + 1;
+              // the rounds before this one already counted their spans
+              scanned += fj * kPullGroup + first + 1;
               found = true;
               keep = false;
               labels[v] = next_label;
@@ -1044,7 +1123,11 @@ __global__ void __launch_bounds__(256)
 __global__ void __launch_bounds__(256)
     bitmap_diff_list_kernel(const uint32_t* __restrict__ vis, uint32_t* prev, uint32_t nw,
                             uint32_t* out, uint32_t* cnt, int set_prev = 0,
-                            const DobfsLoop* st = nullptr) {
+                            const DobfsLoop* st = nullptr, uint32_t* labels = nullptr,
+                            uint32_t level = 0, const unsigned long long* need_total = nullptr,
+                            unsigned long long need_min = 0) {
+  // after a host-loop push: list only when it ran dense (DobfsDev::dense)
+  if (need_total && *need_total < need_min) return;
   // device-driven loop, superstep 0: the list is the source, seeded by the
   // init kernel together with prev (no 8 MB bitmap pass for one vertex)
   if (st && st->iter == 0) return;
@@ -1079,12 +1162,22 @@ __global__ void __launch_bounds__(256)
       s_base = run ? atomicAdd(cnt, run) : 0u;
     }
     __syncthreads();
-    uint32_t o = s_base + s_warp[warp] + x - c;
-    while (d) {
-      out[o++] = i * 32 + (__ffs(d) - 1);
-      d &= d - 1;
+    const uint32_t o = s_base + s_warp[warp] + x - c;
+    // the warp writes word by word (the non-empty ones): lane l stores bit l,
+    // so each store instruction fills consecutive list entries and one
+    // 128-byte line of labels (a thread walking its own word would put 32
+    // lanes on 32 different lines per store)
+    const unsigned lt = (1u << lane) - 1u;
+    for (unsigned m = __ballot_sync(0xffffffffu, d != 0); m; m &= m - 1) {
+      const int src = __ffs(m) - 1;
+      const uint32_t dj = __shfl_sync(0xffffffffu, d, src);
+      const uint32_t oj = __shfl_sync(0xffffffffu, o, src);
+      if ((dj >> lane) & 1u) {
+        const uint32_t v = (base + warp * 32 + src) * 32 + lane;
+        out[oj + __popc(dj & lt)] = v;
+        if (labels) labels[v] = level;  // a dense push's discoveries (DobfsDev::red)
+      }
     }
-    __syncwarp();
     __syncthreads();
   }
 }
@@ -1286,7 +1379,23 @@ struct DobfsPrim : PrimBase {
       MGB_CUDA(cudaMemcpyAsync(w.aux[4].ptr, w.su32[2].ptr, 4 * nw, cudaMemcpyDeviceToDevice,
                                w.stream));
       if (c.P->profile) MGB_CUDA(cudaEventRecord(w.ev_k0, w.stream));
-      c.pipeline(dev(c), w.nv);
+      if (c.P->n == 1 && !mark_preds && c.fused && dense_push_arcs() && c.in_count) {
+        // dense when the advance examines >= dense_push_arcs() arcs (its scan
+        // total, read on the device): visited bits only, out_cnt stays 0, then
+        // labels and the output list from vis & ~prev
+        const uint32_t nb = (c.in_count + kLbBlock - 1) / kLbBlock;  // lb_advance's total slot
+        if (w.lb_bsum.n < nb + 1ull) w.lb_bsum.alloc(nb + 1ull);
+        DobfsDev f = dev(c);
+        f.red_total = w.lb_bsum.ptr + nb;
+        f.red_min = dense_push_arcs();
+        c.pipeline(f, w.nv);
+        MGB_LAUNCH(bitmap_diff_list_kernel, grid_for(nw, 256, num_sms() * 8), 256, 0, w.stream,
+                   w.su32[2].ptr, w.aux[4].ptr, (uint32_t)nw, w.output.ptr, &c.ctr()->out_cnt, 0,
+                   (const DobfsLoop*)nullptr, w.su32[0].ptr, (uint32_t)c.iter + 1, f.red_total,
+                   f.red_min);
+      } else {
+        c.pipeline(dev(c), w.nv);
+      }
       if (c.P->profile) {
         MGB_CUDA(cudaEventRecord(w.ev_k1, w.stream));
         prof_pending_[w.p] = true;
@@ -1651,11 +1760,16 @@ class DobfsGraphRunner {
     MGB_LAUNCH(lb_tiles_kernel, num_sms() * 8, 256, 0, s, w.loop_lb_pref.ptr, w.loop_lb_bsum.ptr,
                0u, w.loop_total.ptr, w.loop_tiles.ptr, (uint32_t)max_tiles, nin);
     DobfsDev f{w.su32[0].ptr, w.su32[1].ptr, w.su32[2].ptr, w.su32[3].ptr, ow, 0u, mp, &st->iter};
+    // dense pushes (no predecessors): labels and counts from the bitmap diff
+    const DensePush dp{w.loop_total.ptr, mark_preds ? 0ull : dense_push_arcs(), w.su32[2].ptr,
+                       w.aux[4].ptr, w.su32[0].ptr, (uint32_t)nw};
+    f.red_total = dp.total;
+    f.red_min = dp.min;
     MGB_LAUNCH((lb_expand_kernel<DobfsDev, true>), num_sms() * 6, kExpBlock, 0, s, f, gv,
                w.loop_front[0].ptr, 0u, w.loop_lb_row.ptr, w.loop_lb_pref.ptr, w.loop_lb_bsum.ptr,
                w.loop_total.ptr, w.loop_tiles.ptr, w.loop_front[1].ptr, &ctr->out_cnt, nin);
     MGB_LAUNCH(dobfs_degsum_end_kernel, num_sms() * 4, 256, 0, s, gv, w.loop_front[1].ptr, ctr,
-               le);
+               le, dp);
     MGB_CUDA(cudaStreamEndCapture(s, &tmp));
     const uint64_t l2 = g_launches.load();
     g_launches.store(l0);  // capture is not execution
@@ -2209,6 +2323,10 @@ struct SsspDev {
   }
   __device__ uint32_t peer_id(uint32_t v, uint32_t, uint32_t) const { return v; }
 };
+
+// a dense superstep's relaxations accept nothing (output listed afterwards)
+template <class T>
+__device__ __forceinline__ bool expand_quiet(const SsspDev<T>& f) { return f.red != 0; }
 
 // batched relaxation: the frozen source distances, weights and current
 // destination distances of the whole batch are loaded first (independent
@@ -2876,6 +2994,9 @@ struct BcDev {
   __device__ bool send_filter(uint32_t, uint32_t) const { return true; }
   __device__ uint32_t peer_id(uint32_t v, uint32_t, uint32_t) const { return v; }
 };
+
+// a dense forward superstep accepts nothing (output listed afterwards)
+__device__ __forceinline__ bool expand_quiet(const BcDev& f) { return f.red != 0; }
 
 // batched forward visit: label loads, then the claiming CASes, then the sigma
 // additions of the whole batch, each group in flight together

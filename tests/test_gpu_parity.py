@@ -549,12 +549,16 @@ def test_dobfs_graph_loop_max_supersteps_and_isolated_source():
     assert r.stats.supersteps == 1
 
 
+FIRST_HIT_POS = list(range(15)) + [17, 18, 19, 25, 26, 33, 42, 43, 50, 58, 75, 90]
+
+
 def _first_hit_graph():
     """source 0 -> hub 1 -> rows x whose first frontier neighbour (the hub) sits at
-    arc position k = 0..14, followed by 0/1/5/20 more arcs: the pull's record
-    arcs (0-1), its in-thread stage (arcs 2-9) and the cooperative stage (10+)"""
+    arc position k, followed by 0/1/5/20 more arcs: the pull's record arcs
+    (0-1), its in-thread stages (arcs 2-17) and the cooperative stage (18+),
+    whose first round tests 8 arcs and later rounds 8 * kGroupSectors"""
     adj = [[1], [0]]
-    for k in range(15):
+    for k in FIRST_HIT_POS:
         for t in (0, 1, 5, 20):
             x = len(adj)
             adj.append([])
@@ -590,7 +594,7 @@ def test_dobfs_pull_first_hit_positions(n, do_a):
         r = mg.dobfs(plan, mg.DobfsOptions(source=0, do_a=do_a, do_b=0.1, mark_preds=True), cfg)
         assert np.array_equal(r.labels, seq.bfs_levels(off, col, 0))
         x = np.nonzero(r.labels == 2)[0]
-        assert np.all(r.preds[x] == 1) and len(x) == 60
+        assert np.all(r.preds[x] == 1) and len(x) == 4 * len(FIRST_HIT_POS)
         if do_a < 1e-6:
             assert r.backward_edges > 0  # the rows were pulled
         if ref.available():

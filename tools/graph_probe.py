@@ -2,7 +2,10 @@
 sources) with the device-driven graph loop and, with MG_NO_GRAPH=1, the
 host-driven loop.  No profiler attached.
 
-    python tools/graph_probe.py [scale] [graph|host]"""
+    python tools/graph_probe.py [scale] [graph|host|ref]
+
+ref: the reference schedule (dobfs_exact_cost off: every forward superstep
+pushes, host-driven loop)."""
 import os
 import sys
 
@@ -22,6 +25,9 @@ modes = [sys.argv[2]] if len(sys.argv) > 2 else ["graph", "host"]
 for mode in modes:
     if mode == "host":
         os.environ["MG_NO_GRAPH"] = "1"
+    if mode == "ref":
+        cfg = mg.EngineConfig(policy=mg.AllocPolicyKind.Maximum, fused=mg.FusedMode.On,
+                              dobfs_exact_cost=False)
     for s in srcs:
         mg.dobfs(plan, mg.DobfsOptions(source=s), cfg, download=False)
     per = []
