@@ -543,7 +543,7 @@ struct Ctx {
     MGB_LAUNCH(lb_tiles_kernel, grid_for(max_tiles + 1, 256, num_sms() * 8), 256, 0, w->stream,
                w->lb_pref.ptr, w->lb_bsum.ptr, in_count, w->lb_bsum.ptr + nb, w->lb_tile.ptr,
                (uint32_t)max_tiles);
-    const unsigned resident = num_sms() * 6;  // 32 KB smem + 256 threads per CTA
+    const unsigned resident = expand_resident<F, kFused>();
     unsigned grid = in_degsum == kUnknownDeg ? resident
                                              : grid_for(in_degsum, lb_tile_size(in_degsum), resident);
     MGB_LAUNCH((lb_expand_kernel<F, kFused>), grid, kExpBlock, 0, w->stream, f, graph(),

@@ -32,6 +32,9 @@ constexpr uint32_t kTile = 8192;  // arcs per tile for large advances
 #ifndef MG_WARPQ
 #define MG_WARPQ 384
 #endif
+#ifndef MG_EXPAND_MIN_CTAS
+#define MG_EXPAND_MIN_CTAS 4
+#endif
 #ifndef MG_KSTAGE
 #define MG_KSTAGE 1536
 #endif
@@ -152,6 +155,27 @@ static __global__ void lb_tiles_kernel(const unsigned long long* __restrict__ pr
     tile_lo[t] = t == ntiles ? n_in - 1 : lb_search(prefix, block_off, n_in, t * ts);
 }
 
+// A functor whose visits never read the arc's source vertex (e.g. a dense
+// DOBFS push without predecessors) lets the locate phase skip the staged
+// source loads.  Found by argument-dependent lookup, like expand_quiet.
+template <class F>
+__device__ __forceinline__ bool expand_needs_src(const F&) {
+  return true;
+}
+// Minimum resident CTAs per SM the expansion is compiled for (register cap);
+// a primitive may specialise it for its functor.
+template <class F>
+struct expand_min_ctas {
+  static constexpr int value = MG_EXPAND_MIN_CTAS;
+};
+// Locate a lane's whole batch with one test when it lies inside one row (the
+// hub rows of a DOBFS push).  Off by default: the extra code path costs SSSP
+// more than it saves (RMAT-24 C3 6.76 -> 7.1 ms with it, same box).
+template <class F>
+struct expand_long_rows {
+  static constexpr bool value = false;
+};
+
 // A functor may declare an expansion "quiet" (nothing is ever accepted, e.g.
 // a dense DOBFS push that only sets visited bits): the kernel then skips the
 // per-batch queue ballots and flushes.  Found by argument-dependent lookup.
@@ -175,7 +199,7 @@ __device__ __forceinline__ bool expand_quiet(const F&) {
 // row of its previous batch (one probe on long rows) instead of a binary
 // search over the whole chunk.
 template <class F, bool kFused>
-__global__ void __launch_bounds__(kExpBlock)
+__global__ void __launch_bounds__(kExpBlock, expand_min_ctas<F>::value)
     lb_expand_kernel(F f, GraphView g, const uint32_t* __restrict__ in, uint32_t n_in,
                      const uint32_t* __restrict__ rowstart,
                      const unsigned long long* __restrict__ prefix,
@@ -193,6 +217,8 @@ __global__ void __launch_bounds__(kExpBlock)
   const unsigned long long ntiles = (total + ts - 1) / ts;
   const unsigned warp = threadIdx.x >> 5, lane = lane_id();
   const bool quiet = expand_quiet(f);
+  const bool need_src = expand_needs_src(f);
+  constexpr bool kLongRows = expand_long_rows<F>::value;
   WarpQueue<kWarpQ, kWarpQ - 32 * kItems> q;
   q.init(s_q[warp]);
   for (unsigned long long tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
@@ -244,14 +270,26 @@ __global__ void __launch_bounds__(kExpBlock)
       }
       uint32_t jnext = s_pref[j + 1];
       uint32_t eid[kItems], src[kItems], nb[kItems];
+      const uint32_t elast = e0 + 32u * (kItems - 1);
+      if (kLongRows && elast < jnext && elast < a1) {  // the lane's whole batch in row j
+        const uint32_t b0 = s_base[j] + e0;
+        const uint32_t s0 = need_src ? s_src[j] : 0u;
 #pragma unroll
-      for (int k = 0; k < kItems; ++k) {  // locate: a short walk in shared memory
-        const uint32_t e = e0 + 32u * k;
-        eid[k] = 0xFFFFFFFFu;
-        if (e < a1) {
-          while (e >= jnext) jnext = s_pref[++j + 1];
-          eid[k] = s_base[j] + e;
-          src[k] = s_src[j];
+        for (int k = 0; k < kItems; ++k) {
+          eid[k] = b0 + 32u * k;
+          src[k] = s0;
+        }
+      } else {
+#pragma unroll
+        for (int k = 0; k < kItems; ++k) {  // locate: a short walk in shared memory
+          const uint32_t e = e0 + 32u * k;
+          eid[k] = 0xFFFFFFFFu;
+          src[k] = 0u;
+          if (e < a1) {
+            while (e >= jnext) jnext = s_pref[++j + 1];
+            eid[k] = s_base[j] + e;
+            if (need_src) src[k] = s_src[j];
+          }
         }
       }
 #pragma unroll
@@ -276,6 +314,21 @@ __global__ void __launch_bounds__(kExpBlock)
     }
   }
   q.flush(out_cnt, out, true);
+}
+
+// Persistent expansion grid: the CTAs that are resident at once (registers
+// and shared memory of this instantiation, asked of the runtime once), so no
+// second wave of CTAs starts late on a grid-stride share of the tiles.
+template <class F, bool kFused>
+inline unsigned expand_resident() {
+  static unsigned per_sm = 0;
+  if (!per_sm) {
+    int b = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, lb_expand_kernel<F, kFused>, kExpBlock, 0);
+    per_sm = b > 0 ? static_cast<unsigned>(b) : 4u;
+    if (const char* e = getenv("MG_EXPAND_CTAS_PER_SM")) per_sm = (unsigned)atoi(e);  // A/B
+  }
+  return num_sms() * per_sm;
 }
 
 // filter (engine.hpp:71-79): compaction by keep(v); input length read on device

@@ -206,15 +206,26 @@ struct BfsPrim : PrimBase {
 
 // exact-cost physical direction: pull when Σdeg(Q) > ratio * |unvisited list|
 // (MG_PULL_RATIO overrides the default, for the sweep in DESIGN.md §7)
-// A push superstep that examines at least this many arcs runs dense
-// (DobfsDev::red) on one partition without predecessors under the fused
-// policy, in the host and the device-driven loop (MG_DOBFS_DENSE_ARCS, 0 = never;
-// RMAT-26 device loop, 8 bench sources: 2^18 6.96 ms, 2^20 6.875, 2^22 6.875,
-// 2^24 6.886, never 7.01-7.08)
+// A push superstep of the host-driven loop that examines at least this many
+// arcs runs dense (DobfsDev::red) on one partition without predecessors under
+// the fused policy (MG_DOBFS_DENSE_ARCS, 0 = never).  Reference schedule over
+// the bench sources: 27.4 ms never, 17.2 ms at 2^20 arcs.
 static unsigned long long dense_push_arcs() {
   static const unsigned long long a = [] {
     const char* e = getenv("MG_DOBFS_DENSE_ARCS");
     return e ? (unsigned long long)atoll(e) : (1ull << 20);
+  }();
+  return a;
+}
+
+// The device-driven (exact-cost) loop pushes only below the pull threshold;
+// there the dense form loses (bench sources, same box: off 6.77 ms, 2^20 arcs
+// 6.91, 2^24 6.90 — one hub-source superstep-0 push costs +85 us), so it is
+// off unless MG_DOBFS_LOOP_DENSE_ARCS sets a threshold.
+static unsigned long long loop_dense_push_arcs() {
+  static const unsigned long long a = [] {
+    const char* e = getenv("MG_DOBFS_LOOP_DENSE_ARCS");
+    return e ? (unsigned long long)atoll(e) : 0ull;
   }();
   return a;
 }
@@ -420,6 +431,9 @@ __global__ void __launch_bounds__(256)
   dobfs_loop_end_last_cta(le, ctr);
 }
 
+#ifndef MG_DENSE_LDCA
+#define MG_DENSE_LDCA 0
+#endif
 struct DobfsDev {
   uint32_t* labels;
   uint32_t* preds;
@@ -445,6 +459,11 @@ struct DobfsDev {
   // and read-only (ld.nc) probes are no faster on RMAT-26 — the probes are
   // spread too widely for L1 reuse.
   __device__ bool prefilter(uint32_t v) const {
+#if MG_DENSE_LDCA
+    // a dense push tolerates stale L1 copies (a stale clear bit costs one
+    // more RED, a set bit is never stale): hub words stay in L1
+    if (red || red_min) return !(__ldca(&vis[v >> 5]) & (1u << (v & 31)));
+#endif
     return !(__ldcg(&vis[v >> 5]) & (1u << (v & 31)));
   }
   // combine (primitives.cpp:255-265): an unvisited vertex takes the remote
@@ -474,8 +493,28 @@ struct DobfsDev {
   __device__ bool dense() const { return red || (red_min && *red_total >= red_min); }
 };
 
+}  // namespace
+#ifndef MG_DOBFS_EXPAND_CTAS
+#define MG_DOBFS_EXPAND_CTAS 4
+#endif
+// The DOBFS push is bound on its visited-bit probes (L2 latency).  Compiled
+// for 4, 5 and 6 resident CTAs per SM (64 / 48 / 40 registers, the last with
+// spills): reference schedule over the bench sources 17.15 / 17.35 / 19.5 ms.
+template <>
+struct expand_min_ctas<DobfsDev> {
+  static constexpr int value = MG_DOBFS_EXPAND_CTAS;
+};
+// hub rows: whole batches inside one row (reference schedule 18.1 -> 17.2 ms)
+template <>
+struct expand_long_rows<DobfsDev> {
+  static constexpr bool value = true;
+};
+namespace {
+
 // a dense push accepts nothing: no output queue work in the expansion
 __device__ __forceinline__ bool expand_quiet(const DobfsDev& f) { return f.dense(); }
+// the source vertex is read only for predecessors
+__device__ __forceinline__ bool expand_needs_src(const DobfsDev& f) { return f.mark_preds != 0; }
 
 // batched forward visit: all test-and-set atomics of the batch in flight
 // before any result is consumed (see visit_batch in operators.cuh)
@@ -1761,11 +1800,11 @@ class DobfsGraphRunner {
                0u, w.loop_total.ptr, w.loop_tiles.ptr, (uint32_t)max_tiles, nin);
     DobfsDev f{w.su32[0].ptr, w.su32[1].ptr, w.su32[2].ptr, w.su32[3].ptr, ow, 0u, mp, &st->iter};
     // dense pushes (no predecessors): labels and counts from the bitmap diff
-    const DensePush dp{w.loop_total.ptr, mark_preds ? 0ull : dense_push_arcs(), w.su32[2].ptr,
+    const DensePush dp{w.loop_total.ptr, mark_preds ? 0ull : loop_dense_push_arcs(), w.su32[2].ptr,
                        w.aux[4].ptr, w.su32[0].ptr, (uint32_t)nw};
     f.red_total = dp.total;
     f.red_min = dp.min;
-    MGB_LAUNCH((lb_expand_kernel<DobfsDev, true>), num_sms() * 6, kExpBlock, 0, s, f, gv,
+    MGB_LAUNCH((lb_expand_kernel<DobfsDev, true>), (expand_resident<DobfsDev, true>()), kExpBlock, 0, s, f, gv,
                w.loop_front[0].ptr, 0u, w.loop_lb_row.ptr, w.loop_lb_pref.ptr, w.loop_lb_bsum.ptr,
                w.loop_total.ptr, w.loop_tiles.ptr, w.loop_front[1].ptr, &ctr->out_cnt, nin);
     MGB_LAUNCH(dobfs_degsum_end_kernel, num_sms() * 4, 256, 0, s, gv, w.loop_front[1].ptr, ctr,
@@ -2151,7 +2190,7 @@ class DobfsMpGraphRunner {
     const uint64_t max_tiles = (2 * w.ne + 1) / kTile + 2 + kMinTiles;
     MGB_LAUNCH(lb_tiles_kernel, num_sms() * 8, 256, 0, s, w.loop_lb_pref.ptr, w.loop_lb_bsum.ptr,
                0u, w.loop_total.ptr, w.loop_tiles.ptr, (uint32_t)max_tiles, nin);
-    MGB_LAUNCH((lb_expand_kernel<DobfsDev, true>), num_sms() * 6, kExpBlock, 0, s, f, gv, in, 0u,
+    MGB_LAUNCH((lb_expand_kernel<DobfsDev, true>), (expand_resident<DobfsDev, true>()), kExpBlock, 0, s, f, gv, in, 0u,
                w.loop_lb_row.ptr, w.loop_lb_pref.ptr, w.loop_lb_bsum.ptr, w.loop_total.ptr,
                w.loop_tiles.ptr, w.output.ptr, &ctr->out_cnt, nin);
     MGB_CUDA(cudaStreamEndCapture(s, &tmp));

@@ -1,7 +1,8 @@
 """Dense DOBFS push supersteps (DobfsDev::red): fire-and-forget visited-bit ORs,
 labels and the output frontier taken afterwards from vis & ~prev.
 
-The threshold (MG_DOBFS_DENSE_ARCS, host and device-driven loop) is read once
+The thresholds (MG_DOBFS_DENSE_ARCS host loop, MG_DOBFS_LOOP_DENSE_ARCS
+device-driven loop) are read once
 per process, so the forced cases run
 in a child process with every push dense; the parent checks the default
 thresholds.  Labels must equal the oracle's BFS levels; direction log, S, W and
@@ -69,12 +70,12 @@ def _child(env):
 
 @pytest.fixture(scope="module")
 def forced():
-    return _child({"MG_DOBFS_DENSE_ARCS": "1"})
+    return _child({"MG_DOBFS_DENSE_ARCS": "1", "MG_DOBFS_LOOP_DENSE_ARCS": "1"})
 
 
 @pytest.fixture(scope="module")
 def never():
-    return _child({"MG_DOBFS_DENSE_ARCS": "0"})
+    return _child({"MG_DOBFS_DENSE_ARCS": "0", "MG_DOBFS_LOOP_DENSE_ARCS": "0"})
 
 
 def test_dense_push_labels_exact(forced):
