@@ -434,6 +434,9 @@ __global__ void __launch_bounds__(256)
 #ifndef MG_DENSE_LDCA
 #define MG_DENSE_LDCA 0
 #endif
+#ifndef MG_DENSE_NOPROBE
+#define MG_DENSE_NOPROBE 0
+#endif
 struct DobfsDev {
   uint32_t* labels;
   uint32_t* preds;
@@ -459,6 +462,9 @@ struct DobfsDev {
   // and read-only (ld.nc) probes are no faster on RMAT-26 — the probes are
   // spread too widely for L1 reuse.
   __device__ bool prefilter(uint32_t v) const {
+#if MG_DENSE_NOPROBE
+    if (red || red_min) return true;  // experiment: every arc issues its RED
+#endif
 #if MG_DENSE_LDCA
     // a dense push tolerates stale L1 copies (a stale clear bit costs one
     // more RED, a set bit is never stale): hub words stay in L1
@@ -691,6 +697,11 @@ constexpr uint32_t kPullQ = kPullBlock * kPV + MG_PULL_QX;  // CTA queue capacit
 // only rows longer than kPullStart go on to the cooperative stage
 constexpr int kPullMid = MG_PULL_MID;
 static_assert(kPullMid == 8, "stage 1b takes arcs 2-9 from the 32-byte record extension");
+// arc-0 frontier probe issued beside the visited probe (first pull of source
+// 0: 297 -> 284 us under ncu; 8 bench sources 6.816 -> 6.789 ms, same box)
+#ifndef MG_PULL_EAGER_FB
+#define MG_PULL_EAGER_FB 1
+#endif
 #ifndef MG_A1_LAZY
 #define MG_A1_LAZY 1
 #endif
@@ -858,9 +869,19 @@ __global__ void __launch_bounds__(kPullBlock, kPullCtas)
     for (int j = 0; j < kPV; ++j) {
       // a list written by the previous superstep's pull holds only unvisited
       // vertices (no push ran since): no visited probe
+#if MG_PULL_EAGER_FB
+      // the arc-0 frontier probe does not wait for the visited probe: both
+      // depend only on the record (a visited vertex's probe is wasted)
+      const bool valid = pos[j] != kInfLabel;
+      const uint32_t vw = valid && !clean ? __ldcg(&vis[r[j].x >> 5]) : 0u;
+      const uint32_t fw = valid ? __ldg(&fb[r[j].z >> 5]) : 0u;
+      open[j] = valid && !((vw >> (r[j].x & 31)) & 1u);
+      h0[j] = open[j] && ((fw >> (r[j].z & 31)) & 1u);
+#else
       open[j] = pos[j] != kInfLabel &&
                 (clean || !((__ldcg(&vis[r[j].x >> 5]) >> (r[j].x & 31)) & 1u));
       h0[j] = open[j] && bit_set(fb, r[j].z);
+#endif
 #if !MG_A1_LAZY
       h1[j] = open[j] && r[j].y > 1 && bit_set(fb, r[j].w);
 #endif
