@@ -97,6 +97,12 @@ struct BfsDev {
   OwnerView ow;
   uint32_t iter;
   int mark_preds;
+  // dense push (bitmap, no predecessors; as DobfsDev::red): when the
+  // advance's arc count reaches red_min, visits only set visited bits with a
+  // fire-and-forget OR; labels and the output come from vis & ~prev
+  const unsigned long long* red_total = nullptr;
+  unsigned long long red_min = 0;
+  __device__ bool dense() const { return vis && red_min && *red_total >= red_min; }
   // visit: unvisited -> label iter+1 (+pred); the CAS / test-and-set makes the
   // discovery unique (called only for arcs whose prefilter() saw it unvisited)
   __device__ bool visit(uint32_t u, uint32_t v, uint32_t) const {
@@ -144,6 +150,17 @@ __device__ __forceinline__ void visit_batch(const BfsDev& f, const uint32_t* src
     for (int k = 0; k < K; ++k) acc[k] = pass[k] && f.visit(src[k], nb[k], eid[k]);
     return;
   }
+  if (f.dense()) {
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+      if (pass[k])
+        asm volatile("red.relaxed.gpu.global.or.b32 [%0], %1;" ::"l"(&f.vis[nb[k] >> 5]),
+                     "r"(1u << (nb[k] & 31))
+                     : "memory");
+      acc[k] = false;
+    }
+    return;
+  }
   uint32_t old[K];
 #pragma unroll
   for (int k = 0; k < K; ++k)
@@ -157,6 +174,22 @@ __device__ __forceinline__ void visit_batch(const BfsDev& f, const uint32_t* src
     }
   }
 }
+
+__device__ __forceinline__ bool expand_quiet(const BfsDev& f) { return f.dense(); }
+__device__ __forceinline__ bool expand_needs_src(const BfsDev& f) { return f.mark_preds != 0; }
+}  // namespace
+template <>
+struct expand_long_rows<BfsDev> {
+  static constexpr bool value = true;
+};
+namespace {
+
+static unsigned long long dense_push_arcs();
+__global__ void bitmap_diff_list_kernel(const uint32_t* __restrict__ vis, uint32_t* prev,
+                                        uint32_t nw, uint32_t* out, uint32_t* cnt, int set_prev,
+                                        const struct DobfsLoop* st, uint32_t* labels,
+                                        uint32_t level, const unsigned long long* need_total,
+                                        unsigned long long need_min);
 
 struct BfsPrim : PrimBase {
   uint32_t source;
@@ -189,7 +222,28 @@ struct BfsPrim : PrimBase {
     return {w.su32[0].ptr, w.su32[1].ptr, w.su32[2].ptr, bitmap ? w.su32[3].ptr : nullptr,
             c.owner_view(), (uint32_t)c.iter, mark_preds ? 1 : 0};
   }
-  void body(Ctx& c) { c.pipeline(dev(c), c.w->nv); }
+  void body(Ctx& c) {
+    Worker& w = *c.w;
+    if (bitmap && c.fused && !mark_preds && dense_push_arcs() && c.in_count) {
+      // dense when the advance examines >= dense_push_arcs() arcs (DobfsPrim)
+      const uint64_t nw = w.nv / 32 + 1;
+      if (w.su32[2].n < nw || !w.su32[2].ptr) w.su32[2].alloc(nw);  // prev (seen is unused)
+      MGB_CUDA(cudaMemcpyAsync(w.su32[2].ptr, w.su32[3].ptr, 4 * nw, cudaMemcpyDeviceToDevice,
+                               w.stream));
+      const uint32_t nb = (c.in_count + kLbBlock - 1) / kLbBlock;  // lb_advance's total slot
+      if (w.lb_bsum.n < nb + 1ull) w.lb_bsum.alloc(nb + 1ull);
+      BfsDev f = dev(c);
+      f.red_total = w.lb_bsum.ptr + nb;
+      f.red_min = dense_push_arcs();
+      c.pipeline(f, w.nv);
+      MGB_LAUNCH(bitmap_diff_list_kernel, grid_for(nw, 256, num_sms() * 8), 256, 0, w.stream,
+                 w.su32[3].ptr, w.su32[2].ptr, (uint32_t)nw, w.output.ptr, &c.ctr()->out_cnt, 0,
+                 (const DobfsLoop*)nullptr, w.su32[0].ptr, (uint32_t)c.iter + 1, f.red_total,
+                 f.red_min);
+      return;
+    }
+    c.pipeline(dev(c), c.w->nv);
+  }
 };
 
 // ===========================================================================

@@ -121,3 +121,24 @@ def test_dense_push_default_thresholds_rmat16():
         for src in (0, 11):
             r = mg.dobfs(plan, mg.DobfsOptions(source=src), mg.EngineConfig(**cfg))
             assert np.array_equal(r.labels, seq.bfs_levels(off, col, src))
+
+
+def test_dense_bfs_push_rmat22():
+    """single-partition BFS with the visited bitmap (|V| >= 2^22): its big
+    pushes run dense at the default threshold; labels equal the oracle's and
+    S, W and the per-superstep frontier sizes the reference engine's"""
+    plan = mg.PartitionPlan.rmat_device(22, 16, 1)
+    off, col, _ = plan.download_graph().arrays()
+    cfg = mg.EngineConfig(policy=mg.AllocPolicyKind.Maximum, fused=mg.FusedMode.On)
+    rp = None
+    if ref.available():
+        rp = ref.RefPlan(ref.RefGraph.from_csr(off, col), np.zeros(len(off) - 1, np.uint32), 1)
+    for src in (0, 1000):
+        r = mg.bfs(plan, mg.BfsOptions(source=src), cfg)
+        assert np.array_equal(r.labels, seq.bfs_levels(off, col, src))
+        assert r.stats.edges_examined > (1 << 20)  # a dense superstep ran
+        if rp is not None:
+            rr = rp.bfs(src)
+            assert r.stats.supersteps == rr.stats.supersteps
+            assert r.stats.edges_examined == rr.stats.edges_examined
+            assert list(r.stats.out_per_iter) == list(rr.out_per_iter)
