@@ -156,7 +156,7 @@ typedef struct mg_config {
   double factors[MG_NUM_ROLES];   /* sizing factors (FixedPrealloc / PreallocFused) */
   /* DOBFS (any number of partitions) and BFS (single partition): run a
    * logically-forward superstep with the pull kernels when the exact frontier
-   * degree sum exceeds 4x the unvisited list (Beamer's exact cost rule; summed
+   * degree sum exceeds 3x the unvisited list (Beamer's exact cost rule; summed
    * over all partitions so every worker takes the same direction).  The
    * output set is the same; labels, direction log, S and the reported W
    * follow the reference rule (BFS: every superstep forward); the records

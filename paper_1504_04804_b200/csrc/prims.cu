@@ -287,7 +287,7 @@ static unsigned long long loop_dense_push_arcs() {
 static double pull_ratio() {
   static const double r = [] {
     const char* e = getenv("MG_PULL_RATIO");
-    return e ? atof(e) : 4.0;
+    return e ? atof(e) : 3.0;
   }();
   return r;
 }
@@ -753,6 +753,11 @@ constexpr int kPullMid = MG_PULL_MID;
 static_assert(kPullMid == 8, "stage 1b takes arcs 2-9 from the 32-byte record extension");
 // arc-0 frontier probe issued beside the visited probe (first pull of source
 // 0: 297 -> 284 us under ncu; 8 bench sources 6.816 -> 6.789 ms, same box)
+// experiment: the warp's visited-word window computed after the probes are
+// issued (bench sources 6.91 -> 6.89 / 6.99 ms: noise), off
+#ifndef MG_PULL_LATE_WINDOW
+#define MG_PULL_LATE_WINDOW 0
+#endif
 #ifndef MG_PULL_EAGER_FB
 #define MG_PULL_EAGER_FB 1
 #endif
@@ -905,6 +910,7 @@ __global__ void __launch_bounds__(kPullBlock, kPullCtas)
 #pragma unroll
     for (int j = 0; j < kPV; ++j)  // coalesced 16-byte records, kPV in flight, evict-first
       r[j] = pos[j] != kInfLabel ? __ldcs(&rec[pos[j]]) : make_uint4(0, 0, kInfLabel, kInfLabel);
+#if !MG_PULL_LATE_WINDOW
     // the window: bitmap words [w0, w0 + span) hold every vertex of the run
     uint32_t vlo = 0xFFFFFFFFu, vhi = 0u;
 #pragma unroll
@@ -918,6 +924,7 @@ __global__ void __launch_bounds__(kPullBlock, kPullCtas)
     const uint32_t w0 = vlo >> 5;
     const uint32_t span = vlo <= vhi ? (vhi >> 5) - w0 + 1 : 0u;
     const bool inwin = span <= kVisWin;  // warp-uniform
+#endif
     bool open[kPV], h0[kPV], h1[kPV];
 #pragma unroll
     for (int j = 0; j < kPV; ++j) {
@@ -943,6 +950,22 @@ __global__ void __launch_bounds__(kPullBlock, kPullCtas)
 #if MG_A1_LAZY
 #pragma unroll
     for (int j = 0; j < kPV; ++j) h1[j] = open[j] && !h0[j] && r[j].y > 1 && bit_set(fb, r[j].w);
+#endif
+#if MG_PULL_LATE_WINDOW
+    // (after the probes are issued: the warp reductions no longer hold them back)
+    // the window: bitmap words [w0, w0 + span) hold every vertex of the run
+    uint32_t vlo = 0xFFFFFFFFu, vhi = 0u;
+#pragma unroll
+    for (int j = 0; j < kPV; ++j)
+      if (pos[j] != kInfLabel) {
+        vlo = min(vlo, r[j].x);
+        vhi = max(vhi, r[j].x);
+      }
+    vlo = __reduce_min_sync(0xffffffffu, vlo);
+    vhi = __reduce_max_sync(0xffffffffu, vhi);
+    const uint32_t w0 = vlo >> 5;
+    const uint32_t span = vlo <= vhi ? (vhi >> 5) - w0 + 1 : 0u;
+    const bool inwin = span <= kVisWin;  // warp-uniform
 #endif
     bool found[kPV], keep[kPV], lng[kPV];
     uint32_t vv[kPV];
