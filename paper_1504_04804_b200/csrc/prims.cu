@@ -3134,6 +3134,15 @@ struct BcDev {
 
 // a dense forward superstep accepts nothing (output listed afterwards)
 __device__ __forceinline__ bool expand_quiet(const BcDev& f) { return f.red != 0; }
+}  // namespace
+#ifndef MG_BC_LONG_ROWS
+#define MG_BC_LONG_ROWS 0
+#endif
+template <>
+struct expand_long_rows<BcDev> {
+  static constexpr bool value = MG_BC_LONG_ROWS;
+};
+namespace {
 
 // batched forward visit: label loads, then the claiming CASes, then the sigma
 // additions of the whole batch, each group in flight together
