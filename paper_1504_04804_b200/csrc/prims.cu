@@ -272,14 +272,13 @@ static unsigned long long dense_push_arcs() {
   return a;
 }
 
-// The device-driven (exact-cost) loop pushes only below the pull threshold;
-// there the dense form loses (bench sources, same box: off 6.77 ms, 2^20 arcs
-// 6.91, 2^24 6.90 — one hub-source superstep-0 push costs +85 us), so it is
-// off unless MG_DOBFS_LOOP_DENSE_ARCS sets a threshold.
+// The device-driven (exact-cost) loop: dense pushes from 2^20 arcs
+// (MG_DOBFS_LOOP_DENSE_ARCS, 0 = never).  They lost while the end kernel ran
+// 4 CTAs per SM (MG_LOOP_END_CTAS above); at 8 they win (6.89 -> 6.78 ms).
 static unsigned long long loop_dense_push_arcs() {
   static const unsigned long long a = [] {
     const char* e = getenv("MG_DOBFS_LOOP_DENSE_ARCS");
-    return e ? (unsigned long long)atoll(e) : 0ull;
+    return e ? (unsigned long long)atoll(e) : (1ull << 20);
   }();
   return a;
 }
@@ -442,6 +441,13 @@ struct DensePush {
   __device__ bool on() const { return min && *total >= min; }
 };
 
+// CTAs per SM of the push branch's end kernel: its dense branch walks the
+// whole visited bitmap (labels + degree sum of every discovery), and at 4 it
+// made dense pushes lose in the device loop (bench sources: off 6.89-6.95 ms,
+// dense 6.99; at 8: dense 6.77-6.78, off 6.88)
+#ifndef MG_LOOP_END_CTAS
+#define MG_LOOP_END_CTAS 8
+#endif
 // push branch's last kernel: the degree sum of the discoveries, then the end
 __global__ void __launch_bounds__(256)
     dobfs_degsum_end_kernel(GraphView g, const uint32_t* __restrict__ in, Counters* ctr,
@@ -1905,7 +1911,7 @@ class DobfsGraphRunner {
     MGB_LAUNCH((lb_expand_kernel<DobfsDev, true>), (expand_resident<DobfsDev, true>()), kExpBlock, 0, s, f, gv,
                w.loop_front[0].ptr, 0u, w.loop_lb_row.ptr, w.loop_lb_pref.ptr, w.loop_lb_bsum.ptr,
                w.loop_total.ptr, w.loop_tiles.ptr, w.loop_front[1].ptr, &ctr->out_cnt, nin);
-    MGB_LAUNCH(dobfs_degsum_end_kernel, num_sms() * 4, 256, 0, s, gv, w.loop_front[1].ptr, ctr,
+    MGB_LAUNCH(dobfs_degsum_end_kernel, num_sms() * MG_LOOP_END_CTAS, 256, 0, s, gv, w.loop_front[1].ptr, ctr,
                le, dp);
     MGB_CUDA(cudaStreamEndCapture(s, &tmp));
     const uint64_t l2 = g_launches.load();
